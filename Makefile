@@ -1,0 +1,44 @@
+# Build of the product library (CUDA sm_100a + C++ host) and of the test
+# oracles.  `make` builds everything buildable here; the GPU box only needs
+# the prebuilt .so files (they travel with the gpurun snapshot).
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+CC       ?= gcc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2507_03509_b200
+CSRC     := $(PKG)/csrc
+LIB      := $(PKG)/libbpdec.so
+OBJDIR   := build/obj
+
+CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -I$(CSRC) -Iinclude -I/usr/local/cuda/include
+NVFLAGS  := -O3 -std=c++20 $(ARCH) -lineinfo -Xcompiler -fPIC,-Wall -I$(CSRC) -Iinclude \
+            -Xptxas -v
+
+HOST_SRC := $(CSRC)/code.cpp $(CSRC)/c_api.cpp
+HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))
+CU_OBJ   := $(OBJDIR)/decoder.o
+HDRS     := $(wildcard $(CSRC)/*.hpp $(CSRC)/*.cuh) include/bpdec.h
+
+.PHONY: all lib oracle ref clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(CU_OBJ): $(CSRC)/decoder.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/ptxas.log || (cat $(OBJDIR)/ptxas.log; false)
+
+$(LIB): $(HOST_OBJ) $(CU_OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
+
+# oracle/ : CPU restatement (always) + the reference itself (when mounted)
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,183 @@
+/*
+ * bpdec.h — C ABI of the B200-native batched LDPC belief-propagation decoder.
+ *
+ * This is the drop-in boundary for the reconciliation hot path of
+ * arXiv 2507.03509 (reference: /root/reference/proj, library `etdec_core`).
+ * Every entry point below names the reference interface it replaces
+ * (file:line under proj/core/).  The reference exposes a C++ API only; a
+ * C++ caller keeps that API through include/bpdec/etdec_compat.hpp, other
+ * callers (ctypes, cgo, JNI) bind these symbols directly.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross the ABI.
+ *  - Every function returning int returns a bpdec_status; on failure a
+ *    thread-local message is available from bpdec_last_error().
+ *  - Status codes 1/2/3 are the reference's exception classes
+ *    (include/etdec/errors.hpp:8-24: ConfigError / IoError / ValidationError,
+ *    CLI exit codes 1/2/3); 4+ are device errors the CPU reference cannot have.
+ *  - There is no CPU fallback: decoder creation fails with BPDEC_ERR_CUDA when
+ *    no sm_100 device is present.
+ */
+#ifndef BPDEC_H_
+#define BPDEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BPDEC_ABI_VERSION 1
+
+typedef enum {
+  BPDEC_OK = 0,
+  BPDEC_ERR_CONFIG = 1,     /* ≙ etdec::ConfigError     errors.hpp:9-12  */
+  BPDEC_ERR_IO = 2,         /* ≙ etdec::IoError         errors.hpp:15-18 */
+  BPDEC_ERR_VALIDATION = 3, /* ≙ etdec::ValidationError errors.hpp:21-24 */
+  BPDEC_ERR_CUDA = 4,
+  BPDEC_ERR_OOM = 5,
+  BPDEC_ERR_INTERNAL = 6
+} bpdec_status;
+
+/* ≙ etdec::StopReason (decoder.hpp:13-17), same numeric order. */
+typedef enum {
+  BPDEC_STOP_SYNDROME = 0, /* kSyndromeSatisfied: PCE-ET fired          */
+  BPDEC_STOP_VNR = 1,      /* kVnrDrop: q^(k) < q^(k-1), k >= 2 (VNR-ET) */
+  BPDEC_STOP_MAX_ITER = 2  /* kMaxIterations: d_max reached             */
+} bpdec_stop_reason;
+
+/* VNR statistic over the degree>=2 variables (decoder.cpp:32-36).
+ * RAW is the reference formula q = sum posterior (correct in the
+ * all-zero-equivalent frame, i.e. syndrome == NULL / all zero).  ABS is the
+ * x-free reliability q = sum |posterior| for true syndrome-mode decoding,
+ * where the transmitted word is unknown to the decoder. */
+typedef enum { BPDEC_Q_RAW = 0, BPDEC_Q_ABS = 1 } bpdec_q_mode;
+
+/* ≙ etdec::DecodeConfig (decoder.hpp:21-26) plus the q-mode switch. */
+typedef struct {
+  int32_t d_max;     /* iteration budget, > 0                 (default 100)  */
+  int32_t use_pce;   /* syndrome check every iteration        (default 1)    */
+  int32_t use_vnr;   /* q-statistic drop check, from k = 2     (default 0)    */
+  int32_t q_mode;    /* bpdec_q_mode                          (default RAW)  */
+  double msg_clamp;  /* message magnitude bound, > 0          (default 30.0) */
+} bpdec_config;
+
+/* Output flags for bpdec_decode_batch. */
+#define BPDEC_BITS_PACKED 0x1u /* bits_out is uint32 [batch][ceil(N/32)], LSB-first */
+
+typedef struct bpdec_code bpdec_code;       /* immutable host Tanner graph      */
+typedef struct bpdec_decoder bpdec_decoder; /* per-device workspace, one thread */
+
+/* ----------------------------------------------------------------- misc -- */
+int bpdec_abi_version(void);
+const char* bpdec_last_error(void);
+/* ≙ etdec::to_string(StopReason) decoder.cpp:10-17 */
+const char* bpdec_stop_reason_name(int32_t reason);
+
+/* ----------------------------------------------------------- code model -- */
+/* ≙ ParityCheckMatrix::from_check_lists (parity_check_matrix.hpp:16-17,
+ * parity_check_matrix.cpp:10-62): check-major CSR, check_ptr[n_checks+1],
+ * check_vars[check_ptr[n_checks]]; same validation (range, duplicates,
+ * 0 < n_checks < n_vars) and the same ValidationError status. */
+int bpdec_code_from_csr(int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
+                        const int32_t* check_vars, bpdec_code** out);
+/* ≙ load_alist_file / save_alist_file (alist.hpp:21,24; alist.cpp:78-202). */
+int bpdec_code_load_alist(const char* path, bpdec_code** out);
+int bpdec_code_save_alist(const bpdec_code* code, const char* path);
+/* ≙ lift_protograph (protograph.hpp:31, protograph.cpp:52-101); base is a
+ * row-major [rows][cols] multiplicity matrix. */
+int bpdec_code_lift_protograph(const int32_t* base, int32_t rows, int32_t cols, int32_t z,
+                               uint64_t seed, bpdec_code** out);
+/* BASELINE.json multi-edge-style construction (new; not in the reference):
+ * N variables, M checks, the last round(f1*N) variables degree 1 on an
+ * identity block over the last checks, the rest with degrees deg[i] in
+ * proportions prob[i], sockets matched by a seeded permutation. */
+int bpdec_code_generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1,
+                            int32_t n_classes, const int32_t* degrees, const double* probs,
+                            uint64_t seed, bpdec_code** out);
+void bpdec_code_destroy(bpdec_code* code);
+/* n_active = |{v : deg(v) >= 2}| (ActiveVarSet, parity_check_matrix.hpp:66-70) */
+int bpdec_code_dims(const bpdec_code* code, int32_t* n_vars, int32_t* n_checks,
+                    int64_t* n_edges, int32_t* n_active);
+/* copies of the CSR (check_ptr[M+1], check_vars[E]); either may be NULL */
+int bpdec_code_csr(const bpdec_code* code, int32_t* check_ptr, int32_t* check_vars);
+/* ≙ active_var_set (parity_check_matrix.cpp:64-70): ascending, n_active entries */
+int bpdec_code_active_vars(const bpdec_code* code, int32_t* members);
+/* s = H x (packed LSB-first, ceil(M/32) words per frame) for n_frames frames */
+int bpdec_code_syndrome(const bpdec_code* code, int32_t n_frames, const uint8_t* bits,
+                        uint32_t* syndrome_out);
+/* ≙ syndrome_check (decoder.hpp:39, decoder.cpp:19-30) generalised to a
+ * target syndrome (NULL = all zero); *ok = 1 iff H bits == syndrome. */
+int bpdec_syndrome_check(const bpdec_code* code, const uint8_t* bits,
+                         const uint32_t* syndrome, int32_t* ok);
+
+/* -------------------------------------------------------------- channel -- */
+/* ≙ snr_for_beta (channel.hpp:24, channel.cpp:29-42): snr = 2^(2R/beta) - 1 */
+int bpdec_snr_for_beta(double beta, double rate, double* snr);
+/* Seeded syndrome-mode frames (BASELINE.json configs).  For global frame
+ * index f = first_frame + b: x_i ~ Bern(1/2) from a counter hash keyed by
+ * (seed, f, i); g_i = NoiseStream(seed, f).normal(i) (rng.hpp:85-99);
+ * llr_i = float((2/sigma^2) * ((1 - 2 x_i) + sigma * g_i)), which at x = 0
+ * is sample_block (channel.cpp:44-61) rounded to float; s = H x.
+ * all_zero != 0 forces x = 0 (the reference's all-zero codeword).
+ * Outputs: llr [n][N] float, x [n][N] u8 (may be NULL), syndrome
+ * [n][ceil(M/32)] (may be NULL).  Host implementation, threaded. */
+int bpdec_sample_frames(const bpdec_code* code, double snr, uint64_t seed, int64_t first_frame,
+                        int32_t n_frames, int32_t all_zero, float* llr_out, uint8_t* x_out,
+                        uint32_t* syndrome_out);
+
+/* -------------------------------------------------------------- decoder -- */
+/* ≙ BpDecoder::BpDecoder (decoder.hpp:57, decoder.cpp:38-48), batched: a
+ * device replica of the code plus message state for max_slots frames in
+ * flight (rounded up to a multiple of 32).  One decoder per host thread. */
+int bpdec_decoder_create(const bpdec_code* code, int32_t device, int32_t max_slots,
+                         bpdec_decoder** out);
+void bpdec_decoder_destroy(bpdec_decoder* dec);
+int bpdec_decoder_slots(const bpdec_decoder* dec, int32_t* slots);
+/* Device bytes held by the decoder (code replica + message state). */
+int bpdec_decoder_device_bytes(const bpdec_decoder* dec, int64_t* bytes);
+
+/* ≙ BpDecoder::decode (decoder.hpp:64-65, decoder.cpp:50-129), batched over
+ * `batch` independent frames and syndrome-aware.
+ *   llr        [batch][N] float32 channel LLRs (host or device pointer)
+ *   syndrome   [batch][ceil(M/32)] target syndrome, LSB-first; NULL = 0
+ *   cfg        decode configuration (validated like decoder.cpp:56-64)
+ *   flags      BPDEC_BITS_PACKED or 0
+ *   bits_out   [batch][N] u8 hard decisions (1 iff posterior < 0), or
+ *              packed words with BPDEC_BITS_PACKED; may be NULL
+ *   iterations_out [batch] int32; reason_out [batch] u8 (bpdec_stop_reason)
+ *   posteriors_out [batch][N] float (stop-iteration posteriors) or NULL
+ *   q_trace_out    [batch][d_max] double, q^(1..k), rest NaN; or NULL
+ *   stream     cudaStream_t to order the work on (NULL = decoder's own)
+ * Pointers may be host or device memory (detected per pointer).  The call
+ * returns when every frame has terminated and outputs are written.  Frames
+ * beyond the slot count stream through the slots as earlier frames stop. */
+int bpdec_decode_batch(bpdec_decoder* dec, int32_t batch, const float* llr,
+                       const uint32_t* syndrome, const bpdec_config* cfg, uint32_t flags,
+                       void* bits_out, int32_t* iterations_out, uint8_t* reason_out,
+                       float* posteriors_out, double* q_trace_out, void* stream);
+
+/* Device-side frame generator for resident-input benchmarks: same draws as
+ * bpdec_sample_frames, written to DEVICE buffers (llr [n][N], syndrome
+ * [n][ceil(M/32)], x packed [n][ceil(N/32)]; x/syndrome may be NULL). */
+int bpdec_decoder_sample_frames_device(bpdec_decoder* dec, double snr, uint64_t seed,
+                                       int64_t first_frame, int32_t n_frames, int32_t all_zero,
+                                       float* d_llr, uint32_t* d_syndrome, uint32_t* d_x_packed,
+                                       void* stream);
+
+/* Per-kernel timing of the most recent bpdec_decode_batch calls (CUDA events
+ * on the launching stream).  Enable before decoding; kernel ids:
+ * 0 check-node, 1 variable-node, 2 syndrome, 3 termination, 4 load, 5 extract. */
+int bpdec_decoder_set_profiling(bpdec_decoder* dec, int32_t enable);
+int bpdec_decoder_profile(const bpdec_decoder* dec, int32_t kernel, double* total_ms,
+                          int64_t* launches, double* frame_iterations);
+int bpdec_decoder_reset_profile(bpdec_decoder* dec);
+/* Number of kernels launched by this decoder since creation / last reset. */
+int bpdec_decoder_launch_count(const bpdec_decoder* dec, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BPDEC_H_ */

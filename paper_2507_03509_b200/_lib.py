@@ -1,0 +1,90 @@
+"""ctypes binding of the C ABI declared in include/bpdec.h.
+
+The shared library is built in-tree (``make lib`` or ``__graft_entry__.build()``)
+as ``paper_2507_03509_b200/libbpdec.so``.  There is no fallback: importing the
+decoder without the library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbpdec.so")
+
+c_i32p = C.POINTER(C.c_int32)
+c_i64p = C.POINTER(C.c_int64)
+c_u32p = C.POINTER(C.c_uint32)
+c_u8p = C.POINTER(C.c_uint8)
+c_f32p = C.POINTER(C.c_float)
+c_f64p = C.POINTER(C.c_double)
+
+
+class Config(C.Structure):
+    """bpdec_config (≙ etdec::DecodeConfig, decoder.hpp:21-26, plus q_mode)."""
+
+    _fields_ = [
+        ("d_max", C.c_int32),
+        ("use_pce", C.c_int32),
+        ("use_vnr", C.c_int32),
+        ("q_mode", C.c_int32),
+        ("msg_clamp", C.c_double),
+    ]
+
+
+# (name, restype, argtypes) for every symbol in include/bpdec.h
+SIGNATURES = [
+    ("bpdec_abi_version", C.c_int, []),
+    ("bpdec_last_error", C.c_char_p, []),
+    ("bpdec_stop_reason_name", C.c_char_p, [C.c_int32]),
+    ("bpdec_code_from_csr", C.c_int, [C.c_int32, C.c_int32, c_i32p, c_i32p, C.POINTER(C.c_void_p)]),
+    ("bpdec_code_load_alist", C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    ("bpdec_code_save_alist", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("bpdec_code_lift_protograph", C.c_int,
+     [c_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("bpdec_code_generate_met", C.c_int,
+     [C.c_int32, C.c_int32, C.c_double, C.c_int32, c_i32p, c_f64p, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("bpdec_code_destroy", None, [C.c_void_p]),
+    ("bpdec_code_dims", C.c_int, [C.c_void_p, c_i32p, c_i32p, c_i64p, c_i32p]),
+    ("bpdec_code_csr", C.c_int, [C.c_void_p, c_i32p, c_i32p]),
+    ("bpdec_code_active_vars", C.c_int, [C.c_void_p, c_i32p]),
+    ("bpdec_code_syndrome", C.c_int, [C.c_void_p, C.c_int32, c_u8p, c_u32p]),
+    ("bpdec_syndrome_check", C.c_int, [C.c_void_p, c_u8p, c_u32p, c_i32p]),
+    ("bpdec_snr_for_beta", C.c_int, [C.c_double, C.c_double, c_f64p]),
+    ("bpdec_sample_frames", C.c_int,
+     [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, c_f32p, c_u8p, c_u32p]),
+    ("bpdec_decoder_create", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("bpdec_decoder_destroy", None, [C.c_void_p]),
+    ("bpdec_decoder_slots", C.c_int, [C.c_void_p, c_i32p]),
+    ("bpdec_decoder_device_bytes", C.c_int, [C.c_void_p, c_i64p]),
+    ("bpdec_decode_batch", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(Config), C.c_uint32, C.c_void_p,
+      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("bpdec_decoder_sample_frames_device", C.c_int,
+     [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+      C.c_void_p, C.c_void_p]),
+    ("bpdec_decoder_set_profiling", C.c_int, [C.c_void_p, C.c_int32]),
+    ("bpdec_decoder_profile", C.c_int, [C.c_void_p, C.c_int32, c_f64p, c_i64p, c_f64p]),
+    ("bpdec_decoder_reset_profile", C.c_int, [C.c_void_p]),
+    ("bpdec_decoder_launch_count", C.c_int, [C.c_void_p, c_i64p]),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Loads libbpdec.so once; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make lib` (or __graft_entry__.build()); "
+            "the decoder has no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

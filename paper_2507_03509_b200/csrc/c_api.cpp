@@ -1,0 +1,385 @@
+// C ABI (include/bpdec.h).  Every entry point catches C++ exceptions and maps
+// them to bpdec_status codes mirroring the reference's exception classes
+// (errors.hpp:8-24); the message is kept per thread for bpdec_last_error().
+#include "../../include/bpdec.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "code.hpp"
+#include "decoder.hpp"
+#include "rng.hpp"
+
+struct bpdec_code {
+  bpdec::Code code;
+};
+struct bpdec_decoder {
+  bpdec::GpuDecoder* impl = nullptr;
+  int32_t n_vars = 0;
+  int32_t n_checks = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return BPDEC_OK;
+  } catch (const bpdec::ConfigError& e) {
+    g_last_error = e.what();
+    return BPDEC_ERR_CONFIG;
+  } catch (const bpdec::IoError& e) {
+    g_last_error = e.what();
+    return BPDEC_ERR_IO;
+  } catch (const bpdec::ValidationError& e) {
+    g_last_error = e.what();
+    return BPDEC_ERR_VALIDATION;
+  } catch (const bpdec::CudaError& e) {
+    g_last_error = e.what();
+    return BPDEC_ERR_CUDA;
+  } catch (const bpdec::OomError& e) {
+    g_last_error = e.what();
+    return BPDEC_ERR_OOM;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return BPDEC_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return BPDEC_ERR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return BPDEC_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (p == nullptr) throw bpdec::ValidationError(std::string("null pointer: ") + what);
+}
+
+int host_threads() {
+  const unsigned n = std::thread::hardware_concurrency();
+  return n == 0 ? 1 : static_cast<int>(n);
+}
+
+// ≙ snr_for_beta (channel.cpp:29-42).
+double snr_for_beta_impl(double beta, double rate) {
+  if (!(beta > 0.0) || beta > 1.0) {
+    throw bpdec::ValidationError("snr_for_beta: beta must lie in (0,1], got " + std::to_string(beta));
+  }
+  if (!(rate > 0.0) || rate >= 1.0) {
+    throw bpdec::ValidationError("snr_for_beta: rate must lie in (0,1), got " + std::to_string(rate));
+  }
+  return std::exp2(2.0 * rate / beta) - 1.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bpdec_abi_version(void) { return BPDEC_ABI_VERSION; }
+
+const char* bpdec_last_error(void) { return g_last_error.c_str(); }
+
+const char* bpdec_stop_reason_name(int32_t reason) {
+  switch (reason) {
+    case BPDEC_STOP_SYNDROME: return "syndrome_satisfied";
+    case BPDEC_STOP_VNR: return "vnr_drop";
+    case BPDEC_STOP_MAX_ITER: return "max_iterations";
+    default: return "unknown";
+  }
+}
+
+int bpdec_code_from_csr(int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
+                        const int32_t* check_vars, bpdec_code** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto* c = new bpdec_code{bpdec::Code::from_csr(n_vars, n_checks, check_ptr, check_vars)};
+    *out = c;
+  });
+}
+
+int bpdec_code_load_alist(const char* path, bpdec_code** out) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    *out = new bpdec_code{bpdec::load_alist_file(path)};
+  });
+}
+
+int bpdec_code_save_alist(const bpdec_code* code, const char* path) {
+  return guarded([&] {
+    need(code, "code");
+    need(path, "path");
+    bpdec::save_alist_file(code->code, path);
+  });
+}
+
+int bpdec_code_lift_protograph(const int32_t* base, int32_t rows, int32_t cols, int32_t z,
+                               uint64_t seed, bpdec_code** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (rows <= 0 || cols <= 0) throw bpdec::ValidationError("protograph lift: empty base matrix");
+    need(base, "base");
+    std::vector<std::vector<int32_t>> b(rows, std::vector<int32_t>(cols));
+    for (int32_t r = 0; r < rows; ++r)
+      for (int32_t c = 0; c < cols; ++c) b[r][c] = base[static_cast<size_t>(r) * cols + c];
+    *out = new bpdec_code{bpdec::lift_protograph(b, z, seed)};
+  });
+}
+
+int bpdec_code_generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1, int32_t n_classes,
+                            const int32_t* degrees, const double* probs, uint64_t seed,
+                            bpdec_code** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (n_classes <= 0) throw bpdec::ValidationError("met generator: need at least one degree class");
+    need(degrees, "degrees");
+    need(probs, "probs");
+    std::vector<int32_t> d(degrees, degrees + n_classes);
+    std::vector<double> p(probs, probs + n_classes);
+    *out = new bpdec_code{bpdec::generate_met(n_vars, n_checks, frac_deg1, d, p, seed)};
+  });
+}
+
+void bpdec_code_destroy(bpdec_code* code) { delete code; }
+
+int bpdec_code_dims(const bpdec_code* code, int32_t* n_vars, int32_t* n_checks, int64_t* n_edges,
+                    int32_t* n_active) {
+  return guarded([&] {
+    need(code, "code");
+    const auto& h = code->code;
+    if (n_vars) *n_vars = h.n_vars;
+    if (n_checks) *n_checks = h.n_checks;
+    if (n_edges) *n_edges = h.n_edges();
+    if (n_active) {
+      int32_t k = 0;
+      for (int32_t v = 0; v < h.n_vars; ++v) k += h.var_degree(v) >= 2 ? 1 : 0;
+      *n_active = k;
+    }
+  });
+}
+
+int bpdec_code_csr(const bpdec_code* code, int32_t* check_ptr, int32_t* check_vars) {
+  return guarded([&] {
+    need(code, "code");
+    const auto& h = code->code;
+    if (check_ptr) std::copy(h.check_ptr.begin(), h.check_ptr.end(), check_ptr);
+    if (check_vars) std::copy(h.check_vars.begin(), h.check_vars.end(), check_vars);
+  });
+}
+
+int bpdec_code_active_vars(const bpdec_code* code, int32_t* members) {
+  return guarded([&] {
+    need(code, "code");
+    need(members, "members");
+    const auto v = bpdec::active_var_set(code->code);
+    std::copy(v.begin(), v.end(), members);
+  });
+}
+
+int bpdec_code_syndrome(const bpdec_code* code, int32_t n_frames, const uint8_t* bits,
+                        uint32_t* syndrome_out) {
+  return guarded([&] {
+    need(code, "code");
+    if (n_frames < 0) throw bpdec::ValidationError("syndrome: n_frames must be non-negative");
+    if (n_frames == 0) return;
+    need(bits, "bits");
+    need(syndrome_out, "syndrome_out");
+    const auto& h = code->code;
+    const size_t mw = (h.n_checks + 31) / 32;
+    for (int32_t f = 0; f < n_frames; ++f) {
+      bpdec::compute_syndrome(h, bits + static_cast<size_t>(f) * h.n_vars, syndrome_out + f * mw);
+    }
+  });
+}
+
+int bpdec_syndrome_check(const bpdec_code* code, const uint8_t* bits, const uint32_t* syndrome,
+                         int32_t* ok) {
+  return guarded([&] {
+    need(code, "code");
+    need(bits, "bits");
+    need(ok, "ok");
+    const auto& h = code->code;
+    *ok = 1;
+    for (int32_t c = 0; c < h.n_checks; ++c) {
+      uint32_t p = 0;
+      for (int32_t e = h.check_ptr[c]; e < h.check_ptr[c + 1]; ++e) p ^= bits[h.check_vars[e]] & 1u;
+      const uint32_t target = syndrome ? (syndrome[c >> 5] >> (c & 31)) & 1u : 0u;
+      if (p != target) {
+        *ok = 0;
+        return;
+      }
+    }
+  });
+}
+
+int bpdec_snr_for_beta(double beta, double rate, double* snr) {
+  return guarded([&] {
+    need(snr, "snr");
+    *snr = snr_for_beta_impl(beta, rate);
+  });
+}
+
+int bpdec_sample_frames(const bpdec_code* code, double snr, uint64_t seed, int64_t first_frame,
+                        int32_t n_frames, int32_t all_zero, float* llr_out, uint8_t* x_out,
+                        uint32_t* syndrome_out) {
+  return guarded([&] {
+    need(code, "code");
+    if (!(snr > 0.0) || !std::isfinite(snr)) throw bpdec::ValidationError("sample: snr must be positive and finite");
+    if (n_frames < 0) throw bpdec::ValidationError("sample: n_frames must be non-negative");
+    need(llr_out, "llr_out");
+    const auto& h = code->code;
+    const int32_t n = h.n_vars;
+    const size_t mw = (h.n_checks + 31) / 32;
+    // sample_block's arithmetic (channel.cpp:51-58) with the BPSK sign of x.
+    const double sigma2 = 1.0 / snr;
+    const double sigma = std::sqrt(sigma2);
+    const double scale = 2.0 / sigma2;
+    auto work = [&](int32_t b) {
+      const uint64_t f = static_cast<uint64_t>(first_frame + b);
+      const uint64_t nkey = bpdec::stream_key(bpdec::kNoiseDomain, seed, f);
+      const uint64_t xkey = bpdec::stream_key(bpdec::kBitDomain, seed, f);
+      std::vector<uint8_t> x(n);
+      float* l = llr_out + static_cast<size_t>(b) * n;
+      for (int32_t i = 0; i < n; ++i) {
+        double u1, u2;
+        bpdec::noise_uniforms(nkey, static_cast<uint64_t>(i), &u1, &u2);
+        const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+        const unsigned xi = all_zero ? 0u : bpdec::message_bit(xkey, static_cast<uint64_t>(i));
+        x[i] = static_cast<uint8_t>(xi);
+        l[i] = static_cast<float>(scale * ((xi ? -1.0 : 1.0) + sigma * g));
+      }
+      if (x_out) std::copy(x.begin(), x.end(), x_out + static_cast<size_t>(b) * n);
+      if (syndrome_out) bpdec::compute_syndrome(h, x.data(), syndrome_out + b * mw);
+    };
+    const int nt = std::max(1, std::min(host_threads(), n_frames));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) {
+      pool.emplace_back([&, t] {
+        for (int32_t b = t; b < n_frames; b += nt) work(b);
+      });
+    }
+    for (auto& th : pool) th.join();
+  });
+}
+
+int bpdec_decoder_create(const bpdec_code* code, int32_t device, int32_t max_slots,
+                         bpdec_decoder** out) {
+  return guarded([&] {
+    need(code, "code");
+    need(out, "out");
+    auto* d = new bpdec_decoder;
+    try {
+      d->impl = bpdec::gpu_decoder_create(code->code, device, max_slots);
+    } catch (...) {
+      delete d;
+      throw;
+    }
+    d->n_vars = code->code.n_vars;
+    d->n_checks = code->code.n_checks;
+    *out = d;
+  });
+}
+
+void bpdec_decoder_destroy(bpdec_decoder* dec) {
+  if (!dec) return;
+  bpdec::gpu_decoder_destroy(dec->impl);
+  delete dec;
+}
+
+int bpdec_decoder_slots(const bpdec_decoder* dec, int32_t* slots) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(slots, "slots");
+    *slots = bpdec::gpu_decoder_slots(dec->impl);
+  });
+}
+
+int bpdec_decoder_device_bytes(const bpdec_decoder* dec, int64_t* bytes) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(bytes, "bytes");
+    *bytes = bpdec::gpu_decoder_device_bytes(dec->impl);
+  });
+}
+
+int bpdec_decode_batch(bpdec_decoder* dec, int32_t batch, const float* llr, const uint32_t* syndrome,
+                       const bpdec_config* cfg, uint32_t flags, void* bits_out, int32_t* iterations_out,
+                       uint8_t* reason_out, float* posteriors_out, double* q_trace_out, void* stream) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(cfg, "cfg");
+    if (cfg->d_max <= 0) throw bpdec::ValidationError("decode: d_max must be positive");
+    if (!(cfg->msg_clamp > 0.0)) throw bpdec::ValidationError("decode: msg_clamp must be positive");
+    if (cfg->q_mode != BPDEC_Q_RAW && cfg->q_mode != BPDEC_Q_ABS) throw bpdec::ConfigError("decode: unknown q_mode");
+    bpdec::DecodeParams p;
+    p.d_max = cfg->d_max;
+    p.use_pce = cfg->use_pce ? 1 : 0;
+    p.use_vnr = cfg->use_vnr ? 1 : 0;
+    p.q_mode = cfg->q_mode;
+    p.msg_clamp = static_cast<float>(cfg->msg_clamp);
+    bpdec::DecodeBuffers b;
+    b.batch = batch;
+    b.llr = llr;
+    b.syndrome = syndrome;
+    b.bits_packed = (flags & BPDEC_BITS_PACKED) != 0;
+    b.bits = bits_out;
+    b.iterations = iterations_out;
+    b.reasons = reason_out;
+    b.posteriors = posteriors_out;
+    b.q_trace = q_trace_out;
+    bpdec::gpu_decode_batch(dec->impl, p, b, stream);
+  });
+}
+
+int bpdec_decoder_sample_frames_device(bpdec_decoder* dec, double snr, uint64_t seed, int64_t first_frame,
+                                       int32_t n_frames, int32_t all_zero, float* d_llr, uint32_t* d_syndrome,
+                                       uint32_t* d_x_packed, void* stream) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(d_llr, "d_llr");
+    bpdec::gpu_sample_frames_device(dec->impl, snr, seed, first_frame, n_frames, all_zero != 0, d_llr,
+                                    d_syndrome, d_x_packed, stream);
+  });
+}
+
+int bpdec_decoder_set_profiling(bpdec_decoder* dec, int32_t enable) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_set_profiling(dec->impl, enable != 0);
+  });
+}
+
+int bpdec_decoder_profile(const bpdec_decoder* dec, int32_t kernel, double* total_ms, int64_t* launches,
+                          double* frame_iterations) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_profile(dec->impl, kernel, total_ms, launches, frame_iterations);
+  });
+}
+
+int bpdec_decoder_reset_profile(bpdec_decoder* dec) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_reset_profile(dec->impl);
+  });
+}
+
+int bpdec_decoder_launch_count(const bpdec_decoder* dec, int64_t* launches) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(launches, "launches");
+    *launches = bpdec::gpu_launch_count(dec->impl);
+  });
+}
+
+}  // extern "C"

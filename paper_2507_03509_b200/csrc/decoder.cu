@@ -1,0 +1,1024 @@
+// B200 (sm_100a) batched flooding sum-product LDPC decoder with PCE/VNR early
+// termination — the hot path of reference proj/core/src/decoder.cpp:50-129.
+//
+// Layout.  Frames in flight occupy "slots"; 32 slots form a
+// group and every per-item array is stored [group][item][32 lanes], so one
+// warp handles one check (or variable) for 32 frames and every access —
+// including the random Tanner-graph gathers — moves whole 128-byte lines.
+// Variables are split into
+//   H : degree != 1 (degree >= 2 first = the VNR set 𝒱, then degree 0)
+//   D1: degree-1 variables, stored in the order of their (single) check.
+// State per slot: channel LLRs (llr_h, llr_d), the posterior of every
+// degree>=2 variable (post), and the check->variable message of every edge
+// that touches a degree>=2 variable (c2v).  Degree-1 edges keep no message
+// state: their variable->check message is clamp(llr) (the reference's
+// clamp((llr + c2v) - c2v), decoder.cpp:100-104, without the double rounding
+// residue) and their posterior llr + c2v is formed inside the check kernel.
+//
+// One decoding step = one flooding iteration for every active slot:
+//   k_check     check-node update (decoder.cpp:82-96) + degree-1 posteriors,
+//               hard bits and the degree-1 part of the syndrome
+//   k_var       variable-node update (decoder.cpp:99-105) for degree>=2
+//               variables, hard bits, per-tile q partial sums (:32-36, :107)
+//   k_syndrome  bit-sliced parity of every check vs the target syndrome
+//               (decoder.cpp:19-30), 32 frames per 32-bit word
+//   k_terminate PCE -> VNR -> d_max decision per frame (decoder.cpp:114-123)
+//   k_extract   outputs of frames that stopped this step (:126-128)
+//   k_load      streams the next frames into freed slots
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "decoder.hpp"
+#include "phi.cuh"
+#include "rng.hpp"
+
+namespace bpdec {
+
+namespace {
+
+#define CUDA_OK(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t err__ = (expr);                                                              \
+    if (err__ != cudaSuccess) {                                                              \
+      if (err__ == cudaErrorMemoryAllocation) {                                              \
+        (void)cudaGetLastError();                                                            \
+        throw OomError(std::string("CUDA out of memory: ") + #expr);                         \
+      }                                                                                      \
+      throw CudaError(std::string("CUDA error ") + cudaGetErrorString(err__) + " at " + #expr); \
+    }                                                                                        \
+  } while (0)
+
+constexpr int kLanes = 32;
+constexpr int kQTile = 256;     // variables per q partial sum (code-fixed order)
+constexpr int kVarWarps = 8;    // warps per k_var block; kQTile = kVarWarps * 32
+constexpr int kThreads = 256;
+enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kLoad = 4, kExtract = 5, kNumKernels = 6 };
+
+// ------------------------------------------------------------ arguments --
+struct Args {
+  // code
+  int32_t N, M, NH, NV, N1, n_tiles;
+  int64_t EH;
+  const int4* cdesc;        // [M] {hi_begin, hi_end, d1_begin, d1_end}
+  const int32_t* chk_hi_h;  // [EH] H index of each degree>=2 edge, check-major
+  const int32_t* vptr;      // [NV+1]
+  const int32_t* vedge;     // [EH] c2v row of each edge of variable h, ascending check
+  const int32_t* vmap;      // [N] original var -> h (>=0) or -1-d (degree 1)
+  const int32_t* dorig;     // [N] device item (H then D1) -> original var
+  // state
+  int32_t G;
+  float* llr_h;             // [G][NH][32]
+  float* llr_d;             // [G][N1][32]
+  float* post;              // [G][NV][32]
+  float* c2v;               // [G][EH][32]
+  float* d1post;            // [G][N1][32] (only when posteriors are requested)
+  uint32_t* hbits;          // [G][NV]
+  uint32_t* d1bits;         // [G][N1]
+  uint32_t* synp;           // [G][M]  target syndrome ^ degree-1 parity
+  uint32_t* syn_target;     // [G][M]
+  double* q_part;           // [G][n_tiles][32]
+  double* qprev;            // [S]
+  int32_t* slot_iter;       // [S] iteration the slot runs next (1-based)
+  int32_t* slot_frame;      // [S]
+  int32_t* pending_frame;   // [S]
+  uint32_t* group_active;   // [G]
+  uint32_t* fail;           // [G]
+  uint32_t* stopped;        // [G]
+  uint32_t* load_mask;      // [G]
+  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags
+  unsigned long long* frame_iters;
+  // decode parameters
+  int32_t batch, d_max, use_pce, use_vnr, q_mode;
+  float clamp;
+  // inputs / outputs (device)
+  const float* in_llr;        // [batch][N]
+  const uint32_t* in_syn;     // [batch][MW] or null
+  int32_t MW, NW;
+  uint8_t* out_bits_u8;       // [batch][N] or null
+  uint32_t* out_bits_pk;      // [batch][NW] or null
+  int32_t* out_iters;
+  uint8_t* out_reasons;
+  float* out_post;
+  double* out_qtrace;
+};
+
+__device__ __forceinline__ float clampf(float x, float c) { return fminf(fmaxf(x, -c), c); }
+__device__ __forceinline__ uint32_t signbit_u(float x) { return __float_as_uint(x) >> 31; }
+__device__ __forceinline__ float with_sign(float mag, uint32_t s) {
+  return __uint_as_float(__float_as_uint(mag) | (s << 31));
+}
+
+// Streaming loads/stores for the once-per-iteration message traffic; the
+// posterior gathers use the default policy so the [G][NV][32] array stays in
+// L2 between the variable pass that writes it and the check pass that
+// re-reads it ~deg times.
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
+
+// Advances a grid-stride cursor past the remainder of an inactive group.
+__device__ __forceinline__ long long skip_group(long long w, long long per_group, long long stride) {
+  const long long next = (w / per_group + 1) * per_group;
+  const long long k = (next - w + stride - 1) / stride;
+  return w + k * stride;
+}
+
+// ------------------------------------------------------------- k_check --
+// One warp = one check x 32 slots.  MAXD bounds the check degree so the
+// messages and phi values live in registers.
+template <int MAXD, bool WANT_POST>
+__global__ void __launch_bounds__(kThreads) k_check(const Args a) {
+  // Degrees up to 16 are fully unrolled into registers; MAXD = 256 is the
+  // generic path (rolled loops over local-memory arrays).
+  constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
+  if (blockIdx.x == 0 && threadIdx.x < a.G) {
+    a.fail[threadIdx.x] = 0u;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const long long total = static_cast<long long>(a.G) * a.M;
+  for (long long w = warp0; w < total;) {
+    const int g = static_cast<int>(w / a.M);
+    const int c = static_cast<int>(w - static_cast<long long>(g) * a.M);
+    const uint32_t amask = a.group_active[g];
+    if (amask == 0u) {
+      w = skip_group(w, a.M, nwarps);
+      continue;
+    }
+    const bool act = (amask >> lane) & 1u;
+    const int4 d = __ldg(&a.cdesc[c]);
+    const int nh = d.y - d.x;
+    const int deg = nh + (d.w - d.z);
+    const uint32_t sbit = (__ldg(&a.syn_target[static_cast<size_t>(g) * a.M + c]) >> lane) & 1u;
+    uint32_t dpar = 0u;  // parity of degree-1 hard bits (lane bit)
+    if (deg > 0) {
+      const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
+      const bool first = (it == 1);
+      const int lim = MAXD <= 16 ? MAXD : deg;
+      float m[MAXD];
+      float l1[MAXD];
+      uint32_t par = sbit;
+#pragma unroll kUnroll
+      for (int j = 0; j < lim; ++j) {
+        if (j < deg) {
+          float v = 0.0f;
+          if (j < nh) {
+            const int h = __ldg(&a.chk_hi_h[d.x + j]);
+            if (act) {
+              if (first) {
+                v = a.llr_h[(static_cast<size_t>(g) * a.NH + h) * kLanes + lane];
+              } else {
+                const float p = a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
+                const float co = ld_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane]);
+                v = clampf(p - co, a.clamp);
+              }
+            }
+          } else {
+            const int dd = d.z + (j - nh);
+            if (act) {
+              const float l = ld_stream(&a.llr_d[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane]);
+              l1[j] = l;
+              v = first ? l : clampf(l, a.clamp);
+            } else {
+              l1[j] = 0.0f;
+            }
+          }
+          m[j] = v;
+          par ^= signbit_u(v);
+        }
+      }
+      float out[MAXD];
+      if (deg == 1) {
+        out[0] = a.clamp;  // empty product: atanh(1) = inf -> clamp
+      } else if (deg == 2) {
+        out[0] = fminf(fabsf(m[1]), a.clamp);  // phi(phi(x)) = x
+        out[1] = fminf(fabsf(m[0]), a.clamp);
+      } else {
+        float ph[MAXD];
+        float pre[MAXD];
+        float run = 0.0f;
+#pragma unroll kUnroll
+        for (int j = 0; j < lim; ++j) {
+          if (j < deg) {
+            ph[j] = dev::phi(fabsf(m[j]));
+            pre[j] = run;
+            run += ph[j];
+          }
+        }
+        float suf = 0.0f;
+#pragma unroll kUnroll
+        for (int j = lim - 1; j >= 0; --j) {
+          if (j < deg) {
+            out[j] = fminf(dev::phi(pre[j] + suf), a.clamp);
+            suf += ph[j];
+          }
+        }
+      }
+#pragma unroll kUnroll
+      for (int j = 0; j < lim; ++j) {
+        if (j < deg) {
+          const float o = with_sign(out[j], par ^ signbit_u(m[j]));
+          if (j < nh) {
+            if (act) st_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane], o);
+          } else {
+            const int dd = d.z + (j - nh);
+            const float pd = l1[j] + o;  // posterior of the degree-1 variable
+            const uint32_t bit = (act && pd < 0.0f) ? 1u : 0u;
+            dpar ^= bit;
+            const uint32_t word = __ballot_sync(0xffffffffu, bit);
+            if (lane == 0) a.d1bits[static_cast<size_t>(g) * a.N1 + dd] = word;
+            if (WANT_POST && act) a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane] = pd;
+          }
+        }
+      }
+    }
+    const uint32_t sw = __ballot_sync(0xffffffffu, (sbit ^ dpar) & 1u);
+    if (lane == 0) a.synp[static_cast<size_t>(g) * a.M + c] = sw;
+    w += nwarps;
+  }
+}
+
+// --------------------------------------------------------------- k_var --
+// One block = one tile of kQTile consecutive degree>=2 variables x 32 slots;
+// warp k handles variables tile*256 + k*32 + (0..31) in order, and the tile's
+// q partial is the warp partials summed in warp order: a summation order that
+// depends on the code only (not on slots, batch size or GPU count).
+template <int QMODE>
+__global__ void __launch_bounds__(kThreads) k_var(const Args a) {
+  __shared__ double red[kVarWarps][kLanes];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const long long total = static_cast<long long>(a.G) * a.n_tiles;
+  for (long long w = blockIdx.x; w < total;) {
+    const int g = static_cast<int>(w / a.n_tiles);
+    const int tile = static_cast<int>(w - static_cast<long long>(g) * a.n_tiles);
+    const uint32_t amask = a.group_active[g];
+    if (amask == 0u) {
+      w = skip_group(w, a.n_tiles, gridDim.x);
+      continue;
+    }
+    const bool act = (amask >> lane) & 1u;
+    double acc = 0.0;
+    const int h0 = tile * kQTile + warp * kLanes;
+    const int h1 = min(h0 + kLanes, a.NV);
+    const size_t gl = static_cast<size_t>(g) * a.NH;
+    const size_t gv = static_cast<size_t>(g) * a.NV;
+    const size_t ge = static_cast<size_t>(g) * a.EH;
+    for (int h = h0; h < h1; ++h) {
+      float p = 0.0f;
+      const int k0 = __ldg(&a.vptr[h]);
+      const int k1 = __ldg(&a.vptr[h + 1]);
+      if (act) {
+        p = ld_stream(&a.llr_h[(gl + h) * kLanes + lane]);
+        for (int k = k0; k < k1; ++k) {
+          p += ld_stream(&a.c2v[(ge + __ldg(&a.vedge[k])) * kLanes + lane]);
+        }
+        a.post[(gv + h) * kLanes + lane] = p;
+        acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
+      if (lane == 0) a.hbits[gv + h] = word;
+    }
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      double q = red[0][lane];
+#pragma unroll
+      for (int k = 1; k < kVarWarps; ++k) q += red[k][lane];
+      a.q_part[(static_cast<size_t>(g) * a.n_tiles + tile) * kLanes + lane] = q;
+    }
+    __syncthreads();
+    w += gridDim.x;
+  }
+}
+
+// ---------------------------------------------------------- k_syndrome --
+// Thread = one check x 32 slots (bit-sliced); checks padded to a multiple of
+// 32 per group so a warp never straddles two groups.
+__global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
+  const int lane = threadIdx.x & 31;
+  const long long mpad = (static_cast<long long>(a.M) + 31) / 32 * 32;
+  const long long total = static_cast<long long>(a.G) * mpad;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long w = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < total;) {
+    const int g = static_cast<int>(w / mpad);
+    const int c = static_cast<int>(w - g * mpad);
+    const uint32_t amask = a.group_active[g];
+    const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]);
+    if (amask == 0u || (fl & amask) == amask) {  // nothing left to learn in this group
+      w = skip_group(w, mpad, stride);
+      continue;
+    }
+    uint32_t word = 0u;
+    if (c < a.M) {
+      word = a.synp[static_cast<size_t>(g) * a.M + c];
+      const int4 d = __ldg(&a.cdesc[c]);
+      for (int e = d.x; e < d.y; ++e) word ^= a.hbits[static_cast<size_t>(g) * a.NV + __ldg(&a.chk_hi_h[e])];
+      word &= amask;
+    }
+    word = __reduce_or_sync(0xffffffffu, word);
+    if (lane == 0 && word != 0u && (fl & word) != word) atomicOr(&a.fail[g], word);
+    w += stride;
+  }
+}
+
+// --------------------------------------------------------- k_terminate --
+// Warp = one slot.  q^(k) = fixed-order double sum of the tile partials;
+// decision order PCE, then VNR (k >= 2, strict), then d_max
+// (decoder.cpp:114-123).
+__global__ void __launch_bounds__(kThreads) k_terminate(const Args a) {
+  const int lane = threadIdx.x & 31;
+  const int s = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (s >= a.G * kLanes) return;
+  const int g = s >> 5, l = s & 31;
+  const uint32_t bit = 1u << l;
+  if (!(a.group_active[g] & bit)) return;
+  double q = 0.0;
+  for (int t = lane; t < a.n_tiles; t += kLanes) q += a.q_part[(static_cast<size_t>(g) * a.n_tiles + t) * kLanes + l];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+  if (lane != 0) return;
+  const int it = a.slot_iter[s];
+  const int f = a.slot_frame[s];
+  atomicAdd(a.frame_iters, 1ull);
+  if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (it - 1)] = q;
+  int reason = -1;
+  if (a.use_pce && !(a.fail[g] & bit)) {
+    reason = 0;
+  } else if (a.use_vnr && it >= 2 && q < a.qprev[s]) {
+    reason = 1;
+  } else if (it >= a.d_max) {
+    reason = 2;
+  }
+  if (reason < 0) {
+    a.slot_iter[s] = it + 1;
+    a.qprev[s] = q;
+    return;
+  }
+  a.out_iters[f] = it;
+  a.out_reasons[f] = static_cast<uint8_t>(reason);
+  atomicAnd(&a.group_active[g], ~bit);
+  atomicOr(&a.stopped[g], bit);
+  atomicAdd(&a.counters[1], 1);
+  const int nf = atomicAdd(&a.counters[0], 1);
+  if (nf < a.batch) {
+    a.pending_frame[s] = nf;
+    atomicOr(&a.load_mask[g], bit);
+  }
+}
+
+// ----------------------------------------------------------- k_extract --
+// Outputs (hard bits, posteriors) of the frames that stopped this step, in
+// the original variable order.  Thread = one variable; a warp covers 32
+// consecutive variables so packed bit words come from one ballot.
+template <bool WANT_POST>
+__global__ void __launch_bounds__(kThreads) k_extract(const Args a) {
+  const int lane = threadIdx.x & 31;
+  const long long npad = (static_cast<long long>(a.N) + 31) / 32 * 32;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (int g = 0; g < a.G; ++g) {
+    uint32_t sm = a.stopped[g];
+    while (sm) {
+      const int l = __ffs(sm) - 1;
+      sm &= sm - 1;
+      const int f = a.slot_frame[g * kLanes + l];
+      for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < npad; i += stride) {
+        uint32_t bit = 0u;
+        float pv = 0.0f;
+        if (i < a.N) {
+          const int vm = __ldg(&a.vmap[i]);
+          if (vm >= 0) {
+            if (vm < a.NV) {
+              bit = (a.hbits[static_cast<size_t>(g) * a.NV + vm] >> l) & 1u;
+              if (WANT_POST) pv = a.post[(static_cast<size_t>(g) * a.NV + vm) * kLanes + l];
+            } else {  // degree-0 variable: posterior = channel LLR
+              pv = a.llr_h[(static_cast<size_t>(g) * a.NH + vm) * kLanes + l];
+              bit = pv < 0.0f ? 1u : 0u;
+            }
+          } else {
+            const int dd = -1 - vm;
+            bit = (a.d1bits[static_cast<size_t>(g) * a.N1 + dd] >> l) & 1u;
+            if (WANT_POST) pv = a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + l];
+          }
+          if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
+          if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
+        }
+        if (a.out_bits_pk) {
+          const uint32_t word = __ballot_sync(0xffffffffu, bit);
+          if (lane == 0) a.out_bits_pk[static_cast<size_t>(f) * a.NW + (i >> 5)] = word;
+        }
+      }
+    }
+  }
+}
+
+// -------------------------------------------------------------- k_load --
+// Streams frames into the slots flagged in load_mask: LLR transpose
+// [frame][var] -> [group][item][lane] through shared memory, target syndrome
+// bits, slot state.  Grid: (item tiles of 32) + (check tiles) + 1 state block.
+__global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks, int check_blocks) {
+  __shared__ float tile[32][33];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int b = blockIdx.x;
+  if (b < item_blocks) {
+    const int n_tiles_items = (a.N + 31) / 32;
+    for (long long w = b; w < static_cast<long long>(a.G) * n_tiles_items; w += item_blocks) {
+      const int g = static_cast<int>(w / n_tiles_items);
+      const int it0 = static_cast<int>(w - static_cast<long long>(g) * n_tiles_items) * 32;
+      const uint32_t lm = a.load_mask[g];
+      if (lm == 0u) continue;
+      // read: warp = slot lane r, lanes = consecutive items
+      for (int r = warp; r < 32; r += kThreads / 32) {
+        if (!((lm >> r) & 1u)) continue;
+        const int f = a.pending_frame[g * kLanes + r];
+        const int item = it0 + lane;
+        float v = 0.0f;
+        if (item < a.N) {
+          v = a.in_llr[static_cast<size_t>(f) * a.N + __ldg(&a.dorig[item])];
+          if (!isfinite(v)) atomicOr(&a.counters[2], 1);
+        }
+        tile[lane][r] = v;
+      }
+      __syncthreads();
+      for (int j = warp; j < 32; j += kThreads / 32) {
+        const int item = it0 + j;
+        if (item < a.N && ((lm >> lane) & 1u)) {
+          const float v = tile[j][lane];
+          if (item < a.NH) {
+            a.llr_h[(static_cast<size_t>(g) * a.NH + item) * kLanes + lane] = v;
+          } else {
+            a.llr_d[(static_cast<size_t>(g) * a.N1 + (item - a.NH)) * kLanes + lane] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  } else if (b < item_blocks + check_blocks) {
+    const long long total = static_cast<long long>(a.G) * a.M;
+    const long long stride = static_cast<long long>(check_blocks) * blockDim.x;
+    for (long long w = static_cast<long long>(b - item_blocks) * blockDim.x + threadIdx.x; w < total; w += stride) {
+      const int g = static_cast<int>(w / a.M);
+      const int c = static_cast<int>(w - static_cast<long long>(g) * a.M);
+      uint32_t lm = a.load_mask[g];
+      if (lm == 0u) continue;
+      uint32_t word = a.syn_target[w] & ~lm;
+      if (a.in_syn) {
+        while (lm) {
+          const int r = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const int f = a.pending_frame[g * kLanes + r];
+          word |= ((__ldg(&a.in_syn[static_cast<size_t>(f) * a.MW + (c >> 5)]) >> (c & 31)) & 1u) << r;
+        }
+      }
+      a.syn_target[w] = word;
+    }
+  } else {
+    for (int s = threadIdx.x; s < a.G * kLanes; s += blockDim.x) {
+      const int g = s >> 5;
+      const uint32_t bit = 1u << (s & 31);
+      if (a.load_mask[g] & bit) {
+        a.slot_frame[s] = a.pending_frame[s];
+        a.slot_iter[s] = 1;
+        a.qprev[s] = 0.0;
+        atomicOr(&a.group_active[g], bit);
+      }
+    }
+  }
+}
+
+// Clears the per-step masks consumed by k_extract / k_load.
+__global__ void k_step_end(const Args a) {
+  for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
+    a.stopped[g] = 0u;
+    a.load_mask[g] = 0u;
+  }
+}
+
+// ---------------------------------------------------------- generators --
+// Syndrome-mode frames on device; same draws as bpdec_sample_frames
+// (channel.cpp:44-61 with the message bit x and s = Hx on top).
+__global__ void k_gen_llr(int32_t N, int32_t NW, double snr, uint64_t seed, int64_t first_frame,
+                          int32_t n_frames, int32_t all_zero, float* llr, uint32_t* xpk) {
+  const double sigma2 = 1.0 / snr;
+  const double sigma = sqrt(sigma2);
+  const double scale = 2.0 / sigma2;
+  const long long npad = (static_cast<long long>(N) + 31) / 32 * 32;
+  const long long total = npad * n_frames;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int b = static_cast<int>(t / npad);
+    const long long i = t - static_cast<long long>(b) * npad;
+    const uint64_t f = static_cast<uint64_t>(first_frame + b);
+    unsigned x = 0;
+    if (i < N) {
+      const uint64_t nkey = stream_key(kNoiseDomain, seed, f);
+      double u1, u2;
+      noise_uniforms(nkey, static_cast<uint64_t>(i), &u1, &u2);
+      const double gval = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+      x = all_zero ? 0u : message_bit(stream_key(kBitDomain, seed, f), static_cast<uint64_t>(i));
+      const double y = (x ? -1.0 : 1.0) + sigma * gval;
+      llr[static_cast<size_t>(b) * N + i] = static_cast<float>(scale * y);
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, x);
+    if (xpk && (threadIdx.x & 31) == 0) xpk[static_cast<size_t>(b) * NW + (i >> 5)] = word;
+  }
+}
+
+// s = H x from packed x (thread = 32 checks of one frame -> one word).
+__global__ void k_gen_syndrome(const Args a, int32_t n_frames, const uint32_t* xpk, uint32_t* syn,
+                               const int32_t* check_ptr, const int32_t* check_vars) {
+  const long long total = static_cast<long long>(n_frames) * a.MW;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int b = static_cast<int>(t / a.MW);
+    const int wd = static_cast<int>(t - static_cast<long long>(b) * a.MW);
+    uint32_t word = 0u;
+    for (int c = wd * 32; c < min(a.M, wd * 32 + 32); ++c) {
+      uint32_t p = 0u;
+      for (int e = check_ptr[c]; e < check_ptr[c + 1]; ++e) {
+        const int v = check_vars[e];
+        p ^= (xpk[static_cast<size_t>(b) * a.NW + (v >> 5)] >> (v & 31)) & 1u;
+      }
+      word |= p << (c & 31);
+    }
+    syn[static_cast<size_t>(b) * a.MW + wd] = word;
+  }
+}
+
+template <typename T>
+T* dalloc(size_t count, int64_t* bytes) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+  *bytes += static_cast<int64_t>(count * sizeof(T));
+  return p;
+}
+
+bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// Device scratch that grows on demand.
+struct Scratch {
+  void* ptr = nullptr;
+  size_t size = 0;
+  void* get(size_t n) {
+    if (n <= size) return ptr;
+    if (ptr) CUDA_OK(cudaFree(ptr));
+    ptr = nullptr;
+    size = 0;
+    CUDA_OK(cudaMalloc(&ptr, n));
+    size = n;
+    return ptr;
+  }
+  ~Scratch() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+}  // namespace
+
+// -------------------------------------------------------- GpuDecoder --
+class GpuDecoder {
+ public:
+  GpuDecoder(const Code& code, int device, int max_slots);
+  ~GpuDecoder();
+  void decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t stream);
+  void sample_device(double snr, uint64_t seed, int64_t first_frame, int32_t n_frames, bool all_zero,
+                     float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t stream);
+
+  int S = 0;
+  int G = 0;
+  int device = 0;
+  int64_t dev_bytes = 0;
+  bool profiling = false;
+  double prof_ms[kNumKernels] = {};
+  int64_t prof_launches[kNumKernels] = {};
+  double prof_frame_iters = 0.0;
+  int64_t launches = 0;
+
+ private:
+  template <typename F>
+  void launch(int kid, cudaStream_t st, F&& f);
+  void run_step(const Args& a, cudaStream_t st, bool want_post);
+
+  Args base{};
+  int32_t max_check_deg = 0;
+  int32_t* d_check_ptr = nullptr;
+  int32_t* d_check_vars = nullptr;
+  std::vector<void*> owned;
+  cudaStream_t own_stream = nullptr;
+  int32_t* h_counters = nullptr;  // pinned ring [kRing][4]
+  static constexpr int kRing = 8;
+  cudaEvent_t ring_ev[kRing] = {};
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<int> prof_kid;
+  Scratch s_llr, s_syn, s_bits, s_iters, s_reasons, s_post, s_qtrace;
+  int grid_check = 0, grid_var = 0, grid_syn = 0, grid_extract = 0;
+  int load_item_blocks = 0, load_check_blocks = 0;
+};
+
+GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    (void)cudaGetLastError();
+    throw CudaError("no CUDA device available (the decoder has no CPU fallback)");
+  }
+  if (dev < 0 || dev >= count) throw ConfigError("device index out of range");
+  CUDA_OK(cudaSetDevice(dev));
+  cudaDeviceProp prop{};
+  CUDA_OK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10) {
+    throw CudaError(std::string("device ") + prop.name + " is not sm_100-class; this build targets sm_100a only");
+  }
+  if (max_slots < 1) throw ValidationError("decoder: max_slots must be positive");
+  S = (max_slots + 31) / 32 * 32;
+  G = S / 32;
+
+  // ---- device code layout
+  const int32_t N = code.n_vars, M = code.n_checks;
+  std::vector<int32_t> deg(N);
+  for (int32_t v = 0; v < N; ++v) deg[v] = code.var_degree(v);
+  std::vector<int32_t> horig;
+  for (int32_t v = 0; v < N; ++v)
+    if (deg[v] >= 2) horig.push_back(v);
+  const int32_t NV = static_cast<int32_t>(horig.size());
+  for (int32_t v = 0; v < N; ++v)
+    if (deg[v] == 0) horig.push_back(v);
+  const int32_t NH = static_cast<int32_t>(horig.size());
+  std::vector<int32_t> vmap(N, 0);
+  for (int32_t h = 0; h < NH; ++h) vmap[horig[h]] = h;
+  std::vector<int4> cdesc(M);
+  std::vector<int32_t> chk_hi_h, dorig(horig), hi_of_edge(code.n_edges(), -1);
+  int32_t n1 = 0;
+  for (int32_t c = 0; c < M; ++c) {
+    max_check_deg = std::max(max_check_deg, code.check_degree(c));
+    int4 d;
+    d.x = static_cast<int32_t>(chk_hi_h.size());
+    for (int32_t e = code.check_ptr[c]; e < code.check_ptr[c + 1]; ++e) {
+      const int32_t v = code.check_vars[e];
+      if (deg[v] >= 2) {
+        hi_of_edge[e] = static_cast<int32_t>(chk_hi_h.size());
+        chk_hi_h.push_back(vmap[v]);
+      }
+    }
+    d.y = static_cast<int32_t>(chk_hi_h.size());
+    d.z = n1;
+    for (int32_t e = code.check_ptr[c]; e < code.check_ptr[c + 1]; ++e) {
+      const int32_t v = code.check_vars[e];
+      if (deg[v] == 1) {
+        vmap[v] = -1 - n1;
+        dorig.push_back(v);
+        ++n1;
+      }
+    }
+    d.w = n1;
+    cdesc[c] = d;
+  }
+  if (max_check_deg > 256) throw ValidationError("decoder: check degree above 256 is not supported");
+  const int64_t EH = static_cast<int64_t>(chk_hi_h.size());
+  std::vector<int32_t> vptr(NV + 1, 0), vedge;
+  vedge.reserve(EH);
+  for (int32_t h = 0; h < NV; ++h) {
+    const int32_t v = horig[h];
+    for (int32_t k = code.var_ptr[v]; k < code.var_ptr[v + 1]; ++k) vedge.push_back(hi_of_edge[code.var_edges[k]]);
+    vptr[h + 1] = static_cast<int32_t>(vedge.size());
+  }
+
+  Args& a = base;
+  a.N = N;
+  a.M = M;
+  a.NH = NH;
+  a.NV = NV;
+  a.N1 = n1;
+  a.EH = EH;
+  a.n_tiles = std::max(1, (NV + kQTile - 1) / kQTile);
+  a.G = G;
+  a.MW = (M + 31) / 32;
+  a.NW = (N + 31) / 32;
+  auto up = [&](const auto& vec, auto* dptr) {
+    using T = std::remove_pointer_t<decltype(dptr)>;
+    T* p = dalloc<T>(vec.size(), &dev_bytes);
+    owned.push_back(p);
+    if (!vec.empty()) CUDA_OK(cudaMemcpy(p, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  };
+  a.cdesc = up(cdesc, static_cast<int4*>(nullptr));
+  a.chk_hi_h = up(chk_hi_h, static_cast<int32_t*>(nullptr));
+  a.vptr = up(vptr, static_cast<int32_t*>(nullptr));
+  a.vedge = up(vedge, static_cast<int32_t*>(nullptr));
+  a.vmap = up(vmap, static_cast<int32_t*>(nullptr));
+  a.dorig = up(dorig, static_cast<int32_t*>(nullptr));
+  d_check_ptr = up(code.check_ptr, static_cast<int32_t*>(nullptr));
+  d_check_vars = up(code.check_vars, static_cast<int32_t*>(nullptr));
+
+  auto own = [&](auto* p) {
+    owned.push_back(p);
+    return p;
+  };
+  const size_t L = kLanes;
+  a.llr_h = own(dalloc<float>(static_cast<size_t>(G) * NH * L, &dev_bytes));
+  a.llr_d = own(dalloc<float>(static_cast<size_t>(G) * n1 * L, &dev_bytes));
+  a.post = own(dalloc<float>(static_cast<size_t>(G) * NV * L, &dev_bytes));
+  a.c2v = own(dalloc<float>(static_cast<size_t>(G) * EH * L, &dev_bytes));
+  a.d1post = nullptr;  // allocated on first request
+  a.hbits = own(dalloc<uint32_t>(static_cast<size_t>(G) * NV, &dev_bytes));
+  a.d1bits = own(dalloc<uint32_t>(static_cast<size_t>(G) * n1, &dev_bytes));
+  a.synp = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
+  a.syn_target = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
+  a.q_part = own(dalloc<double>(static_cast<size_t>(G) * a.n_tiles * L, &dev_bytes));
+  a.qprev = own(dalloc<double>(S, &dev_bytes));
+  a.slot_iter = own(dalloc<int32_t>(S, &dev_bytes));
+  a.slot_frame = own(dalloc<int32_t>(S, &dev_bytes));
+  a.pending_frame = own(dalloc<int32_t>(S, &dev_bytes));
+  a.group_active = own(dalloc<uint32_t>(G, &dev_bytes));
+  a.fail = own(dalloc<uint32_t>(G, &dev_bytes));
+  a.stopped = own(dalloc<uint32_t>(G, &dev_bytes));
+  a.load_mask = own(dalloc<uint32_t>(G, &dev_bytes));
+  a.counters = own(dalloc<int32_t>(4, &dev_bytes));
+  a.frame_iters = own(dalloc<unsigned long long>(1, &dev_bytes));
+  CUDA_OK(cudaMemset(a.group_active, 0, G * sizeof(uint32_t)));
+  CUDA_OK(cudaMemset(a.stopped, 0, G * sizeof(uint32_t)));
+  CUDA_OK(cudaMemset(a.load_mask, 0, G * sizeof(uint32_t)));
+  CUDA_OK(cudaMemset(a.syn_target, 0, static_cast<size_t>(G) * M * sizeof(uint32_t)));
+
+  CUDA_OK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaHostAlloc(&h_counters, kRing * 4 * sizeof(int32_t), cudaHostAllocDefault));
+  for (auto& e : ring_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+  const int sms = prop.multiProcessorCount;
+  grid_check = sms * 8;
+  grid_var = sms * 8;
+  grid_syn = sms * 8;
+  grid_extract = sms * 4;
+  load_item_blocks = sms * 4;
+  load_check_blocks = sms * 2;
+}
+
+GpuDecoder::~GpuDecoder() {
+  cudaSetDevice(device);
+  for (void* p : owned) cudaFree(p);
+  if (base.d1post) cudaFree(base.d1post);
+  for (auto& e : ring_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : prof_ev) cudaEventDestroy(e);
+  if (h_counters) cudaFreeHost(h_counters);
+  if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+template <typename F>
+void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (profiling) {
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    CUDA_OK(cudaEventRecord(e0, st));
+  }
+  f();
+  CUDA_OK(cudaGetLastError());
+  ++launches;
+  if (profiling) {
+    CUDA_OK(cudaEventRecord(e1, st));
+    prof_ev.push_back(e0);
+    prof_ev.push_back(e1);
+    prof_kid.push_back(kid);
+  }
+}
+
+void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
+  const int md = max_check_deg;
+  launch(kCheck, st, [&] {
+#define BPDEC_CHECK_CASE(D)                                                                 \
+  if (md <= D) {                                                                            \
+    if (want_post)                                                                          \
+      k_check<D, true><<<grid_check, kThreads, 0, st>>>(a);                                 \
+    else                                                                                    \
+      k_check<D, false><<<grid_check, kThreads, 0, st>>>(a);                                \
+    return;                                                                                 \
+  }
+    BPDEC_CHECK_CASE(3)
+    BPDEC_CHECK_CASE(4)
+    BPDEC_CHECK_CASE(6)
+    BPDEC_CHECK_CASE(8)
+    BPDEC_CHECK_CASE(16)
+    BPDEC_CHECK_CASE(256)
+#undef BPDEC_CHECK_CASE
+  });
+  launch(kVar, st, [&] {
+    if (a.q_mode == 0)
+      k_var<0><<<grid_var, kThreads, 0, st>>>(a);
+    else
+      k_var<1><<<grid_var, kThreads, 0, st>>>(a);
+  });
+  if (a.use_pce) launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 0, st>>>(a); });
+  launch(kTerm, st, [&] { k_terminate<<<(G * kLanes * 32 + kThreads - 1) / kThreads, kThreads, 0, st>>>(a); });
+  launch(kExtract, st, [&] {
+    if (want_post)
+      k_extract<true><<<grid_extract, kThreads, 0, st>>>(a);
+    else
+      k_extract<false><<<grid_extract, kThreads, 0, st>>>(a);
+  });
+  launch(kLoad, st, [&] {
+    k_load<<<load_item_blocks + load_check_blocks + 1, kThreads, 0, st>>>(a, load_item_blocks, load_check_blocks);
+  });
+  k_step_end<<<1, 32, 0, st>>>(a);
+  CUDA_OK(cudaGetLastError());
+  ++launches;
+}
+
+void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t st_in) {
+  CUDA_OK(cudaSetDevice(device));
+  const cudaStream_t st = st_in ? st_in : own_stream;
+  if (p.d_max <= 0) throw ValidationError("decode: d_max must be positive");
+  if (!(p.msg_clamp > 0.0f)) throw ValidationError("decode: msg_clamp must be positive");
+  if (b.batch < 0) throw ValidationError("decode: batch must be non-negative");
+  if (b.batch == 0) return;
+  if (b.llr == nullptr) throw ValidationError("decode: null LLR pointer");
+  if (b.iterations == nullptr || b.reasons == nullptr) throw ValidationError("decode: iterations/reason outputs are required");
+  Args a = base;
+  const size_t B = static_cast<size_t>(b.batch);
+  const bool want_post = b.posteriors != nullptr;
+  if (want_post && a.d1post == nullptr) {
+    a.d1post = dalloc<float>(static_cast<size_t>(G) * a.N1 * kLanes, &dev_bytes);
+    base.d1post = a.d1post;
+  }
+  a.batch = b.batch;
+  a.d_max = p.d_max;
+  a.use_pce = p.use_pce;
+  a.use_vnr = p.use_vnr;
+  a.q_mode = p.q_mode;
+  a.clamp = p.msg_clamp;
+
+  // inputs
+  if (is_device_ptr(b.llr)) {
+    a.in_llr = b.llr;
+  } else {
+    float* d = static_cast<float*>(s_llr.get(B * a.N * sizeof(float)));
+    CUDA_OK(cudaMemcpyAsync(d, b.llr, B * a.N * sizeof(float), cudaMemcpyHostToDevice, st));
+    a.in_llr = d;
+  }
+  a.in_syn = nullptr;
+  if (b.syndrome) {
+    if (is_device_ptr(b.syndrome)) {
+      a.in_syn = b.syndrome;
+    } else {
+      uint32_t* d = static_cast<uint32_t*>(s_syn.get(B * a.MW * sizeof(uint32_t)));
+      CUDA_OK(cudaMemcpyAsync(d, b.syndrome, B * a.MW * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+      a.in_syn = d;
+    }
+  }
+  // outputs (device targets; staged when the caller passed host memory)
+  auto dev_out = [&](void* user, size_t bytes, Scratch& s, bool* staged) -> void* {
+    *staged = false;
+    if (user == nullptr) return nullptr;
+    if (is_device_ptr(user)) return user;
+    *staged = true;
+    return s.get(bytes);
+  };
+  const size_t bits_bytes = b.bits_packed ? B * a.NW * sizeof(uint32_t) : B * a.N;
+  bool st_bits, st_it, st_rs, st_post, st_q;
+  void* d_bits = dev_out(b.bits, bits_bytes, s_bits, &st_bits);
+  a.out_bits_u8 = (!b.bits_packed && d_bits) ? static_cast<uint8_t*>(d_bits) : nullptr;
+  a.out_bits_pk = (b.bits_packed && d_bits) ? static_cast<uint32_t*>(d_bits) : nullptr;
+  a.out_iters = static_cast<int32_t*>(dev_out(b.iterations, B * sizeof(int32_t), s_iters, &st_it));
+  a.out_reasons = static_cast<uint8_t*>(dev_out(b.reasons, B, s_reasons, &st_rs));
+  a.out_post = static_cast<float*>(dev_out(b.posteriors, B * a.N * sizeof(float), s_post, &st_post));
+  a.out_qtrace = static_cast<double*>(dev_out(b.q_trace, B * p.d_max * sizeof(double), s_qtrace, &st_q));
+  if (a.out_qtrace) CUDA_OK(cudaMemsetAsync(a.out_qtrace, 0xff, B * p.d_max * sizeof(double), st));  // NaN
+
+  // initial slot assignment: frames 0..min(B,S)-1 -> slots 0..
+  const int first = static_cast<int>(std::min<size_t>(B, S));
+  {
+    std::vector<int32_t> pend(S, 0);
+    std::vector<uint32_t> lm(G, 0u);
+    for (int s = 0; s < first; ++s) {
+      pend[s] = s;
+      lm[s >> 5] |= 1u << (s & 31);
+    }
+    int32_t ctr[4] = {first, 0, 0, 0};
+    CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemsetAsync(a.group_active, 0, G * sizeof(uint32_t), st));
+    CUDA_OK(cudaMemsetAsync(a.stopped, 0, G * sizeof(uint32_t), st));
+    CUDA_OK(cudaMemsetAsync(a.frame_iters, 0, sizeof(unsigned long long), st));
+    // the host vectors die at scope end: make the copies complete first
+    CUDA_OK(cudaStreamSynchronize(st));
+  }
+  launch(kLoad, st, [&] {
+    k_load<<<load_item_blocks + load_check_blocks + 1, kThreads, 0, st>>>(a, load_item_blocks, load_check_blocks);
+  });
+  k_step_end<<<1, 32, 0, st>>>(a);
+  CUDA_OK(cudaGetLastError());
+  ++launches;
+
+  // step loop: poll the frames-done counter with a lag so the GPU never idles
+  const int64_t waves = (static_cast<int64_t>(B) + S - 1) / S;
+  const int64_t max_steps = static_cast<int64_t>(p.d_max) * waves + 2;
+  constexpr int kLag = 4;
+  int64_t step = 0;
+  bool done = false;
+  for (; step < max_steps + kLag && !done; ++step) {
+    run_step(a, st, want_post);
+    const int slot = static_cast<int>(step % kRing);
+    CUDA_OK(cudaMemcpyAsync(h_counters + 4 * slot, a.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaEventRecord(ring_ev[slot], st));
+    if (step >= kLag) {
+      const int old = static_cast<int>((step - kLag) % kRing);
+      CUDA_OK(cudaEventSynchronize(ring_ev[old]));
+      if (h_counters[4 * old + 2] != 0) break;  // invalid input detected
+      if (h_counters[4 * old + 1] >= b.batch) done = true;
+    }
+  }
+  CUDA_OK(cudaStreamSynchronize(st));
+  int32_t ctr[4];
+  CUDA_OK(cudaMemcpy(ctr, a.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
+  if (ctr[2] != 0) throw ValidationError("decode: non-finite input LLR");
+  if (ctr[1] < b.batch) throw CudaError("decode: internal error, frames did not terminate");
+  if (profiling) {
+    unsigned long long fi = 0;
+    CUDA_OK(cudaMemcpy(&fi, a.frame_iters, sizeof(fi), cudaMemcpyDeviceToHost));
+    prof_frame_iters += static_cast<double>(fi);
+    for (size_t k = 0; k < prof_kid.size(); ++k) {
+      float ms = 0.0f;
+      CUDA_OK(cudaEventElapsedTime(&ms, prof_ev[2 * k], prof_ev[2 * k + 1]));
+      prof_ms[prof_kid[k]] += ms;
+      prof_launches[prof_kid[k]] += 1;
+    }
+    for (auto& e : prof_ev) cudaEventDestroy(e);
+    prof_ev.clear();
+    prof_kid.clear();
+  }
+  // copy staged outputs back
+  if (st_bits) CUDA_OK(cudaMemcpyAsync(b.bits, d_bits, bits_bytes, cudaMemcpyDeviceToHost, st));
+  if (st_it) CUDA_OK(cudaMemcpyAsync(b.iterations, a.out_iters, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (st_rs) CUDA_OK(cudaMemcpyAsync(b.reasons, a.out_reasons, B, cudaMemcpyDeviceToHost, st));
+  if (st_post) CUDA_OK(cudaMemcpyAsync(b.posteriors, a.out_post, B * a.N * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (st_q) CUDA_OK(cudaMemcpyAsync(b.q_trace, a.out_qtrace, B * p.d_max * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+}
+
+void GpuDecoder::sample_device(double snr, uint64_t seed, int64_t first_frame, int32_t n_frames, bool all_zero,
+                               float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t st_in) {
+  CUDA_OK(cudaSetDevice(device));
+  const cudaStream_t st = st_in ? st_in : own_stream;
+  if (!(snr > 0.0) || !std::isfinite(snr)) throw ValidationError("sample: snr must be positive and finite");
+  if (n_frames <= 0) return;
+  uint32_t* x = d_x;
+  Scratch tmp;
+  if (x == nullptr && d_syn != nullptr) x = static_cast<uint32_t*>(tmp.get(static_cast<size_t>(n_frames) * base.NW * 4));
+  k_gen_llr<<<1184, kThreads, 0, st>>>(base.N, base.NW, snr, seed, first_frame, n_frames, all_zero ? 1 : 0, d_llr, x);
+  CUDA_OK(cudaGetLastError());
+  ++launches;
+  if (d_syn) {
+    k_gen_syndrome<<<592, kThreads, 0, st>>>(base, n_frames, x, d_syn, d_check_ptr, d_check_vars);
+    CUDA_OK(cudaGetLastError());
+    ++launches;
+  }
+  CUDA_OK(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------ wrappers --
+GpuDecoder* gpu_decoder_create(const Code& code, int device, int max_slots) {
+  return new GpuDecoder(code, device, max_slots);
+}
+void gpu_decoder_destroy(GpuDecoder* dec) { delete dec; }
+int gpu_decoder_slots(const GpuDecoder* dec) { return dec->S; }
+int64_t gpu_decoder_device_bytes(const GpuDecoder* dec) { return dec->dev_bytes; }
+void gpu_decode_batch(GpuDecoder* dec, const DecodeParams& p, const DecodeBuffers& b, void* stream) {
+  dec->decode(p, b, static_cast<cudaStream_t>(stream));
+}
+void gpu_sample_frames_device(GpuDecoder* dec, double snr, uint64_t seed, int64_t first_frame, int32_t n_frames,
+                              bool all_zero, float* d_llr, uint32_t* d_syndrome, uint32_t* d_x_packed, void* stream) {
+  dec->sample_device(snr, seed, first_frame, n_frames, all_zero, d_llr, d_syndrome, d_x_packed,
+                     static_cast<cudaStream_t>(stream));
+}
+void gpu_set_profiling(GpuDecoder* dec, bool enable) { dec->profiling = enable; }
+void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches, double* frame_iterations) {
+  if (kernel < 0 || kernel >= kNumKernels) throw ValidationError("profile: kernel id out of range");
+  if (total_ms) *total_ms = dec->prof_ms[kernel];
+  if (launches) *launches = dec->prof_launches[kernel];
+  if (frame_iterations) *frame_iterations = dec->prof_frame_iters;
+}
+void gpu_reset_profile(GpuDecoder* dec) {
+  std::fill(std::begin(dec->prof_ms), std::end(dec->prof_ms), 0.0);
+  std::fill(std::begin(dec->prof_launches), std::end(dec->prof_launches), 0);
+  dec->prof_frame_iters = 0.0;
+  dec->launches = 0;
+}
+int64_t gpu_launch_count(const GpuDecoder* dec) { return dec->launches; }
+
+}  // namespace bpdec

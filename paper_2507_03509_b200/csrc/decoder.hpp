@@ -1,0 +1,46 @@
+// Host-side interface of the CUDA decoder (no CUDA types; used by c_api.cpp).
+#pragma once
+
+#include <cstdint>
+
+#include "code.hpp"
+
+namespace bpdec {
+
+struct DecodeParams {
+  int32_t d_max = 100;
+  int32_t use_pce = 1;
+  int32_t use_vnr = 0;
+  int32_t q_mode = 0;  // 0 raw, 1 abs
+  float msg_clamp = 30.0f;
+};
+
+struct DecodeBuffers {
+  int32_t batch = 0;
+  const float* llr = nullptr;          // [batch][N]
+  const uint32_t* syndrome = nullptr;  // [batch][ceil(M/32)] or null
+  bool bits_packed = false;
+  void* bits = nullptr;                // u8 [batch][N] or u32 [batch][ceil(N/32)]
+  int32_t* iterations = nullptr;
+  uint8_t* reasons = nullptr;
+  float* posteriors = nullptr;
+  double* q_trace = nullptr;
+};
+
+class GpuDecoder;
+
+GpuDecoder* gpu_decoder_create(const Code& code, int device, int max_slots);
+void gpu_decoder_destroy(GpuDecoder* dec);
+int gpu_decoder_slots(const GpuDecoder* dec);
+int64_t gpu_decoder_device_bytes(const GpuDecoder* dec);
+void gpu_decode_batch(GpuDecoder* dec, const DecodeParams& p, const DecodeBuffers& b, void* stream);
+void gpu_sample_frames_device(GpuDecoder* dec, double snr, uint64_t seed, int64_t first_frame,
+                              int32_t n_frames, bool all_zero, float* d_llr, uint32_t* d_syndrome,
+                              uint32_t* d_x_packed, void* stream);
+void gpu_set_profiling(GpuDecoder* dec, bool enable);
+void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches,
+                 double* frame_iterations);
+void gpu_reset_profile(GpuDecoder* dec);
+int64_t gpu_launch_count(const GpuDecoder* dec);
+
+}  // namespace bpdec

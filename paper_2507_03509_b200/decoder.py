@@ -1,0 +1,490 @@
+"""Python mirror of the reference ``etdec`` decode interface over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/core/include/etdec/*.hpp) so tests read like the
+reference's own:
+
+=======================  ====================================================
+this module              reference
+=======================  ====================================================
+ParityCheckMatrix        etdec::ParityCheckMatrix (parity_check_matrix.hpp:12)
+active_var_set           etdec::active_var_set    (parity_check_matrix.hpp:70)
+load_alist/save_alist    alist.hpp:20-24
+lift_protograph          protograph.hpp:31
+DecodeConfig             etdec::DecodeConfig      (decoder.hpp:21-26)
+StopReason               etdec::StopReason        (decoder.hpp:13-17)
+DecodeOutcome            etdec::DecodeOutcome     (decoder.hpp:28-36)
+BpDecoder.decode         BpDecoder::decode        (decoder.hpp:64-65)
+decode                   etdec::decode            (decoder.hpp:78-79)
+syndrome_check           decoder.hpp:39
+vnr_statistic            decoder.hpp:42
+vnr_should_stop          decoder.hpp:45
+snr_for_beta             channel.hpp:24
+ConfigError/IoError/     errors.hpp:8-24
+ValidationError
+=======================  ====================================================
+
+``BatchDecoder.decode_batch`` is the B200-native batched entry point (many
+frames per call, syndrome-aware); ``BpDecoder.decode`` is the single-frame
+shim with the reference's signature.  Every decode runs the CUDA kernels;
+there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+__all__ = [
+    "ConfigError", "IoError", "ValidationError", "BpdecCudaError", "BpdecOomError",
+    "ParityCheckMatrix", "ActiveVarSet", "active_var_set", "load_alist", "save_alist",
+    "lift_protograph", "generate_met", "DecodeConfig", "StopReason", "DecodeOutcome",
+    "BatchResult", "BpDecoder", "BatchDecoder", "decode", "syndrome_check", "vnr_statistic",
+    "vnr_should_stop", "snr_for_beta", "sample_frames", "pack_bits", "unpack_bits",
+]
+
+
+class BpdecError(RuntimeError):
+    status = 6
+
+
+class ConfigError(BpdecError):
+    """≙ etdec::ConfigError (errors.hpp:9-12), CLI exit code 1."""
+    status = 1
+
+
+class IoError(BpdecError):
+    """≙ etdec::IoError (errors.hpp:15-18), CLI exit code 2."""
+    status = 2
+
+
+class ValidationError(BpdecError):
+    """≙ etdec::ValidationError (errors.hpp:21-24), CLI exit code 3."""
+    status = 3
+
+
+class BpdecCudaError(BpdecError):
+    status = 4
+
+
+class BpdecOomError(BpdecError):
+    status = 5
+
+
+_ERRORS = {1: ConfigError, 2: IoError, 3: ValidationError, 4: BpdecCudaError, 5: BpdecOomError}
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = _lib.load().bpdec_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, BpdecError)(msg)
+
+
+def _ptr(a, ctype=None):
+    """Raw address of a numpy array, a torch tensor (data_ptr) or None."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValidationError("array must be C-contiguous")
+        return a.ctypes.data_as(ctype) if ctype is not None else C.c_void_p(a.ctypes.data)
+    raise TypeError(f"unsupported buffer type {type(a)!r}")
+
+
+# --------------------------------------------------------------------- code --
+class ParityCheckMatrix:
+    """Immutable Tanner graph (≙ etdec::ParityCheckMatrix).  Construct with the
+    factories; ``n_vars``, ``n_checks``, ``n_edges``, ``rate()``,
+    ``check_vars(c)``, ``var_degree(v)`` mirror the reference accessors."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._lib = _lib.load()
+        self._h = handle
+        n, m, e, a = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
+        _check(self._lib.bpdec_code_dims(handle, C.byref(n), C.byref(m), C.byref(e), C.byref(a)))
+        self.n_vars, self.n_checks, self.n_edges, self.n_active = n.value, m.value, e.value, a.value
+        self._csr = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.bpdec_code_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ≙ from_check_lists (parity_check_matrix.cpp:10-62)
+    @classmethod
+    def from_check_lists(cls, n_vars: int, per_check_vars: Sequence[Sequence[int]]) -> "ParityCheckMatrix":
+        ptr = np.zeros(len(per_check_vars) + 1, dtype=np.int32)
+        for c, lst in enumerate(per_check_vars):
+            ptr[c + 1] = ptr[c] + len(lst)
+        flat = np.fromiter((v for lst in per_check_vars for v in lst), dtype=np.int64, count=int(ptr[-1]))
+        if flat.size and (flat.min() < -2**31 or flat.max() >= 2**31):
+            raise ValidationError("parity-check matrix: variable index out of range")
+        return cls.from_csr(n_vars, len(per_check_vars), ptr, flat.astype(np.int32))
+
+    @classmethod
+    def from_csr(cls, n_vars: int, n_checks: int, check_ptr, check_vars) -> "ParityCheckMatrix":
+        lib = _lib.load()
+        ptr = np.ascontiguousarray(check_ptr, dtype=np.int32)
+        var = np.ascontiguousarray(check_vars, dtype=np.int32)
+        if ptr.size != n_checks + 1:
+            raise ValidationError("parity-check matrix: check_ptr must have n_checks+1 entries")
+        if ptr.size and var.size < int(ptr[-1]):
+            raise ValidationError("parity-check matrix: check_vars shorter than check_ptr[-1]")
+        h = C.c_void_p()
+        _check(lib.bpdec_code_from_csr(n_vars, n_checks, _ptr(ptr, _lib.c_i32p), _ptr(var, _lib.c_i32p), C.byref(h)))
+        return cls(h)
+
+    def csr(self):
+        if self._csr is None:
+            ptr = np.zeros(self.n_checks + 1, dtype=np.int32)
+            var = np.zeros(max(self.n_edges, 1), dtype=np.int32)
+            _check(self._lib.bpdec_code_csr(self._h, _ptr(ptr, _lib.c_i32p), _ptr(var, _lib.c_i32p)))
+            self._csr = (ptr, var[: self.n_edges])
+        return self._csr
+
+    def rate(self) -> float:
+        return (self.n_vars - self.n_checks) / self.n_vars
+
+    def check_degree(self, c: int) -> int:
+        ptr, _ = self.csr()
+        return int(ptr[c + 1] - ptr[c])
+
+    def check_vars(self, c: int) -> np.ndarray:
+        ptr, var = self.csr()
+        return var[ptr[c]: ptr[c + 1]]
+
+    def var_degrees(self) -> np.ndarray:
+        _, var = self.csr()
+        return np.bincount(var, minlength=self.n_vars).astype(np.int32)
+
+    def var_degree(self, v: int) -> int:
+        return int(self.var_degrees()[v])
+
+    def check_degrees(self) -> np.ndarray:
+        ptr, _ = self.csr()
+        return np.diff(ptr).astype(np.int32)
+
+    def syndrome(self, bits: np.ndarray) -> np.ndarray:
+        """s = H x for one ([N]) or many ([F, N]) u8 words -> packed u32 words."""
+        b = np.ascontiguousarray(bits, dtype=np.uint8)
+        frames = 1 if b.ndim == 1 else b.shape[0]
+        out = np.zeros((frames, (self.n_checks + 31) // 32), dtype=np.uint32)
+        _check(self._lib.bpdec_code_syndrome(self._h, frames, _ptr(b, _lib.c_u8p), _ptr(out, _lib.c_u32p)))
+        return out[0] if b.ndim == 1 else out
+
+
+@dataclass
+class ActiveVarSet:
+    """≙ etdec::ActiveVarSet: variables of degree >= 2, ascending."""
+    members: np.ndarray
+
+
+def active_var_set(code: ParityCheckMatrix) -> ActiveVarSet:
+    out = np.zeros(max(code.n_active, 1), dtype=np.int32)
+    _check(code._lib.bpdec_code_active_vars(code.handle, _ptr(out, _lib.c_i32p)))
+    return ActiveVarSet(out[: code.n_active])
+
+
+def load_alist(path: str) -> ParityCheckMatrix:
+    lib = _lib.load()
+    h = C.c_void_p()
+    _check(lib.bpdec_code_load_alist(path.encode(), C.byref(h)))
+    return ParityCheckMatrix(h)
+
+
+def save_alist(code: ParityCheckMatrix, path: str) -> None:
+    _check(code._lib.bpdec_code_save_alist(code.handle, path.encode()))
+
+
+def lift_protograph(base: Sequence[Sequence[int]], z: int, seed: int) -> ParityCheckMatrix:
+    lib = _lib.load()
+    b = np.ascontiguousarray(base, dtype=np.int32)
+    if b.ndim != 2:
+        raise ValidationError("protograph lift: ragged base matrix")
+    h = C.c_void_p()
+    _check(lib.bpdec_code_lift_protograph(_ptr(b, _lib.c_i32p), b.shape[0], b.shape[1], z, seed, C.byref(h)))
+    return ParityCheckMatrix(h)
+
+
+def generate_met(n_vars: int, n_checks: int, frac_deg1: float, degrees: Sequence[int],
+                 probs: Sequence[float], seed: int) -> ParityCheckMatrix:
+    """BASELINE.json code construction (rule in csrc/code.cpp)."""
+    lib = _lib.load()
+    d = np.ascontiguousarray(degrees, dtype=np.int32)
+    p = np.ascontiguousarray(probs, dtype=np.float64)
+    if d.size != p.size:
+        raise ValidationError("met generator: degree and probability lists must be aligned")
+    h = C.c_void_p()
+    _check(lib.bpdec_code_generate_met(n_vars, n_checks, float(frac_deg1), d.size, _ptr(d, _lib.c_i32p),
+                                       _ptr(p, _lib.c_f64p), seed, C.byref(h)))
+    return ParityCheckMatrix(h)
+
+
+# ------------------------------------------------------------------ decoder --
+class StopReason(enum.IntEnum):
+    """≙ etdec::StopReason (decoder.hpp:13-17)."""
+    kSyndromeSatisfied = 0
+    kVnrDrop = 1
+    kMaxIterations = 2
+
+    def __str__(self) -> str:  # ≙ to_string (decoder.cpp:10-17)
+        return _lib.load().bpdec_stop_reason_name(int(self)).decode()
+
+
+Q_RAW, Q_ABS = 0, 1
+
+
+@dataclass
+class DecodeConfig:
+    """≙ etdec::DecodeConfig (decoder.hpp:21-26) + q-mode (RAW = reference)."""
+    d_max: int = 100
+    use_pce: bool = True
+    use_vnr: bool = False
+    msg_clamp: float = 30.0
+    q_mode: int = Q_RAW
+
+    def c_struct(self) -> _lib.Config:
+        return _lib.Config(int(self.d_max), int(bool(self.use_pce)), int(bool(self.use_vnr)),
+                           int(self.q_mode), float(self.msg_clamp))
+
+
+@dataclass
+class DecodeOutcome:
+    """≙ etdec::DecodeOutcome (decoder.hpp:28-36)."""
+    bits: np.ndarray
+    iterations: int
+    reason: StopReason
+    q_trace: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    posteriors: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.float32))
+
+    def converged(self) -> bool:
+        return self.reason == StopReason.kSyndromeSatisfied
+
+
+@dataclass
+class BatchResult:
+    iterations: np.ndarray
+    reasons: np.ndarray
+    bits: Optional[np.ndarray] = None
+    posteriors: Optional[np.ndarray] = None
+    q_trace: Optional[np.ndarray] = None
+
+    def outcome(self, f: int) -> DecodeOutcome:
+        k = int(self.iterations[f])
+        return DecodeOutcome(
+            bits=None if self.bits is None else self.bits[f],
+            iterations=k,
+            reason=StopReason(int(self.reasons[f])),
+            q_trace=np.zeros(0) if self.q_trace is None else self.q_trace[f, :k].copy(),
+            posteriors=np.zeros(0, dtype=np.float32) if self.posteriors is None else self.posteriors[f],
+        )
+
+
+class BatchDecoder:
+    """B200 batched decoder: a device replica of ``code`` and message state for
+    ``max_slots`` frames in flight (≙ BpDecoder construction, decoder.cpp:38-48,
+    once per GPU instead of once per worker thread)."""
+
+    def __init__(self, code: ParityCheckMatrix, device: int = 0, max_slots: int = 64):
+        self._lib = _lib.load()
+        self.code = code
+        h = C.c_void_p()
+        _check(self._lib.bpdec_decoder_create(code.handle, device, max_slots, C.byref(h)))
+        self._h = h
+        s = C.c_int32()
+        _check(self._lib.bpdec_decoder_slots(h, C.byref(s)))
+        self.slots = s.value
+        self.device = device
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.bpdec_decoder_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_bytes(self) -> int:
+        b = C.c_int64()
+        _check(self._lib.bpdec_decoder_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def decode_batch(self, llr, cfg: DecodeConfig, syndrome=None, *, want_bits: bool = True,
+                     packed: bool = False, want_posteriors: bool = False, want_q_trace: bool = False,
+                     stream: int = 0, out=None) -> BatchResult:
+        """Decode ``llr`` [B, N] (float32 numpy or CUDA tensor) against
+        ``syndrome`` [B, ceil(M/32)] u32 (None = all-zero).  Outputs are numpy
+        arrays unless ``out`` (dict of preallocated buffers) is given."""
+        n = self.code.n_vars
+        if hasattr(llr, "data_ptr"):
+            batch = int(llr.shape[0])
+            if llr.shape[-1] != n:
+                raise ValidationError(f"decode: LLR length {llr.shape[-1]} does not match n_vars={n}")
+        else:
+            llr = np.ascontiguousarray(llr, dtype=np.float32)
+            if llr.ndim == 1:
+                llr = llr[None, :]
+            if llr.shape[1] != n:
+                raise ValidationError(f"decode: LLR length {llr.shape[1]} does not match n_vars={n}")
+            batch = llr.shape[0]
+        if syndrome is not None and not hasattr(syndrome, "data_ptr"):
+            syndrome = np.ascontiguousarray(syndrome, dtype=np.uint32).reshape(batch, -1)
+        if out is None:
+            out = {}
+            out["iterations"] = np.zeros(batch, dtype=np.int32)
+            out["reasons"] = np.zeros(batch, dtype=np.uint8)
+            if want_bits:
+                out["bits"] = (np.zeros((batch, (n + 31) // 32), dtype=np.uint32) if packed
+                               else np.zeros((batch, n), dtype=np.uint8))
+            if want_posteriors:
+                out["posteriors"] = np.zeros((batch, n), dtype=np.float32)
+            if want_q_trace:
+                out["q_trace"] = np.zeros((batch, cfg.d_max), dtype=np.float64)
+        c = cfg.c_struct()
+        flags = 1 if packed else 0
+        _check(self._lib.bpdec_decode_batch(
+            self._h, batch, _ptr(llr), _ptr(syndrome), C.byref(c), flags, _ptr(out.get("bits")),
+            _ptr(out["iterations"]), _ptr(out["reasons"]), _ptr(out.get("posteriors")),
+            _ptr(out.get("q_trace")), C.c_void_p(stream) if stream else None))
+        return BatchResult(out["iterations"], out["reasons"], out.get("bits"), out.get("posteriors"),
+                           out.get("q_trace"))
+
+    def sample_frames_device(self, snr: float, seed: int, first_frame: int, n_frames: int, llr_dev,
+                             syndrome_dev=None, x_packed_dev=None, all_zero: bool = False, stream: int = 0):
+        _check(self._lib.bpdec_decoder_sample_frames_device(
+            self._h, float(snr), seed, first_frame, n_frames, int(all_zero), _ptr(llr_dev), _ptr(syndrome_dev),
+            _ptr(x_packed_dev), C.c_void_p(stream) if stream else None))
+
+    # profiling (CUDA events on the launching stream)
+    KERNELS = ("check", "variable", "syndrome", "terminate", "load", "extract")
+
+    def set_profiling(self, enable: bool):
+        _check(self._lib.bpdec_decoder_set_profiling(self._h, int(enable)))
+
+    def reset_profile(self):
+        _check(self._lib.bpdec_decoder_reset_profile(self._h))
+
+    def profile(self) -> dict:
+        res = {}
+        for k, name in enumerate(self.KERNELS):
+            ms, n, fi = C.c_double(), C.c_int64(), C.c_double()
+            _check(self._lib.bpdec_decoder_profile(self._h, k, C.byref(ms), C.byref(n), C.byref(fi)))
+            res[name] = {"ms": ms.value, "launches": n.value}
+            res["frame_iterations"] = fi.value
+        return res
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(self._lib.bpdec_decoder_launch_count(self._h, C.byref(n)))
+        return n.value
+
+
+class BpDecoder:
+    """Single-frame shim with the reference signature (decoder.hpp:57-65):
+    ``BpDecoder(code).decode(llr_in, active, cfg)`` -> DecodeOutcome.  LLRs are
+    rounded to float32 (the decoder's input type)."""
+
+    def __init__(self, code: ParityCheckMatrix, device: int = 0):
+        self.code = code
+        self._dec = BatchDecoder(code, device=device, max_slots=32)
+
+    def decode(self, llr_in, active: Optional[ActiveVarSet] = None, cfg: Optional[DecodeConfig] = None,
+               syndrome=None, observer=None) -> DecodeOutcome:
+        cfg = cfg or DecodeConfig()
+        llr = np.asarray(llr_in, dtype=np.float64)
+        if llr.ndim != 1 or llr.size != self.code.n_vars:
+            raise ValidationError(f"decode: LLR length {llr.size} does not match n_vars={self.code.n_vars}")
+        if not np.all(np.isfinite(llr)):
+            raise ValidationError("decode: non-finite input LLR")
+        r = self._dec.decode_batch(llr.astype(np.float32)[None, :], cfg,
+                                   None if syndrome is None else np.asarray(syndrome, dtype=np.uint32)[None, :],
+                                   want_posteriors=True, want_q_trace=True)
+        out = r.outcome(0)
+        if observer is not None:  # IterationObserver emulation from q_trace (decoder.hpp:53-55)
+            for k in range(out.iterations):
+                observer(k + 1, None, None, float(out.q_trace[k]))
+        return out
+
+
+def decode(code: ParityCheckMatrix, llr_in, active: Optional[ActiveVarSet], cfg: DecodeConfig,
+           syndrome=None) -> DecodeOutcome:
+    """≙ etdec::decode (decoder.hpp:78-79): throwaway decoder."""
+    return BpDecoder(code).decode(llr_in, active, cfg, syndrome=syndrome)
+
+
+def syndrome_check(code: ParityCheckMatrix, bits, syndrome=None) -> bool:
+    """≙ syndrome_check (decoder.cpp:19-30); optional target syndrome."""
+    b = np.ascontiguousarray(bits, dtype=np.uint8)
+    if b.size != code.n_vars:
+        raise ValidationError(
+            f"syndrome_check: bit vector length {b.size} does not match n_vars={code.n_vars}")
+    s = None if syndrome is None else np.ascontiguousarray(syndrome, dtype=np.uint32)
+    ok = C.c_int32()
+    _check(code._lib.bpdec_syndrome_check(code.handle, _ptr(b, _lib.c_u8p), _ptr(s, _lib.c_u32p), C.byref(ok)))
+    return bool(ok.value)
+
+
+def vnr_statistic(posteriors, active: ActiveVarSet) -> float:
+    """≙ vnr_statistic (decoder.cpp:32-36): sequential double sum."""
+    q = 0.0
+    p = np.asarray(posteriors, dtype=np.float64)
+    for v in active.members:
+        q += float(p[v])
+    return q
+
+
+def vnr_should_stop(q_k: float, q_km1: float) -> bool:
+    """≙ vnr_should_stop (decoder.hpp:45): strict decrease."""
+    return q_k < q_km1
+
+
+def snr_for_beta(beta: float, rate: float) -> float:
+    """≙ snr_for_beta (channel.cpp:29-42): snr = 2^(2R/beta) - 1."""
+    out = C.c_double()
+    _check(_lib.load().bpdec_snr_for_beta(float(beta), float(rate), C.byref(out)))
+    return out.value
+
+
+def sample_frames(code: ParityCheckMatrix, snr: float, seed: int, first_frame: int, n_frames: int,
+                  all_zero: bool = False):
+    """Seeded syndrome-mode frames -> (llr [F,N] f32, x [F,N] u8, s [F,MW] u32)."""
+    llr = np.zeros((n_frames, code.n_vars), dtype=np.float32)
+    x = np.zeros((n_frames, code.n_vars), dtype=np.uint8)
+    s = np.zeros((n_frames, (code.n_checks + 31) // 32), dtype=np.uint32)
+    _check(code._lib.bpdec_sample_frames(code.handle, float(snr), seed, first_frame, n_frames, int(all_zero),
+                                         _ptr(llr, _lib.c_f32p), _ptr(x, _lib.c_u8p), _ptr(s, _lib.c_u32p)))
+    return llr, x, s
+
+
+def pack_bits(bits: np.ndarray) -> np.ndarray:
+    """u8 [.., N] -> u32 [.., ceil(N/32)] LSB-first."""
+    b = np.asarray(bits, dtype=np.uint8)
+    n = b.shape[-1]
+    pad = (-n) % 32
+    if pad:
+        b = np.concatenate([b, np.zeros(b.shape[:-1] + (pad,), dtype=np.uint8)], axis=-1)
+    return np.packbits(b.reshape(b.shape[:-1] + (-1, 32)), axis=-1, bitorder="little").view(np.uint32)[..., 0]
+
+
+def unpack_bits(words: np.ndarray, n: int) -> np.ndarray:
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    b = np.unpackbits(w.view(np.uint8), bitorder="little")
+    return b.reshape(w.shape[:-1] + (-1,))[..., :n]
