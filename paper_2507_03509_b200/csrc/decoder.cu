@@ -129,129 +129,209 @@ __device__ __forceinline__ long long skip_group(long long w, long long per_group
 }
 
 // ------------------------------------------------------------- k_check --
-// One warp = one check x 32 slots.  MAXD bounds the check degree so the
-// messages and phi values live in registers.
+// One warp = one chunk of 32 consecutive checks x 32 slots of one group.
+// The chunk's index data (check descriptors, target-syndrome words, the H
+// indices of its degree>=2 edges) is staged in shared memory with coalesced
+// loads first, so the only global latency left per check is the message
+// gather itself; two checks are in flight per warp.  MAXD bounds the check
+// degree (registers); MAXD = 256 is the rolled generic path.
+template <int MAXD>
+struct CheckState {
+  float m[MAXD];
+  float l1[MAXD];
+  int4 d;
+  int deg, nh;
+  uint32_t sbit, par;
+  int c;
+};
+
+template <int MAXD>
+__device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, int g, int c, const int4 d,
+                                           uint32_t sword, const int32_t* hh, int lane, bool act, bool first) {
+  constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
+  s.c = c;
+  s.d = d;
+  s.nh = d.y - d.x;
+  s.deg = s.nh + (d.w - d.z);
+  s.sbit = (sword >> lane) & 1u;
+  s.par = s.sbit;
+  const int lim = MAXD <= 16 ? MAXD : s.deg;
+#pragma unroll kUnroll
+  for (int j = 0; j < lim; ++j) {
+    if (j < s.deg) {
+      float v = 0.0f;
+      if (j < s.nh) {
+        const int h = hh[j];
+        if (act) {
+          const float* src = first ? &a.llr_h[(static_cast<size_t>(g) * a.NH + h) * kLanes + lane]
+                                   : &a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
+          const float p = *src;
+          const float co = first ? 0.0f : ld_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane]);
+          v = first ? p : clampf(p - co, a.clamp);
+        }
+        s.l1[j] = 0.0f;
+      } else {
+        const int dd = d.z + (j - s.nh);
+        float l = 0.0f;
+        if (act) l = ld_stream(&a.llr_d[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane]);
+        s.l1[j] = l;
+        v = first ? l : clampf(l, a.clamp);
+      }
+      s.m[j] = v;
+    }
+  }
+}
+
+template <int MAXD, bool WANT_POST>
+__device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>& s, int g, int lane, bool act) {
+  constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
+  const int deg = s.deg;
+  const int lim = MAXD <= 16 ? MAXD : deg;
+  uint32_t par = s.par;
+#pragma unroll kUnroll
+  for (int j = 0; j < lim; ++j)
+    if (j < deg) par ^= signbit_u(s.m[j]);
+  float out[MAXD];
+  if (deg == 1) {
+    out[0] = a.clamp;  // empty product: atanh(1) = inf -> clamp
+  } else if (deg == 2) {
+    out[0] = fminf(fabsf(s.m[1]), a.clamp);  // phi(phi(x)) = x
+    out[1] = fminf(fabsf(s.m[0]), a.clamp);
+  } else if (deg > 2) {
+    float ph[MAXD];
+    float pre[MAXD];
+    float run = 0.0f;
+#pragma unroll kUnroll
+    for (int j = 0; j < lim; ++j) {
+      if (j < deg) {
+        ph[j] = dev::phi(fabsf(s.m[j]));
+        pre[j] = run;
+        run += ph[j];
+      }
+    }
+    float suf = 0.0f;
+#pragma unroll kUnroll
+    for (int j = lim - 1; j >= 0; --j) {
+      if (j < deg) {
+        out[j] = fminf(dev::phi(pre[j] + suf), a.clamp);
+        suf += ph[j];
+      }
+    }
+  }
+  uint32_t dpar = 0u;
+#pragma unroll kUnroll
+  for (int j = 0; j < lim; ++j) {
+    if (j < deg) {
+      const float o = with_sign(out[j], par ^ signbit_u(s.m[j]));
+      if (j < s.nh) {
+        if (act) st_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + s.d.x + j) * kLanes + lane], o);
+      } else {
+        const int dd = s.d.z + (j - s.nh);
+        const float pd = s.l1[j] + o;  // posterior of the degree-1 variable
+        const uint32_t bit = (act && pd < 0.0f) ? 1u : 0u;
+        dpar ^= bit;
+        const uint32_t word = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) a.d1bits[static_cast<size_t>(g) * a.N1 + dd] = word;
+        if (WANT_POST && act) a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane] = pd;
+      }
+    }
+  }
+  return __ballot_sync(0xffffffffu, (s.sbit ^ dpar) & 1u);
+}
+
 template <int MAXD, bool WANT_POST>
 __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
-  // Degrees up to 16 are fully unrolled into registers; MAXD = 256 is the
-  // generic path (rolled loops over local-memory arrays).
-  constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
-  if (blockIdx.x == 0 && threadIdx.x < a.G) {
-    a.fail[threadIdx.x] = 0u;
-  }
+  constexpr bool kStage = MAXD <= 16;
+  constexpr int kHH = kStage ? 32 * MAXD : 1;
+  __shared__ int4 s_desc[kThreads / 32][32];
+  __shared__ uint32_t s_syn[kThreads / 32][32];
+  __shared__ int32_t s_hh[kThreads / 32][kHH];
+  if (blockIdx.x == 0 && threadIdx.x < a.G) a.fail[threadIdx.x] = 0u;
   const int lane = threadIdx.x & 31;
+  const int wi = threadIdx.x >> 5;
   const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  const long long total = static_cast<long long>(a.G) * a.M;
+  const int chunks = (a.M + 31) / 32;
+  const long long total = static_cast<long long>(a.G) * chunks;
   for (long long w = warp0; w < total;) {
-    const int g = static_cast<int>(w / a.M);
-    const int c = static_cast<int>(w - static_cast<long long>(g) * a.M);
+    const int g = static_cast<int>(w / chunks);
+    const int c0 = static_cast<int>(w - static_cast<long long>(g) * chunks) * 32;
     const uint32_t amask = a.group_active[g];
     if (amask == 0u) {
-      w = skip_group(w, a.M, nwarps);
+      w = skip_group(w, chunks, nwarps);
       continue;
     }
+    const int nc = min(32, a.M - c0);
     const bool act = (amask >> lane) & 1u;
-    const int4 d = __ldg(&a.cdesc[c]);
-    const int nh = d.y - d.x;
-    const int deg = nh + (d.w - d.z);
-    const uint32_t sbit = (__ldg(&a.syn_target[static_cast<size_t>(g) * a.M + c]) >> lane) & 1u;
-    uint32_t dpar = 0u;  // parity of degree-1 hard bits (lane bit)
-    if (deg > 0) {
-      const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
-      const bool first = (it == 1);
-      const int lim = MAXD <= 16 ? MAXD : deg;
-      float m[MAXD];
-      float l1[MAXD];
-      uint32_t par = sbit;
-#pragma unroll kUnroll
-      for (int j = 0; j < lim; ++j) {
-        if (j < deg) {
-          float v = 0.0f;
-          if (j < nh) {
-            const int h = __ldg(&a.chk_hi_h[d.x + j]);
-            if (act) {
-              if (first) {
-                v = a.llr_h[(static_cast<size_t>(g) * a.NH + h) * kLanes + lane];
-              } else {
-                const float p = a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
-                const float co = ld_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane]);
-                v = clampf(p - co, a.clamp);
-              }
-            }
-          } else {
-            const int dd = d.z + (j - nh);
-            if (act) {
-              const float l = ld_stream(&a.llr_d[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane]);
-              l1[j] = l;
-              v = first ? l : clampf(l, a.clamp);
-            } else {
-              l1[j] = 0.0f;
-            }
-          }
-          m[j] = v;
-          par ^= signbit_u(v);
-        }
+    const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
+    const bool first = (it == 1);
+    __syncwarp();
+    if (lane < nc) {
+      s_desc[wi][lane] = __ldg(&a.cdesc[c0 + lane]);
+      s_syn[wi][lane] = a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane];
+    }
+    __syncwarp();
+    const int hb0 = s_desc[wi][0].x;
+    if (kStage) {
+      const int nhh = s_desc[wi][nc - 1].y - hb0;
+      for (int i = lane; i < nhh; i += 32) s_hh[wi][i] = __ldg(&a.chk_hi_h[hb0 + i]);
+      __syncwarp();
+    }
+    uint32_t myword = 0u;
+    for (int j = 0; j < nc; j += 2) {
+      CheckState<MAXD> A, B;
+      const int4 dA = s_desc[wi][j];
+      check_load<MAXD>(a, A, g, c0 + j, dA, s_syn[wi][j], kStage ? &s_hh[wi][dA.x - hb0] : &a.chk_hi_h[dA.x],
+                       lane, act, first);
+      const bool hasB = j + 1 < nc;
+      if (hasB) {
+        const int4 dB = s_desc[wi][j + 1];
+        check_load<MAXD>(a, B, g, c0 + j + 1, dB, s_syn[wi][j + 1],
+                         kStage ? &s_hh[wi][dB.x - hb0] : &a.chk_hi_h[dB.x], lane, act, first);
       }
-      float out[MAXD];
-      if (deg == 1) {
-        out[0] = a.clamp;  // empty product: atanh(1) = inf -> clamp
-      } else if (deg == 2) {
-        out[0] = fminf(fabsf(m[1]), a.clamp);  // phi(phi(x)) = x
-        out[1] = fminf(fabsf(m[0]), a.clamp);
-      } else {
-        float ph[MAXD];
-        float pre[MAXD];
-        float run = 0.0f;
-#pragma unroll kUnroll
-        for (int j = 0; j < lim; ++j) {
-          if (j < deg) {
-            ph[j] = dev::phi(fabsf(m[j]));
-            pre[j] = run;
-            run += ph[j];
-          }
-        }
-        float suf = 0.0f;
-#pragma unroll kUnroll
-        for (int j = lim - 1; j >= 0; --j) {
-          if (j < deg) {
-            out[j] = fminf(dev::phi(pre[j] + suf), a.clamp);
-            suf += ph[j];
-          }
-        }
-      }
-#pragma unroll kUnroll
-      for (int j = 0; j < lim; ++j) {
-        if (j < deg) {
-          const float o = with_sign(out[j], par ^ signbit_u(m[j]));
-          if (j < nh) {
-            if (act) st_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane], o);
-          } else {
-            const int dd = d.z + (j - nh);
-            const float pd = l1[j] + o;  // posterior of the degree-1 variable
-            const uint32_t bit = (act && pd < 0.0f) ? 1u : 0u;
-            dpar ^= bit;
-            const uint32_t word = __ballot_sync(0xffffffffu, bit);
-            if (lane == 0) a.d1bits[static_cast<size_t>(g) * a.N1 + dd] = word;
-            if (WANT_POST && act) a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane] = pd;
-          }
-        }
+      const uint32_t wa = check_finish<MAXD, WANT_POST>(a, A, g, lane, act);
+      if (lane == j) myword = wa;
+      if (hasB) {
+        const uint32_t wb = check_finish<MAXD, WANT_POST>(a, B, g, lane, act);
+        if (lane == j + 1) myword = wb;
       }
     }
-    const uint32_t sw = __ballot_sync(0xffffffffu, (sbit ^ dpar) & 1u);
-    if (lane == 0) a.synp[static_cast<size_t>(g) * a.M + c] = sw;
+    if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = myword;
     w += nwarps;
   }
 }
 
 // --------------------------------------------------------------- k_var --
-// One block = one tile of kQTile consecutive degree>=2 variables x 32 slots;
-// warp k handles variables tile*256 + k*32 + (0..31) in order, and the tile's
-// q partial is the warp partials summed in warp order: a summation order that
-// depends on the code only (not on slots, batch size or GPU count).
+// One warp = 32 consecutive degree>=2 variables x 32 slots; its CSC slice
+// (vptr, vedge) is staged in shared memory, then two variables are in flight
+// at a time with their message gathers issued before the (ordered) sums.
+// A block covers kQTile = 256 variables and the tile's q partial is the warp
+// partials summed in warp order: a summation order that depends on the code
+// only (not on slots, batch size or GPU count).
+constexpr int kVarStage = 32 * 24;  // staged edge ids per warp (mean degree <= 24)
+constexpr int kVarBatch = 8;        // gathers issued together
+
+// ve points at the edge ids of CSC slot `kb` (staged copy or global array).
+__device__ __forceinline__ float var_sum(const Args& a, size_t gl, size_t ge, int h, int k0, int k1,
+                                         const int32_t* ve, int kb, int lane) {
+  float p = ld_stream(&a.llr_h[(gl + h) * kLanes + lane]);
+  for (int k = k0; k < k1; k += kVarBatch) {
+    float v[kVarBatch];
+#pragma unroll
+    for (int u = 0; u < kVarBatch; ++u)
+      v[u] = (k + u < k1) ? ld_stream(&a.c2v[(ge + ve[k + u - kb]) * kLanes + lane]) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < kVarBatch; ++u)
+      if (k + u < k1) p += v[u];  // ascending check order (decoder.cpp:101)
+  }
+  return p;
+}
+
 template <int QMODE>
 __global__ void __launch_bounds__(kThreads) k_var(const Args a) {
   __shared__ double red[kVarWarps][kLanes];
+  __shared__ int32_t s_ptr[kVarWarps][33];
+  __shared__ int32_t s_ve[kVarWarps][kVarStage];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const long long total = static_cast<long long>(a.G) * a.n_tiles;
@@ -266,24 +346,42 @@ __global__ void __launch_bounds__(kThreads) k_var(const Args a) {
     const bool act = (amask >> lane) & 1u;
     double acc = 0.0;
     const int h0 = tile * kQTile + warp * kLanes;
-    const int h1 = min(h0 + kLanes, a.NV);
+    const int nv = max(0, min(kLanes, a.NV - h0));
     const size_t gl = static_cast<size_t>(g) * a.NH;
     const size_t gv = static_cast<size_t>(g) * a.NV;
     const size_t ge = static_cast<size_t>(g) * a.EH;
-    for (int h = h0; h < h1; ++h) {
-      float p = 0.0f;
-      const int k0 = __ldg(&a.vptr[h]);
-      const int k1 = __ldg(&a.vptr[h + 1]);
-      if (act) {
-        p = ld_stream(&a.llr_h[(gl + h) * kLanes + lane]);
-        for (int k = k0; k < k1; ++k) {
-          p += ld_stream(&a.c2v[(ge + __ldg(&a.vedge[k])) * kLanes + lane]);
+    if (nv > 0) {
+      if (lane < nv) s_ptr[warp][lane] = __ldg(&a.vptr[h0 + lane]);
+      if (lane == 0) s_ptr[warp][nv] = __ldg(&a.vptr[h0 + nv]);
+      __syncwarp();
+      const int kb = s_ptr[warp][0];
+      const int nk = s_ptr[warp][nv] - kb;
+      const bool staged = nk <= kVarStage;
+      if (staged)
+        for (int i = lane; i < nk; i += 32) s_ve[warp][i] = __ldg(&a.vedge[kb + i]);
+      __syncwarp();
+      const int32_t* ve = staged ? &s_ve[warp][0] : a.vedge + kb;
+      for (int i = 0; i < nv; i += 2) {
+        const int hA = h0 + i;
+        float pA = 0.0f, pB = 0.0f;
+        const bool hasB = i + 1 < nv;
+        if (act) {
+          pA = var_sum(a, gl, ge, hA, s_ptr[warp][i], s_ptr[warp][i + 1], ve, kb, lane);
+          if (hasB) pB = var_sum(a, gl, ge, hA + 1, s_ptr[warp][i + 1], s_ptr[warp][i + 2], ve, kb, lane);
+          a.post[(gv + hA) * kLanes + lane] = pA;
+          acc += QMODE == 0 ? static_cast<double>(pA) : static_cast<double>(fabsf(pA));
+          if (hasB) {
+            a.post[(gv + hA + 1) * kLanes + lane] = pB;
+            acc += QMODE == 0 ? static_cast<double>(pB) : static_cast<double>(fabsf(pB));
+          }
         }
-        a.post[(gv + h) * kLanes + lane] = p;
-        acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+        const uint32_t wA = __ballot_sync(0xffffffffu, act && pA < 0.0f);
+        const uint32_t wB = __ballot_sync(0xffffffffu, act && pB < 0.0f);
+        if (lane == 0) {
+          a.hbits[gv + hA] = wA;
+          if (hasB) a.hbits[gv + hA + 1] = wB;
+        }
       }
-      const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
-      if (lane == 0) a.hbits[gv + h] = word;
     }
     red[warp][lane] = acc;
     __syncthreads();
@@ -781,19 +879,21 @@ GpuDecoder::~GpuDecoder() {
 
 template <typename F>
 void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // events come from a pool reused across decodes (creation is not free)
+  const size_t k = prof_kid.size();
   if (profiling) {
-    CUDA_OK(cudaEventCreate(&e0));
-    CUDA_OK(cudaEventCreate(&e1));
-    CUDA_OK(cudaEventRecord(e0, st));
+    while (prof_ev.size() < 2 * (k + 1)) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      prof_ev.push_back(e);
+    }
+    CUDA_OK(cudaEventRecord(prof_ev[2 * k], st));
   }
   f();
   CUDA_OK(cudaGetLastError());
   ++launches;
   if (profiling) {
-    CUDA_OK(cudaEventRecord(e1, st));
-    prof_ev.push_back(e0);
-    prof_ev.push_back(e1);
+    CUDA_OK(cudaEventRecord(prof_ev[2 * k + 1], st));
     prof_kid.push_back(kid);
   }
 }
@@ -958,8 +1058,6 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       prof_ms[prof_kid[k]] += ms;
       prof_launches[prof_kid[k]] += 1;
     }
-    for (auto& e : prof_ev) cudaEventDestroy(e);
-    prof_ev.clear();
     prof_kid.clear();
   }
   // copy staged outputs back
