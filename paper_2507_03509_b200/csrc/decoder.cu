@@ -71,6 +71,9 @@ struct Args {
   const int32_t* vedge;     // [EH] c2v row of each edge of variable h, ascending check
   const int32_t* vmap;      // [N] original var -> h (>=0) or -1-d (degree 1)
   const int32_t* dorig;     // [N] device item (H then D1) -> original var
+  const int32_t* corig;     // [M] device check -> original check
+  const int32_t* ctype;     // [ceil(M/32)] chunk type NH*8+ND (homogeneous, full) or -1
+  const int32_t* vtype;     // [ceil(NV/32)] chunk degree (homogeneous, full) or -1
   // state
   int32_t G;
   float* llr_h;             // [G][NH][32]
@@ -129,12 +132,19 @@ __device__ __forceinline__ long long skip_group(long long w, long long per_group
 }
 
 // ------------------------------------------------------------- k_check --
-// One warp = one chunk of 32 consecutive checks x 32 slots of one group.
-// The chunk's index data (check descriptors, target-syndrome words, the H
-// indices of its degree>=2 edges) is staged in shared memory with coalesced
-// loads first, so the only global latency left per check is the message
-// gather itself; two checks are in flight per warp.  MAXD bounds the check
-// degree (registers); MAXD = 256 is the rolled generic path.
+// One warp = one chunk of 32 consecutive (device-order) checks x 32 slots of
+// one group.  Checks are sorted by type (NH edges to degree>=2 variables, ND
+// degree-1 edges) when the device layout is built, so almost every chunk is
+// homogeneous: its c2v rows are hb + i*NH + j and its degree-1 rows db + i,
+// only the H indices of the gathers come from (staged) memory, and the
+// typed path below processes K checks at once with straight-line code so
+// K*(NH+ND) message loads are in flight per warp.  Mixed chunks (at most one
+// per type boundary) and unsupported types take the generic path.
+//
+// Iteration 1 (decoder.cpp:69-73): post was initialised to the channel LLR
+// at load, and the c2v load is skipped, so v2c = llr - 0 = llr, unclamped.
+// Later iterations: v2c = clamp(post - c2v) (decoder.cpp:104); degree-1
+// edges: clamp(llr) (the reference's clamp((llr + c2v) - c2v)).
 template <int MAXD>
 struct CheckState {
   float m[MAXD];
@@ -142,14 +152,12 @@ struct CheckState {
   int4 d;
   int deg, nh;
   uint32_t sbit, par;
-  int c;
 };
 
 template <int MAXD>
-__device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, int g, int c, const int4 d,
-                                           uint32_t sword, const int32_t* hh, int lane, bool act, bool first) {
+__device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, int g, const int4 d, uint32_t sword,
+                                           const int32_t* hh, int lane, bool act, bool first) {
   constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
-  s.c = c;
   s.d = d;
   s.nh = d.y - d.x;
   s.deg = s.nh + (d.w - d.z);
@@ -163,9 +171,7 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
       if (j < s.nh) {
         const int h = hh[j];
         if (act) {
-          const float* src = first ? &a.llr_h[(static_cast<size_t>(g) * a.NH + h) * kLanes + lane]
-                                   : &a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
-          const float p = *src;
+          const float p = a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
           const float co = first ? 0.0f : ld_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane]);
           v = first ? p : clampf(p - co, a.clamp);
         }
@@ -182,6 +188,35 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
   }
 }
 
+// Magnitudes of the outgoing messages from the incoming ones (phi domain;
+// prefix/suffix sums, no subtraction).  deg 1: empty product -> clamp;
+// deg 2: phi(phi(x)) = x, passed through.
+template <int D>
+__device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&out)[D], float clamp) {
+  if (D == 1) {
+    out[0] = clamp;
+  } else if (D == 2) {
+    out[0] = fminf(fabsf(m[1]), clamp);
+    out[1] = fminf(fabsf(m[D > 1 ? 0 : 0]), clamp);
+  } else {
+    float ph[D];
+    float pre[D];
+    float run = 0.0f;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      ph[j] = dev::phi(fabsf(m[j]));
+      pre[j] = run;
+      run += ph[j];
+    }
+    float suf = 0.0f;
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+      out[j] = fminf(dev::phi(pre[j] + suf), clamp);
+      suf += ph[j];
+    }
+  }
+}
+
 template <int MAXD, bool WANT_POST>
 __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>& s, int g, int lane, bool act) {
   constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
@@ -193,9 +228,9 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
     if (j < deg) par ^= signbit_u(s.m[j]);
   float out[MAXD];
   if (deg == 1) {
-    out[0] = a.clamp;  // empty product: atanh(1) = inf -> clamp
+    out[0] = a.clamp;
   } else if (deg == 2) {
-    out[0] = fminf(fabsf(s.m[1]), a.clamp);  // phi(phi(x)) = x
+    out[0] = fminf(fabsf(s.m[1]), a.clamp);
     out[1] = fminf(fabsf(s.m[0]), a.clamp);
   } else if (deg > 2) {
     float ph[MAXD];
@@ -239,6 +274,70 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
   return __ballot_sync(0xffffffffu, (s.sbit ^ dpar) & 1u);
 }
 
+// Typed chunk: 32 checks, each with NH edges to degree>=2 variables (c2v rows
+// hb + 32-check-local i*NH + j) and ND <= 1 degree-1 edge (row db + i).
+template <int NH, int ND, bool WANT_POST>
+__device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
+                                                  const uint32_t* ssyn, int lane, bool act, bool first,
+                                                  uint32_t* synw, uint32_t* d1w) {
+  constexpr int D = NH + ND;
+  constexpr int K = D <= 2 ? 8 : (D <= 4 ? 4 : 2);
+  const float* postg = a.post + static_cast<size_t>(g) * a.NV * kLanes + lane;
+  float* c2vg = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes + lane;
+  const float* llrd = a.llr_d + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane;
+  float* d1p = WANT_POST ? a.d1post + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane : nullptr;
+  const float clamp = a.clamp;
+#pragma unroll 1
+  for (int i0 = 0; i0 < 32; i0 += K) {
+    float m[K][D > 0 ? D : 1];
+    float l1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int j = 0; j < NH; ++j) {
+        const int h = hh[(i0 + k) * NH + j];
+        float p = 0.0f, co = 0.0f;
+        if (act) {
+          p = postg[static_cast<size_t>(h) * kLanes];
+          if (!first) co = ld_stream(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes);
+        }
+        const float v = p - co;
+        m[k][j] = first ? v : clampf(v, clamp);
+      }
+      if (ND) {
+        const float l = act ? ld_stream(llrd + static_cast<size_t>(i0 + k) * kLanes) : 0.0f;
+        l1[k] = l;
+        m[k][NH] = first ? l : clampf(l, clamp);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
+      uint32_t par = sbit;
+#pragma unroll
+      for (int j = 0; j < D; ++j) par ^= signbit_u(m[k][j]);
+      float out[D > 0 ? D : 1];
+      check_magnitudes<D>(m[k], out, clamp);
+#pragma unroll
+      for (int j = 0; j < NH; ++j) {
+        const float o = with_sign(out[j], par ^ signbit_u(m[k][j]));
+        if (act) st_stream(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o);
+      }
+      uint32_t dbit = 0u;
+      if (ND) {
+        const float o = with_sign(out[NH], par ^ signbit_u(m[k][NH]));
+        const float pd = l1[k] + o;  // posterior of the degree-1 variable
+        dbit = (act && pd < 0.0f) ? 1u : 0u;
+        if (WANT_POST && act) d1p[static_cast<size_t>(i0 + k) * kLanes] = pd;
+        const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
+        if (lane == i0 + k) *d1w = dw;
+      }
+      const uint32_t sw = __ballot_sync(0xffffffffu, sbit ^ dbit);
+      if (lane == i0 + k) *synw = sw;
+    }
+  }
+}
+
 template <int MAXD, bool WANT_POST>
 __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
   constexpr bool kStage = MAXD <= 16;
@@ -255,7 +354,8 @@ __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
   const long long total = static_cast<long long>(a.G) * chunks;
   for (long long w = warp0; w < total;) {
     const int g = static_cast<int>(w / chunks);
-    const int c0 = static_cast<int>(w - static_cast<long long>(g) * chunks) * 32;
+    const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
+    const int c0 = ch * 32;
     const uint32_t amask = a.group_active[g];
     if (amask == 0u) {
       w = skip_group(w, chunks, nwarps);
@@ -265,6 +365,12 @@ __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
     const bool act = (amask >> lane) & 1u;
     const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
     const bool first = (it == 1);
+    const int type = kStage ? __ldg(&a.ctype[ch]) : -1;
+    // degree-1 checks only change in a frame's first iteration
+    if ((type == 1 || type == 8) && !__any_sync(0xffffffffu, act && first)) {
+      w += nwarps;
+      continue;
+    }
     __syncwarp();
     if (lane < nc) {
       s_desc[wi][lane] = __ldg(&a.cdesc[c0 + lane]);
@@ -277,51 +383,109 @@ __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
       for (int i = lane; i < nhh; i += 32) s_hh[wi][i] = __ldg(&a.chk_hi_h[hb0 + i]);
       __syncwarp();
     }
-    uint32_t myword = 0u;
-    for (int j = 0; j < nc; j += 2) {
-      CheckState<MAXD> A, B;
-      const int4 dA = s_desc[wi][j];
-      check_load<MAXD>(a, A, g, c0 + j, dA, s_syn[wi][j], kStage ? &s_hh[wi][dA.x - hb0] : &a.chk_hi_h[dA.x],
-                       lane, act, first);
-      const bool hasB = j + 1 < nc;
-      if (hasB) {
-        const int4 dB = s_desc[wi][j + 1];
-        check_load<MAXD>(a, B, g, c0 + j + 1, dB, s_syn[wi][j + 1],
-                         kStage ? &s_hh[wi][dB.x - hb0] : &a.chk_hi_h[dB.x], lane, act, first);
-      }
-      const uint32_t wa = check_finish<MAXD, WANT_POST>(a, A, g, lane, act);
-      if (lane == j) myword = wa;
-      if (hasB) {
-        const uint32_t wb = check_finish<MAXD, WANT_POST>(a, B, g, lane, act);
-        if (lane == j + 1) myword = wb;
+    uint32_t synw = 0u, d1w = 0u;
+    const int db0 = s_desc[wi][0].z;
+    bool typed = true;
+    switch (type) {
+#define BPDEC_TYPED(NH_, ND_)                                                                       \
+  case NH_ * 8 + ND_:                                                                               \
+    if (NH_ + ND_ <= MAXD)                                                                          \
+      check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], lane, act, first, \
+                                             &synw, &d1w);                                          \
+    break;
+      BPDEC_TYPED(0, 1)
+      BPDEC_TYPED(1, 0)
+      BPDEC_TYPED(1, 1)
+      BPDEC_TYPED(2, 0)
+      BPDEC_TYPED(2, 1)
+      BPDEC_TYPED(3, 0)
+      BPDEC_TYPED(3, 1)
+      BPDEC_TYPED(6, 0)
+#undef BPDEC_TYPED
+      default:
+        typed = false;
+    }
+    if (typed) {
+      if ((type & 7) != 0) a.d1bits[static_cast<size_t>(g) * a.N1 + db0 + lane] = d1w;
+    } else {
+      for (int j = 0; j < nc; j += 2) {
+        CheckState<MAXD> A, B;
+        const int4 dA = s_desc[wi][j];
+        check_load<MAXD>(a, A, g, dA, s_syn[wi][j], kStage ? &s_hh[wi][dA.x - hb0] : &a.chk_hi_h[dA.x], lane, act,
+                         first);
+        const bool hasB = j + 1 < nc;
+        if (hasB) {
+          const int4 dB = s_desc[wi][j + 1];
+          check_load<MAXD>(a, B, g, dB, s_syn[wi][j + 1], kStage ? &s_hh[wi][dB.x - hb0] : &a.chk_hi_h[dB.x], lane,
+                           act, first);
+        }
+        const uint32_t wa = check_finish<MAXD, WANT_POST>(a, A, g, lane, act);
+        if (lane == j) synw = wa;
+        if (hasB) {
+          const uint32_t wb = check_finish<MAXD, WANT_POST>(a, B, g, lane, act);
+          if (lane == j + 1) synw = wb;
+        }
       }
     }
-    if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = myword;
+    if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = synw;
     w += nwarps;
   }
 }
 
 // --------------------------------------------------------------- k_var --
-// One warp = 32 consecutive degree>=2 variables x 32 slots; its CSC slice
-// (vptr, vedge) is staged in shared memory, then two variables are in flight
-// at a time with their message gathers issued before the (ordered) sums.
-// A block covers kQTile = 256 variables and the tile's q partial is the warp
-// partials summed in warp order: a summation order that depends on the code
-// only (not on slots, batch size or GPU count).
-constexpr int kVarStage = 32 * 24;  // staged edge ids per warp (mean degree <= 24)
-constexpr int kVarBatch = 8;        // gathers issued together
+// One warp = 32 consecutive (device-order) degree>=2 variables x 32 slots.
+// Variables are sorted by degree in the device layout, so a chunk is almost
+// always homogeneous: its CSC slice (edge ids of its c2v rows) is staged in
+// shared memory and the typed path gathers K variables' messages at once
+// before the (ordered) sums.  A block covers kQTile = 256 variables and the
+// tile's q partial is the warp partials summed in warp order — a summation
+// order fixed by the code (not by slots, batch size or GPU count).
+constexpr int kVarStage = 32 * 24;  // staged edge ids per warp
+
+template <int D, int QMODE>
+__device__ __forceinline__ void var_chunk_typed(const Args& a, int g, int h0, const int32_t* ve, int lane,
+                                                bool act, double* acc, uint32_t* hw) {
+  constexpr int K = D <= 4 ? 4 : (D <= 8 ? 2 : 1);
+  const float* llrh = a.llr_h + (static_cast<size_t>(g) * a.NH + h0) * kLanes + lane;
+  const float* c2vg = a.c2v + static_cast<size_t>(g) * a.EH * kLanes + lane;
+  float* postg = a.post + (static_cast<size_t>(g) * a.NV + h0) * kLanes + lane;
+#pragma unroll 1
+  for (int i0 = 0; i0 < 32; i0 += K) {
+    float l[K];
+    float v[K][D];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      l[k] = act ? ld_stream(llrh + static_cast<size_t>(i0 + k) * kLanes) : 0.0f;
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        v[k][j] = act ? ld_stream(c2vg + static_cast<size_t>(ve[(i0 + k) * D + j]) * kLanes) : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float p = l[k];
+#pragma unroll
+      for (int j = 0; j < D; ++j) p += v[k][j];  // ascending check order (decoder.cpp:101)
+      if (act) {
+        postg[static_cast<size_t>(i0 + k) * kLanes] = p;
+        *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
+      if (lane == i0 + k) *hw = word;
+    }
+  }
+}
 
 // ve points at the edge ids of CSC slot `kb` (staged copy or global array).
 __device__ __forceinline__ float var_sum(const Args& a, size_t gl, size_t ge, int h, int k0, int k1,
                                          const int32_t* ve, int kb, int lane) {
   float p = ld_stream(&a.llr_h[(gl + h) * kLanes + lane]);
-  for (int k = k0; k < k1; k += kVarBatch) {
-    float v[kVarBatch];
+  for (int k = k0; k < k1; k += 8) {
+    float v[8];
 #pragma unroll
-    for (int u = 0; u < kVarBatch; ++u)
+    for (int u = 0; u < 8; ++u)
       v[u] = (k + u < k1) ? ld_stream(&a.c2v[(ge + ve[k + u - kb]) * kLanes + lane]) : 0.0f;
 #pragma unroll
-    for (int u = 0; u < kVarBatch; ++u)
+    for (int u = 0; u < 8; ++u)
       if (k + u < k1) p += v[u];  // ascending check order (decoder.cpp:101)
   }
   return p;
@@ -361,27 +525,40 @@ __global__ void __launch_bounds__(kThreads) k_var(const Args a) {
         for (int i = lane; i < nk; i += 32) s_ve[warp][i] = __ldg(&a.vedge[kb + i]);
       __syncwarp();
       const int32_t* ve = staged ? &s_ve[warp][0] : a.vedge + kb;
-      for (int i = 0; i < nv; i += 2) {
-        const int hA = h0 + i;
-        float pA = 0.0f, pB = 0.0f;
-        const bool hasB = i + 1 < nv;
-        if (act) {
-          pA = var_sum(a, gl, ge, hA, s_ptr[warp][i], s_ptr[warp][i + 1], ve, kb, lane);
-          if (hasB) pB = var_sum(a, gl, ge, hA + 1, s_ptr[warp][i + 1], s_ptr[warp][i + 2], ve, kb, lane);
-          a.post[(gv + hA) * kLanes + lane] = pA;
-          acc += QMODE == 0 ? static_cast<double>(pA) : static_cast<double>(fabsf(pA));
-          if (hasB) {
-            a.post[(gv + hA + 1) * kLanes + lane] = pB;
-            acc += QMODE == 0 ? static_cast<double>(pB) : static_cast<double>(fabsf(pB));
+      const int vt = staged ? __ldg(&a.vtype[h0 / 32]) : -1;
+      uint32_t hw = 0u;
+      bool typed = true;
+      switch (vt) {
+#define BPDEC_VTYPED(D_) \
+  case D_:               \
+    var_chunk_typed<D_, QMODE>(a, g, h0, ve, lane, act, &acc, &hw); \
+    break;
+        BPDEC_VTYPED(2)
+        BPDEC_VTYPED(3)
+        BPDEC_VTYPED(4)
+        BPDEC_VTYPED(6)
+        BPDEC_VTYPED(8)
+        BPDEC_VTYPED(12)
+        BPDEC_VTYPED(16)
+        BPDEC_VTYPED(20)
+#undef BPDEC_VTYPED
+        default:
+          typed = false;
+      }
+      if (!typed) {
+        for (int i = 0; i < nv; ++i) {
+          const int h = h0 + i;
+          float p = 0.0f;
+          if (act) {
+            p = var_sum(a, gl, ge, h, s_ptr[warp][i], s_ptr[warp][i + 1], ve, kb, lane);
+            a.post[(gv + h) * kLanes + lane] = p;
+            acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
           }
-        }
-        const uint32_t wA = __ballot_sync(0xffffffffu, act && pA < 0.0f);
-        const uint32_t wB = __ballot_sync(0xffffffffu, act && pB < 0.0f);
-        if (lane == 0) {
-          a.hbits[gv + hA] = wA;
-          if (hasB) a.hbits[gv + hA + 1] = wB;
+          const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
+          if (lane == i) hw = word;
         }
       }
+      if (lane < nv) a.hbits[gv + h0 + lane] = hw;
     }
     red[warp][lane] = acc;
     __syncthreads();
@@ -551,6 +728,8 @@ __global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks
           const float v = tile[j][lane];
           if (item < a.NH) {
             a.llr_h[(static_cast<size_t>(g) * a.NH + item) * kLanes + lane] = v;
+            // posterior state starts at the channel LLR (v2c of iteration 1)
+            if (item < a.NV) a.post[(static_cast<size_t>(g) * a.NV + item) * kLanes + lane] = v;
           } else {
             a.llr_d[(static_cast<size_t>(g) * a.N1 + (item - a.NH)) * kLanes + lane] = v;
           }
@@ -568,11 +747,12 @@ __global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks
       if (lm == 0u) continue;
       uint32_t word = a.syn_target[w] & ~lm;
       if (a.in_syn) {
+        const int co = __ldg(&a.corig[c]);  // syndrome input is in original check order
         while (lm) {
           const int r = __ffs(lm) - 1;
           lm &= lm - 1;
           const int f = a.pending_frame[g * kLanes + r];
-          word |= ((__ldg(&a.in_syn[static_cast<size_t>(f) * a.MW + (c >> 5)]) >> (c & 31)) & 1u) << r;
+          word |= ((__ldg(&a.in_syn[static_cast<size_t>(f) * a.MW + (co >> 5)]) >> (co & 31)) & 1u) << r;
         }
       }
       a.syn_target[w] = word;
@@ -746,23 +926,41 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   S = (max_slots + 31) / 32 * 32;
   G = S / 32;
 
-  // ---- device code layout
+  // ---- device code layout (DESIGN.md §3)
+  // variables: degree>=2 sorted by (degree, index) -> h in [0, NV); then
+  // degree 0 -> [NV, NH); degree-1 variables -> D1 rows in device check order.
+  // checks: sorted by type (NH edges to degree>=2 vars, ND degree-1 edges).
   const int32_t N = code.n_vars, M = code.n_checks;
   std::vector<int32_t> deg(N);
   for (int32_t v = 0; v < N; ++v) deg[v] = code.var_degree(v);
   std::vector<int32_t> horig;
   for (int32_t v = 0; v < N; ++v)
     if (deg[v] >= 2) horig.push_back(v);
+  std::stable_sort(horig.begin(), horig.end(), [&](int32_t x, int32_t y) { return deg[x] < deg[y]; });
   const int32_t NV = static_cast<int32_t>(horig.size());
   for (int32_t v = 0; v < N; ++v)
     if (deg[v] == 0) horig.push_back(v);
   const int32_t NH = static_cast<int32_t>(horig.size());
   std::vector<int32_t> vmap(N, 0);
   for (int32_t h = 0; h < NH; ++h) vmap[horig[h]] = h;
+  std::vector<int32_t> cnh(M, 0), cnd(M, 0);
+  for (int32_t c = 0; c < M; ++c) {
+    for (int32_t e = code.check_ptr[c]; e < code.check_ptr[c + 1]; ++e) {
+      const int32_t d = deg[code.check_vars[e]];
+      if (d >= 2) ++cnh[c];
+      else ++cnd[c];
+    }
+  }
+  std::vector<int32_t> corig(M);
+  for (int32_t c = 0; c < M; ++c) corig[c] = c;
+  std::stable_sort(corig.begin(), corig.end(), [&](int32_t x, int32_t y) {
+    return cnh[x] != cnh[y] ? cnh[x] < cnh[y] : cnd[x] < cnd[y];
+  });
   std::vector<int4> cdesc(M);
   std::vector<int32_t> chk_hi_h, dorig(horig), hi_of_edge(code.n_edges(), -1);
   int32_t n1 = 0;
-  for (int32_t c = 0; c < M; ++c) {
+  for (int32_t cd = 0; cd < M; ++cd) {
+    const int32_t c = corig[cd];
     max_check_deg = std::max(max_check_deg, code.check_degree(c));
     int4 d;
     d.x = static_cast<int32_t>(chk_hi_h.size());
@@ -784,16 +982,36 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
       }
     }
     d.w = n1;
-    cdesc[c] = d;
+    cdesc[cd] = d;
   }
   if (max_check_deg > 256) throw ValidationError("decoder: check degree above 256 is not supported");
+  // chunk types: homogeneous full chunks of 32 checks get NH*8+ND, else -1
+  std::vector<int32_t> ctype((M + 31) / 32, -1);
+  for (size_t k = 0; k < ctype.size(); ++k) {
+    const int32_t c0 = static_cast<int32_t>(k * 32);
+    if (c0 + 32 > M) continue;
+    const int32_t t = cnh[corig[c0]] * 8 + cnd[corig[c0]];
+    bool same = cnd[corig[c0]] <= 1 && cnh[corig[c0]] <= 7;
+    for (int32_t i = 1; i < 32 && same; ++i) same = cnh[corig[c0 + i]] * 8 + cnd[corig[c0 + i]] == t;
+    if (same) ctype[k] = t;
+  }
   const int64_t EH = static_cast<int64_t>(chk_hi_h.size());
   std::vector<int32_t> vptr(NV + 1, 0), vedge;
   vedge.reserve(EH);
   for (int32_t h = 0; h < NV; ++h) {
     const int32_t v = horig[h];
+    // ascending ORIGINAL check order: the reference's summation order
     for (int32_t k = code.var_ptr[v]; k < code.var_ptr[v + 1]; ++k) vedge.push_back(hi_of_edge[code.var_edges[k]]);
     vptr[h + 1] = static_cast<int32_t>(vedge.size());
+  }
+  std::vector<int32_t> vtype((NV + 31) / 32, -1);
+  for (size_t k = 0; k < vtype.size(); ++k) {
+    const int32_t h0 = static_cast<int32_t>(k * 32);
+    if (h0 + 32 > NV) continue;
+    const int32_t d0 = deg[horig[h0]];
+    bool same = true;
+    for (int32_t i = 1; i < 32 && same; ++i) same = deg[horig[h0 + i]] == d0;
+    if (same) vtype[k] = d0;
   }
 
   Args& a = base;
@@ -820,6 +1038,9 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.vedge = up(vedge, static_cast<int32_t*>(nullptr));
   a.vmap = up(vmap, static_cast<int32_t*>(nullptr));
   a.dorig = up(dorig, static_cast<int32_t*>(nullptr));
+  a.corig = up(corig, static_cast<int32_t*>(nullptr));
+  a.ctype = up(ctype, static_cast<int32_t*>(nullptr));
+  a.vtype = up(vtype, static_cast<int32_t*>(nullptr));
   d_check_ptr = up(code.check_ptr, static_cast<int32_t*>(nullptr));
   d_check_vars = up(code.check_vars, static_cast<int32_t*>(nullptr));
 
