@@ -42,3 +42,12 @@ oracle:
 clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
+
+# C++ host-layer test program (reference-shaped API over the C ABI)
+COMPAT_TEST := build/compat_test
+$(COMPAT_TEST): tests/cpp/compat_test.cpp include/bpdec/etdec_compat.hpp include/bpdec.h $(LIB)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++20 -Wall -Wextra -Iinclude -o $@ $< -L$(PKG) -lbpdec -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+compat_test: $(COMPAT_TEST)
+.PHONY: compat_test

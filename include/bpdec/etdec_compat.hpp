@@ -1,0 +1,251 @@
+// etdec_compat.hpp — header-only C++ host layer with the reference's decode
+// interface (namespace etdec in /root/reference/proj/core/include/etdec/),
+// implemented on top of the C ABI in include/bpdec.h.
+//
+// A caller of the reference switches by replacing
+//     #include <etdec/decoder.hpp>           with   #include <bpdec/etdec_compat.hpp>
+//     etdec::                                 with   bpdec::compat::
+// and linking libbpdec.so.  Same class names, argument meaning and exception
+// classes; the difference is that decode runs on the GPU and there is also a
+// batched, syndrome-aware entry point (BpDecoder::decode_batch).
+//
+//   reference (file:line)                          here
+//   ParityCheckMatrix::from_check_lists (pcm.hpp:16) ParityCheckMatrix::from_check_lists
+//   load_alist_file / save_alist_file (alist.hpp:21,24)  load_alist_file / save_alist_file
+//   lift_protograph (protograph.hpp:31)            lift_protograph
+//   active_var_set (pcm.hpp:70)                    active_var_set
+//   DecodeConfig / DecodeOutcome / StopReason      same (decoder.hpp:13-36)
+//   BpDecoder(code), BpDecoder::decode (decoder.hpp:57-65)  same (+ syndrome overload)
+//   decode(code, llr, active, cfg) (decoder.hpp:78-79)      same
+//   syndrome_check / vnr_statistic / vnr_should_stop (decoder.hpp:39-45)  same
+//   snr_for_beta (channel.hpp:24)                  snr_for_beta
+//   ConfigError / IoError / ValidationError (errors.hpp:8-24)  same
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../bpdec.h"
+
+namespace bpdec::compat {
+
+class ConfigError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class IoError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ValidationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check_status(int st) {
+  if (st == BPDEC_OK) return;
+  const std::string msg = bpdec_last_error();
+  switch (st) {
+    case BPDEC_ERR_CONFIG: throw ConfigError(msg);
+    case BPDEC_ERR_IO: throw IoError(msg);
+    case BPDEC_ERR_VALIDATION: throw ValidationError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+class ParityCheckMatrix {
+ public:
+  static ParityCheckMatrix from_check_lists(int n_vars, const std::vector<std::vector<int>>& per_check_vars) {
+    std::vector<int32_t> ptr(per_check_vars.size() + 1, 0), vars;
+    for (size_t c = 0; c < per_check_vars.size(); ++c) {
+      vars.insert(vars.end(), per_check_vars[c].begin(), per_check_vars[c].end());
+      ptr[c + 1] = static_cast<int32_t>(vars.size());
+    }
+    bpdec_code* h = nullptr;
+    check_status(bpdec_code_from_csr(n_vars, static_cast<int32_t>(per_check_vars.size()), ptr.data(),
+                                     vars.empty() ? nullptr : vars.data(), &h));
+    return ParityCheckMatrix(h);
+  }
+  static ParityCheckMatrix adopt(bpdec_code* h) { return ParityCheckMatrix(h); }
+
+  int n_vars() const { return n_vars_; }
+  int n_checks() const { return n_checks_; }
+  int n_edges() const { return static_cast<int>(n_edges_); }
+  double rate() const { return static_cast<double>(n_vars_ - n_checks_) / n_vars_; }
+  const bpdec_code* handle() const { return h_.get(); }
+
+ private:
+  explicit ParityCheckMatrix(bpdec_code* h) : h_(h, &bpdec_code_destroy) {
+    int32_t active = 0;
+    check_status(bpdec_code_dims(h, &n_vars_, &n_checks_, &n_edges_, &active));
+  }
+  std::shared_ptr<bpdec_code> h_;
+  int32_t n_vars_ = 0, n_checks_ = 0;
+  int64_t n_edges_ = 0;
+};
+
+inline ParityCheckMatrix load_alist_file(const std::string& path) {
+  bpdec_code* h = nullptr;
+  check_status(bpdec_code_load_alist(path.c_str(), &h));
+  return ParityCheckMatrix::adopt(h);
+}
+inline void save_alist_file(const ParityCheckMatrix& code, const std::string& path) {
+  check_status(bpdec_code_save_alist(code.handle(), path.c_str()));
+}
+inline ParityCheckMatrix lift_protograph(const std::vector<std::vector<int>>& base, int z, std::uint64_t seed) {
+  if (base.empty() || base.front().empty()) throw ValidationError("protograph lift: empty base matrix");
+  const size_t rows = base.size(), cols = base.front().size();
+  std::vector<int32_t> flat;
+  for (const auto& r : base) {
+    if (r.size() != cols) throw ValidationError("protograph lift: ragged base matrix");
+    flat.insert(flat.end(), r.begin(), r.end());
+  }
+  bpdec_code* h = nullptr;
+  check_status(bpdec_code_lift_protograph(flat.data(), static_cast<int32_t>(rows), static_cast<int32_t>(cols), z,
+                                          seed, &h));
+  return ParityCheckMatrix::adopt(h);
+}
+
+struct ActiveVarSet {
+  std::vector<int> members;
+};
+inline ActiveVarSet active_var_set(const ParityCheckMatrix& code) {
+  int32_t n = 0, m = 0, a = 0;
+  int64_t e = 0;
+  check_status(bpdec_code_dims(code.handle(), &n, &m, &e, &a));
+  ActiveVarSet s;
+  s.members.resize(a);
+  if (a) check_status(bpdec_code_active_vars(code.handle(), s.members.data()));
+  return s;
+}
+
+enum class StopReason { kSyndromeSatisfied, kVnrDrop, kMaxIterations };
+inline const char* to_string(StopReason r) { return bpdec_stop_reason_name(static_cast<int32_t>(r)); }
+
+struct DecodeConfig {
+  int d_max = 100;
+  bool use_pce = true;
+  bool use_vnr = false;
+  double msg_clamp = 30.0;
+  int q_mode = BPDEC_Q_RAW;  // extension: BPDEC_Q_ABS for true syndrome mode
+};
+
+struct DecodeOutcome {
+  std::vector<std::uint8_t> bits;
+  int iterations = 0;
+  StopReason reason = StopReason::kMaxIterations;
+  std::vector<double> q_trace;
+  std::vector<double> posteriors;
+  bool converged() const { return reason == StopReason::kSyndromeSatisfied; }
+};
+
+inline bool syndrome_check(const ParityCheckMatrix& code, std::span<const std::uint8_t> bits) {
+  if (bits.size() != static_cast<size_t>(code.n_vars())) {
+    throw ValidationError("syndrome_check: bit vector length " + std::to_string(bits.size()) +
+                          " does not match n_vars=" + std::to_string(code.n_vars()));
+  }
+  int32_t ok = 0;
+  check_status(bpdec_syndrome_check(code.handle(), bits.data(), nullptr, &ok));
+  return ok != 0;
+}
+
+inline double vnr_statistic(std::span<const double> posteriors, const ActiveVarSet& active) {
+  double q = 0.0;
+  for (int v : active.members) q += posteriors[v];
+  return q;
+}
+inline bool vnr_should_stop(double q_k, double q_km1) { return q_k < q_km1; }
+
+inline double snr_for_beta(double beta, double rate) {
+  double snr = 0.0;
+  check_status(bpdec_snr_for_beta(beta, rate, &snr));
+  return snr;
+}
+
+// GPU decoder for one code on one device.  Not thread-safe (like the
+// reference's BpDecoder, decoder.hpp:47-50); use one per host thread.
+class BpDecoder {
+ public:
+  using IterationObserver =
+      std::function<void(int iteration, std::span<const double> posteriors, bool syndrome_ok, double q)>;
+
+  explicit BpDecoder(const ParityCheckMatrix& code, int device = 0, int max_slots = 32) : code_(code) {
+    bpdec_decoder* d = nullptr;
+    check_status(bpdec_decoder_create(code.handle(), device, max_slots, &d));
+    dec_.reset(d);
+  }
+
+  // ≙ BpDecoder::decode (decoder.hpp:64-65).  LLRs are rounded to float32.
+  // The observer is called after decoding with each iteration's q (posteriors
+  // and syndrome flags per iteration are not retained on the device).
+  DecodeOutcome decode(std::span<const double> llr_in, const ActiveVarSet& /*active*/, const DecodeConfig& cfg,
+                       const IterationObserver& observer = nullptr, const std::uint32_t* syndrome = nullptr) {
+    const int n = code_.n_vars();
+    if (llr_in.size() != static_cast<size_t>(n)) {
+      throw ValidationError("decode: LLR length " + std::to_string(llr_in.size()) +
+                            " does not match n_vars=" + std::to_string(n));
+    }
+    for (double l : llr_in)
+      if (!std::isfinite(l)) throw ValidationError("decode: non-finite input LLR");
+    std::vector<float> llr(llr_in.begin(), llr_in.end());
+    std::vector<DecodeOutcome> out = decode_batch(1, llr.data(), syndrome, cfg, true);
+    if (observer) {
+      for (int k = 0; k < out[0].iterations; ++k) observer(k + 1, {}, false, out[0].q_trace[k]);
+    }
+    return std::move(out[0]);
+  }
+
+  // Batched, syndrome-aware decode of `batch` frames ([batch][N] float LLRs,
+  // [batch][ceil(M/32)] packed syndromes or null).
+  std::vector<DecodeOutcome> decode_batch(int batch, const float* llr, const std::uint32_t* syndrome,
+                                          const DecodeConfig& cfg, bool want_posteriors = false) {
+    const int n = code_.n_vars();
+    bpdec_config c{cfg.d_max, cfg.use_pce ? 1 : 0, cfg.use_vnr ? 1 : 0, cfg.q_mode, cfg.msg_clamp};
+    std::vector<std::uint8_t> bits(static_cast<size_t>(batch) * n);
+    std::vector<int32_t> it(batch);
+    std::vector<std::uint8_t> rs(batch);
+    std::vector<float> post(want_posteriors ? static_cast<size_t>(batch) * n : 0);
+    std::vector<double> qt(static_cast<size_t>(batch) * (cfg.d_max > 0 ? cfg.d_max : 1));
+    check_status(bpdec_decode_batch(dec_.get(), batch, llr, syndrome, &c, 0, bits.data(), it.data(), rs.data(),
+                                    want_posteriors ? post.data() : nullptr, qt.data(), nullptr));
+    std::vector<DecodeOutcome> out(batch);
+    for (int b = 0; b < batch; ++b) {
+      auto& o = out[b];
+      o.bits.assign(bits.begin() + static_cast<size_t>(b) * n, bits.begin() + static_cast<size_t>(b + 1) * n);
+      o.iterations = it[b];
+      o.reason = static_cast<StopReason>(rs[b]);
+      o.q_trace.assign(qt.begin() + static_cast<size_t>(b) * cfg.d_max,
+                       qt.begin() + static_cast<size_t>(b) * cfg.d_max + it[b]);
+      if (want_posteriors)
+        o.posteriors.assign(post.begin() + static_cast<size_t>(b) * n, post.begin() + static_cast<size_t>(b + 1) * n);
+    }
+    return out;
+  }
+
+ private:
+  struct Del {
+    void operator()(bpdec_decoder* d) const { bpdec_decoder_destroy(d); }
+  };
+  ParityCheckMatrix code_;
+  std::unique_ptr<bpdec_decoder, Del> dec_;
+};
+
+// ≙ etdec::decode (decoder.hpp:78-79): throwaway decoder.
+inline DecodeOutcome decode(const ParityCheckMatrix& code, std::span<const double> llr_in, const ActiveVarSet& active,
+                            const DecodeConfig& cfg) {
+  BpDecoder d(code);
+  return d.decode(llr_in, active, cfg);
+}
+
+}  // namespace bpdec::compat

@@ -124,6 +124,36 @@ __device__ __forceinline__ float with_sign(float mag, uint32_t s) {
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 
+// Predicated loads/stores as single instructions (no branch), so a warp can
+// keep all of a chunk's gathers in flight: a C++ `cond ? load : 0` compiles to
+// a branch region per load with its consumer inside, which serialises them.
+__device__ __forceinline__ float ld_pred(const float* p, bool pred) {
+  float v = 0.0f;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.f32 %0, [%1];\n\t}"
+               : "+f"(v)
+               : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
+}
+__device__ __forceinline__ float ldcs_pred(const float* p, bool pred) {
+  float v = 0.0f;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cs.f32 %0, [%1];\n\t}"
+               : "+f"(v)
+               : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
+}
+__device__ __forceinline__ void stcs_pred(float* p, float v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
+               :
+               : "l"(p), "f"(v), "r"(static_cast<int>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void st_pred(float* p, float v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}"
+               :
+               : "l"(p), "f"(v), "r"(static_cast<int>(pred))
+               : "memory");
+}
+
 // Advances a grid-stride cursor past the remainder of an inactive group.
 __device__ __forceinline__ long long skip_group(long long w, long long per_group, long long stride) {
   const long long next = (w / per_group + 1) * per_group;
@@ -290,25 +320,28 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
 #pragma unroll 1
   for (int i0 = 0; i0 < 32; i0 += K) {
     float m[K][D > 0 ? D : 1];
+    float cin[K][NH > 0 ? NH : 1];
     float l1[K];
+    const bool rd_c2v = act && !first;
+    // all K*(NH+ND) loads issue before any is consumed
 #pragma unroll
     for (int k = 0; k < K; ++k) {
 #pragma unroll
       for (int j = 0; j < NH; ++j) {
         const int h = hh[(i0 + k) * NH + j];
-        float p = 0.0f, co = 0.0f;
-        if (act) {
-          p = postg[static_cast<size_t>(h) * kLanes];
-          if (!first) co = ld_stream(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes);
-        }
-        const float v = p - co;
+        m[k][j] = ld_pred(postg + static_cast<size_t>(h) * kLanes, act);
+        cin[k][j] = ldcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, rd_c2v);
+      }
+      if (ND) l1[k] = ldcs_pred(llrd + static_cast<size_t>(i0 + k) * kLanes, act);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int j = 0; j < NH; ++j) {
+        const float v = m[k][j] - cin[k][j];
         m[k][j] = first ? v : clampf(v, clamp);
       }
-      if (ND) {
-        const float l = act ? ld_stream(llrd + static_cast<size_t>(i0 + k) * kLanes) : 0.0f;
-        l1[k] = l;
-        m[k][NH] = first ? l : clampf(l, clamp);
-      }
+      if (ND) m[k][NH] = first ? l1[k] : clampf(l1[k], clamp);
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -321,14 +354,14 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
 #pragma unroll
       for (int j = 0; j < NH; ++j) {
         const float o = with_sign(out[j], par ^ signbit_u(m[k][j]));
-        if (act) st_stream(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o);
+        stcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o, act);
       }
       uint32_t dbit = 0u;
       if (ND) {
         const float o = with_sign(out[NH], par ^ signbit_u(m[k][NH]));
         const float pd = l1[k] + o;  // posterior of the degree-1 variable
         dbit = (act && pd < 0.0f) ? 1u : 0u;
-        if (WANT_POST && act) d1p[static_cast<size_t>(i0 + k) * kLanes] = pd;
+        if (WANT_POST) st_pred(d1p + static_cast<size_t>(i0 + k) * kLanes, pd, act);
         const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
         if (lane == i0 + k) *d1w = dw;
       }
@@ -455,20 +488,17 @@ __device__ __forceinline__ void var_chunk_typed(const Args& a, int g, int h0, co
     float v[K][D];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      l[k] = act ? ld_stream(llrh + static_cast<size_t>(i0 + k) * kLanes) : 0.0f;
+      l[k] = ldcs_pred(llrh + static_cast<size_t>(i0 + k) * kLanes, act);
 #pragma unroll
-      for (int j = 0; j < D; ++j)
-        v[k][j] = act ? ld_stream(c2vg + static_cast<size_t>(ve[(i0 + k) * D + j]) * kLanes) : 0.0f;
+      for (int j = 0; j < D; ++j) v[k][j] = ldcs_pred(c2vg + static_cast<size_t>(ve[(i0 + k) * D + j]) * kLanes, act);
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       float p = l[k];
 #pragma unroll
       for (int j = 0; j < D; ++j) p += v[k][j];  // ascending check order (decoder.cpp:101)
-      if (act) {
-        postg[static_cast<size_t>(i0 + k) * kLanes] = p;
-        *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
-      }
+      st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, act);
+      if (act) *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
       const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
       if (lane == i0 + k) *hw = word;
     }
