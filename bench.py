@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pce-compare", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=None)
+    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period during the timed region")
     return ap.parse_args()
 
 
@@ -58,8 +59,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 200):
         self.index = index
+        self.period = period_ms
         self.proc = None
         self.lines = []
 
@@ -67,7 +69,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.period)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -192,46 +194,41 @@ def emit(obj):
 
 # ------------------------------------------------------ reference arm --
 def run_reference(args):
-    rank, world, local, dist = dist_setup(args.gpus)
+    """Rank 0 alone times the reference CPU decoder; other ranks exit."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
     import paper_2507_03509_b200 as P
     w = P.WORKLOADS[args.workload]
-    if rank != 0:
-        barrier(dist)
+    import oracle
+    if not oracle.reference_available():
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libetdec_ref.so not built (needs /root/reference)"})
         return
-    try:
-        import oracle
-        if not oracle.reference_available():
-            emit({"impl": "reference", "unavailable": "oracle/_ref/libetdec_ref.so not built (needs /root/reference)"})
-            barrier(dist)
-            return
-        code = w.make_code()
-        threads = os.cpu_count() or 1
-        frames = args.cpu_frames or threads
-        snr = P.snr_for_beta(args.beta, code.rate())
-        llr, x, _ = P.sample_frames(code, snr, P.FRAME_SEED, 0, frames)
-        leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float64)
-        times, iters = [], []
-        for k in range(args.warmup + args.steps):
-            dt, it, _ = cpu_reference_time(code, leq, w.d_max, threads)
-            if k >= args.warmup:
-                times.append(dt)
-                iters.append(it)
-        T = float(np.sum(times))
-        value = float(np.sum(iters)) * code.n_edges / T
-        sample = (f"{frames} frames of {w.name} (beta={args.beta}, VNR+PCE, D_max={w.d_max}) per step, "
-                  f"all-zero-equivalent inputs L*(1-2x), s=0 (the reference's semantics)")
-        emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-              "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
-              "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-              "data": "synthetic (seeded BASELINE generator)",
-              "config": {"workload": w.name, "frames_per_step": frames, "beta": args.beta, "d_max": w.d_max,
-                         "et": "vnr+pce", "threads": threads},
-              "d_bar": float(np.sum(iters)) / (frames * len(times)),
-              "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                               "sample": sample},
-              "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
-    finally:
-        barrier(dist)
+    code = w.make_code()
+    threads = os.cpu_count() or 1
+    frames = args.cpu_frames or threads
+    snr = P.snr_for_beta(args.beta, code.rate())
+    llr, x, _ = P.sample_frames(code, snr, P.FRAME_SEED, 0, frames)
+    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float64)
+    times, iters = [], []
+    for k in range(args.warmup + args.steps):
+        dt, it, _ = cpu_reference_time(code, leq, w.d_max, threads)
+        if k >= args.warmup:
+            times.append(dt)
+            iters.append(it)
+    T = float(np.sum(times))
+    value = float(np.sum(iters)) * code.n_edges / T
+    sample = (f"{frames} frames of {w.name} (beta={args.beta}, VNR+PCE, D_max={w.d_max}) per step, "
+              f"all-zero-equivalent inputs L*(1-2x), s=0 (the reference's semantics)")
+    emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic (seeded BASELINE generator)",
+          "config": {"workload": w.name, "frames_per_step": frames, "beta": args.beta, "d_max": w.d_max,
+                     "et": "vnr+pce", "threads": threads},
+          "d_bar": float(np.sum(iters)) / (frames * len(times)),
+          "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                           "sample": sample},
+          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
 # ------------------------------------------------------------- our arm --
@@ -269,9 +266,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    dec.reset_profile()
-    dec.set_profiling(True)
-    clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local, args.clock_ms)
     barrier(dist)
     torch.cuda.synchronize()
     clocks.start()
@@ -289,6 +284,14 @@ def run_ours(args):
     launches = dec.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     barrier(dist)
+    # per-kernel CUDA-event timing: the same K steps again with an event pair
+    # around every launch (kept out of the headline timing: the events add
+    # host work per launch)
+    dec.reset_profile()
+    dec.set_profiling(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     prof = dec.profile()
     dec.set_profiling(False)
     T = max_over_ranks(ms / 1e3, dist)

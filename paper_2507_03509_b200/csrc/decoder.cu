@@ -72,7 +72,8 @@ struct Args {
   const int32_t* vmap;      // [N] original var -> h (>=0) or -1-d (degree 1)
   const int32_t* dorig;     // [N] device item (H then D1) -> original var
   const int32_t* corig;     // [M] device check -> original check
-  const int32_t* ctype;     // [ceil(M/32)] chunk type NH*8+ND (homogeneous, full) or -1
+  const int4* ctype;        // [ceil(M/32)] {type NH*8+ND (homogeneous full chunk) or -1,
+                            //  first hi edge, first degree-1 row, hi edge end}
   const int32_t* vtype;     // [ceil(NV/32)] chunk degree (homogeneous, full) or -1
   // state
   int32_t G;
@@ -398,26 +399,28 @@ __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
     const bool act = (amask >> lane) & 1u;
     const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
     const bool first = (it == 1);
-    const int type = kStage ? __ldg(&a.ctype[ch]) : -1;
+    const int4 cdk = __ldg(&a.ctype[ch]);
+    const int type = kStage ? cdk.x : -1;
     // degree-1 checks only change in a frame's first iteration
     if ((type == 1 || type == 8) && !__any_sync(0xffffffffu, act && first)) {
       w += nwarps;
       continue;
     }
     __syncwarp();
-    if (lane < nc) {
-      s_desc[wi][lane] = __ldg(&a.cdesc[c0 + lane]);
-      s_syn[wi][lane] = a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane];
+    if (lane < nc) s_syn[wi][lane] = a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane];
+    int hb0 = cdk.y;
+    if (type < 0) {  // generic chunk: per-check descriptors
+      if (lane < nc) s_desc[wi][lane] = __ldg(&a.cdesc[c0 + lane]);
+      __syncwarp();
+      hb0 = s_desc[wi][0].x;
+    }
+    if (kStage) {
+      const int nhh = cdk.w - hb0;
+      for (int i = lane; i < nhh; i += 32) s_hh[wi][i] = __ldg(&a.chk_hi_h[hb0 + i]);
     }
     __syncwarp();
-    const int hb0 = s_desc[wi][0].x;
-    if (kStage) {
-      const int nhh = s_desc[wi][nc - 1].y - hb0;
-      for (int i = lane; i < nhh; i += 32) s_hh[wi][i] = __ldg(&a.chk_hi_h[hb0 + i]);
-      __syncwarp();
-    }
     uint32_t synw = 0u, d1w = 0u;
-    const int db0 = s_desc[wi][0].z;
+    const int db0 = cdk.z;
     bool typed = true;
     switch (type) {
 #define BPDEC_TYPED(NH_, ND_)                                                                       \
@@ -425,6 +428,8 @@ __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
     if (NH_ + ND_ <= MAXD)                                                                          \
       check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], lane, act, first, \
                                              &synw, &d1w);                                          \
+    else                                                                                            \
+      typed = false;                                                                                \
     break;
       BPDEC_TYPED(0, 1)
       BPDEC_TYPED(1, 0)
@@ -637,18 +642,26 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
 // Warp = one slot.  q^(k) = fixed-order double sum of the tile partials;
 // decision order PCE, then VNR (k >= 2, strict), then d_max
 // (decoder.cpp:114-123).
-__global__ void __launch_bounds__(kThreads) k_terminate(const Args a) {
+__global__ void __launch_bounds__(1024) k_terminate(const Args a) {
+  // block = one group; warp w sums tiles w, w+32, ... for every slot (lane),
+  // coalesced over lanes; warp 0 then adds the 32 warp sums in order.
+  __shared__ double red[32][kLanes];
+  const int g = blockIdx.x;
   const int lane = threadIdx.x & 31;
-  const int s = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
-  if (s >= a.G * kLanes) return;
-  const int g = s >> 5, l = s & 31;
-  const uint32_t bit = 1u << l;
-  if (!(a.group_active[g] & bit)) return;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t amask = a.group_active[g];
+  if (amask == 0u) return;
   double q = 0.0;
-  for (int t = lane; t < a.n_tiles; t += kLanes) q += a.q_part[(static_cast<size_t>(g) * a.n_tiles + t) * kLanes + l];
+  for (int t = warp; t < a.n_tiles; t += 32) q += a.q_part[(static_cast<size_t>(g) * a.n_tiles + t) * kLanes + lane];
+  red[warp][lane] = q;
+  __syncthreads();
+  if (warp != 0) return;
+  q = red[0][lane];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
-  if (lane != 0) return;
+  for (int k = 1; k < 32; ++k) q += red[k][lane];
+  const uint32_t bit = 1u << lane;
+  if (!(amask & bit)) return;
+  const int s = g * kLanes + lane;
   const int it = a.slot_iter[s];
   const int f = a.slot_frame[s];
   atomicAdd(a.frame_iters, 1ull);
@@ -684,6 +697,11 @@ __global__ void __launch_bounds__(kThreads) k_terminate(const Args a) {
 // consecutive variables so packed bit words come from one ballot.
 template <bool WANT_POST>
 __global__ void __launch_bounds__(kThreads) k_extract(const Args a) {
+  {
+    uint32_t any = 0u;
+    for (int g = 0; g < a.G; ++g) any |= a.stopped[g];
+    if (any == 0u) return;  // nothing stopped this step
+  }
   const int lane = threadIdx.x & 31;
   const long long npad = (static_cast<long long>(a.N) + 31) / 32 * 32;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -729,6 +747,11 @@ __global__ void __launch_bounds__(kThreads) k_extract(const Args a) {
 // bits, slot state.  Grid: (item tiles of 32) + (check tiles) + 1 state block.
 __global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks, int check_blocks) {
   __shared__ float tile[32][33];
+  {
+    uint32_t any = 0u;
+    for (int g = 0; g < a.G; ++g) any |= a.load_mask[g];
+    if (any == 0u) return;  // no slot to (re)fill this step
+  }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int b = blockIdx.x;
@@ -1015,15 +1038,25 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
     cdesc[cd] = d;
   }
   if (max_check_deg > 256) throw ValidationError("decoder: check degree above 256 is not supported");
-  // chunk types: homogeneous full chunks of 32 checks get NH*8+ND, else -1
-  std::vector<int32_t> ctype((M + 31) / 32, -1);
+  // chunk descriptors: {NH*8+ND for a homogeneous full chunk of 32 checks of a
+  // typed-path shape else -1, first hi edge, first degree-1 row, hi edge end}
+  std::vector<int4> ctype((M + 31) / 32);
   for (size_t k = 0; k < ctype.size(); ++k) {
     const int32_t c0 = static_cast<int32_t>(k * 32);
-    if (c0 + 32 > M) continue;
-    const int32_t t = cnh[corig[c0]] * 8 + cnd[corig[c0]];
-    bool same = cnd[corig[c0]] <= 1 && cnh[corig[c0]] <= 7;
-    for (int32_t i = 1; i < 32 && same; ++i) same = cnh[corig[c0 + i]] * 8 + cnd[corig[c0 + i]] == t;
-    if (same) ctype[k] = t;
+    const int32_t c1 = std::min<int32_t>(M, c0 + 32);
+    int4 t;
+    t.x = -1;
+    t.y = cdesc[c0].x;
+    t.z = cdesc[c0].z;
+    t.w = cdesc[c1 - 1].y;
+    if (c1 - c0 == 32) {
+      const int32_t t0 = cnh[corig[c0]] * 8 + cnd[corig[c0]];
+      bool same = true;
+      for (int32_t i = 1; i < 32 && same; ++i) same = cnh[corig[c0 + i]] * 8 + cnd[corig[c0 + i]] == t0;
+      const bool shape_ok = t0 == 1 || t0 == 8 || t0 == 9 || t0 == 16 || t0 == 17 || t0 == 24 || t0 == 25 || t0 == 48;
+      if (same && shape_ok) t.x = t0;
+    }
+    ctype[k] = t;
   }
   const int64_t EH = static_cast<int64_t>(chk_hi_h.size());
   std::vector<int32_t> vptr(NV + 1, 0), vedge;
@@ -1069,7 +1102,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.vmap = up(vmap, static_cast<int32_t*>(nullptr));
   a.dorig = up(dorig, static_cast<int32_t*>(nullptr));
   a.corig = up(corig, static_cast<int32_t*>(nullptr));
-  a.ctype = up(ctype, static_cast<int32_t*>(nullptr));
+  a.ctype = up(ctype, static_cast<int4*>(nullptr));
   a.vtype = up(vtype, static_cast<int32_t*>(nullptr));
   d_check_ptr = up(code.check_ptr, static_cast<int32_t*>(nullptr));
   d_check_vars = up(code.check_vars, static_cast<int32_t*>(nullptr));
@@ -1175,7 +1208,7 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
       k_var<1><<<grid_var, kThreads, 0, st>>>(a);
   });
   if (a.use_pce) launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 0, st>>>(a); });
-  launch(kTerm, st, [&] { k_terminate<<<(G * kLanes * 32 + kThreads - 1) / kThreads, kThreads, 0, st>>>(a); });
+  launch(kTerm, st, [&] { k_terminate<<<G, 1024, 0, st>>>(a); });
   launch(kExtract, st, [&] {
     if (want_post)
       k_extract<true><<<grid_extract, kThreads, 0, st>>>(a);
