@@ -37,7 +37,7 @@ E_BYTES_MODEL_A = None  # filled per code: 16E + 4N + (N+M)/8 per frame-iteratio
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg2")
@@ -72,6 +72,11 @@ class ClockSampler:
                  "-lms", str(self.period)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's NVML start-up must not overlap the timed region
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10:
+                time.sleep(0.05)
+            self.lines.clear()
         except OSError:
             self.proc = None
 

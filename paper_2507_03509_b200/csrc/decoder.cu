@@ -58,6 +58,7 @@ constexpr int kLanes = 32;
 constexpr int kQTile = 256;     // variables per q partial sum (code-fixed order)
 constexpr int kVarWarps = 8;    // warps per k_var block; kQTile = kVarWarps * 32
 constexpr int kThreads = 256;
+constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
 enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kLoad = 4, kExtract = 5, kNumKernels = 6 };
 
 // ------------------------------------------------------------ arguments --
@@ -128,7 +129,7 @@ __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 // Predicated loads/stores as single instructions (no branch), so a warp can
 // keep all of a chunk's gathers in flight: a C++ `cond ? load : 0` compiles to
 // a branch region per load with its consumer inside, which serialises them.
-__device__ __forceinline__ float ld_pred(const float* p, bool pred) {
+[[maybe_unused]] __device__ __forceinline__ float ld_pred(const float* p, bool pred) {
   float v = 0.0f;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.f32 %0, [%1];\n\t}"
                : "+f"(v)
@@ -307,78 +308,154 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
 
 // Typed chunk: 32 checks, each with NH edges to degree>=2 variables (c2v rows
 // hb + 32-check-local i*NH + j) and ND <= 1 degree-1 edge (row db + i).
+// K checks form a batch of R = K*(2*NH+ND) message rows.  Batches are
+// copied asynchronously (cp.async, one 4-byte element per lane per row, so a
+// warp moves whole 128-byte rows) into a two-stage per-warp shared-memory
+// ring: the rows of batch b+1 are in flight while batch b is computed from
+// shared memory, and no registers are held for data in flight.  Each lane
+// only reads back the elements it copied itself, so cp.async.wait_group is
+// the only synchronisation needed.
+constexpr int kStageRows = 24;  // rows per batch stage (max over typed shapes)
+
+template <int NH, int ND>
+struct CheckShape {
+  static constexpr int RPC = 2 * NH + ND;  // rows per check
+  static constexpr int K = RPC == 0 ? 32 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
+  static_assert(K * RPC <= kStageRows, "stage too small");
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool pred) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+               "r"(pred ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4_ef(float* sdst, const float* gsrc, bool pred, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n" ::"r"(smem_u32(sdst)),
+               "l"(gsrc), "r"(pred ? 4 : 0), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+
+template <int NH, int ND>
+__device__ __forceinline__ void check_batch_issue(float* stage, const float* postg, const float* c2vg,
+                                                  const float* llrd, const int32_t* hh, int i0, bool act,
+                                                  bool rd_c2v, uint64_t pol) {
+  constexpr int K = CheckShape<NH, ND>::K;
+  constexpr int RPC = CheckShape<NH, ND>::RPC;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const int h = hh[(i0 + k) * NH + j];
+      cp_async4(stage + (k * RPC + j) * kLanes, postg + static_cast<size_t>(h) * kLanes, act);
+      cp_async4_ef(stage + (k * RPC + NH + j) * kLanes, c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes,
+                   rd_c2v, pol);
+    }
+    if (ND) cp_async4_ef(stage + (k * RPC + 2 * NH) * kLanes, llrd + static_cast<size_t>(i0 + k) * kLanes, act, pol);
+  }
+  cp_async_commit();
+}
+
+template <int NH, int ND, bool WANT_POST>
+__device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p,
+                                                    const uint32_t* ssyn, int i0, int lane, bool act, bool first,
+                                                    float clamp, uint32_t* synw, uint32_t* d1w) {
+  constexpr int D = NH + ND;
+  constexpr int K = CheckShape<NH, ND>::K;
+  constexpr int RPC = CheckShape<NH, ND>::RPC;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    float m[D > 0 ? D : 1];
+    float l = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const float v = stage[(k * RPC + j) * kLanes] - stage[(k * RPC + NH + j) * kLanes];
+      m[j] = first ? v : clampf(v, clamp);
+    }
+    if (ND) {
+      l = stage[(k * RPC + 2 * NH) * kLanes];
+      m[NH] = first ? l : clampf(l, clamp);
+    }
+    const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
+    uint32_t par = sbit;
+#pragma unroll
+    for (int j = 0; j < D; ++j) par ^= signbit_u(m[j]);
+    float out[D > 0 ? D : 1];
+    check_magnitudes<D>(m, out, clamp);
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const float o = with_sign(out[j], par ^ signbit_u(m[j]));
+      stcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o, act);
+    }
+    uint32_t dbit = 0u;
+    if (ND) {
+      const float o = with_sign(out[NH], par ^ signbit_u(m[NH]));
+      const float pd = l + o;  // posterior of the degree-1 variable
+      dbit = (act && pd < 0.0f) ? 1u : 0u;
+      if (WANT_POST) st_pred(d1p + static_cast<size_t>(i0 + k) * kLanes, pd, act);
+      const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
+      if (lane == i0 + k) *d1w = dw;
+    }
+    const uint32_t sw = __ballot_sync(0xffffffffu, sbit ^ dbit);
+    if (lane == i0 + k) *synw = sw;
+  }
+}
+
 template <int NH, int ND, bool WANT_POST>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
-                                                  const uint32_t* ssyn, int lane, bool act, bool first,
+                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                   uint32_t* synw, uint32_t* d1w) {
-  constexpr int D = NH + ND;
-  constexpr int K = D <= 2 ? 8 : (D <= 4 ? 4 : 2);
+  constexpr int K = CheckShape<NH, ND>::K;
   const float* postg = a.post + static_cast<size_t>(g) * a.NV * kLanes + lane;
   float* c2vg = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes + lane;
   const float* llrd = a.llr_d + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane;
   float* d1p = WANT_POST ? a.d1post + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane : nullptr;
   const float clamp = a.clamp;
+  const bool rd_c2v = act && !first;
+  const uint64_t pol = policy_evict_first();
+  float* st0 = ring + lane;
+  float* st1 = ring + kStageRows * kLanes + lane;
+  check_batch_issue<NH, ND>(st0, postg, c2vg, llrd, hh, 0, act, rd_c2v, pol);
 #pragma unroll 1
-  for (int i0 = 0; i0 < 32; i0 += K) {
-    float m[K][D > 0 ? D : 1];
-    float cin[K][NH > 0 ? NH : 1];
-    float l1[K];
-    const bool rd_c2v = act && !first;
-    // all K*(NH+ND) loads issue before any is consumed
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-#pragma unroll
-      for (int j = 0; j < NH; ++j) {
-        const int h = hh[(i0 + k) * NH + j];
-        m[k][j] = ld_pred(postg + static_cast<size_t>(h) * kLanes, act);
-        cin[k][j] = ldcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, rd_c2v);
-      }
-      if (ND) l1[k] = ldcs_pred(llrd + static_cast<size_t>(i0 + k) * kLanes, act);
+  for (int i0 = 0; i0 < 32; i0 += 2 * K) {
+    if (i0 + K < 32) {
+      check_batch_issue<NH, ND>(st1, postg, c2vg, llrd, hh, i0 + K, act, rd_c2v, pol);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-#pragma unroll
-      for (int j = 0; j < NH; ++j) {
-        const float v = m[k][j] - cin[k][j];
-        m[k][j] = first ? v : clampf(v, clamp);
-      }
-      if (ND) m[k][NH] = first ? l1[k] : clampf(l1[k], clamp);
+    check_batch_compute<NH, ND, WANT_POST>(st0, c2vg, d1p, ssyn, i0, lane, act, first, clamp, synw, d1w);
+    if (i0 + K >= 32) break;
+    if (i0 + 2 * K < 32) {
+      check_batch_issue<NH, ND>(st0, postg, c2vg, llrd, hh, i0 + 2 * K, act, rd_c2v, pol);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
-      uint32_t par = sbit;
-#pragma unroll
-      for (int j = 0; j < D; ++j) par ^= signbit_u(m[k][j]);
-      float out[D > 0 ? D : 1];
-      check_magnitudes<D>(m[k], out, clamp);
-#pragma unroll
-      for (int j = 0; j < NH; ++j) {
-        const float o = with_sign(out[j], par ^ signbit_u(m[k][j]));
-        stcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o, act);
-      }
-      uint32_t dbit = 0u;
-      if (ND) {
-        const float o = with_sign(out[NH], par ^ signbit_u(m[k][NH]));
-        const float pd = l1[k] + o;  // posterior of the degree-1 variable
-        dbit = (act && pd < 0.0f) ? 1u : 0u;
-        if (WANT_POST) st_pred(d1p + static_cast<size_t>(i0 + k) * kLanes, pd, act);
-        const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
-        if (lane == i0 + k) *d1w = dw;
-      }
-      const uint32_t sw = __ballot_sync(0xffffffffu, sbit ^ dbit);
-      if (lane == i0 + k) *synw = sw;
-    }
+    check_batch_compute<NH, ND, WANT_POST>(st1, c2vg, d1p, ssyn, i0 + K, lane, act, first, clamp, synw, d1w);
   }
 }
 
 template <int MAXD, bool WANT_POST>
-__global__ void __launch_bounds__(kThreads) k_check(const Args a) {
+__global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   constexpr bool kStage = MAXD <= 16;
   constexpr int kHH = kStage ? 32 * MAXD : 1;
-  __shared__ int4 s_desc[kThreads / 32][32];
-  __shared__ uint32_t s_syn[kThreads / 32][32];
-  __shared__ int32_t s_hh[kThreads / 32][kHH];
+  __shared__ int4 s_desc[kCheckThreads / 32][32];
+  __shared__ uint32_t s_syn[kCheckThreads / 32][32];
+  __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
+  __shared__ __align__(16) float s_ring[kCheckThreads / 32][2 * kStageRows * kLanes];
   if (blockIdx.x == 0 && threadIdx.x < a.G) a.fail[threadIdx.x] = 0u;
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
@@ -426,8 +503,8 @@ __global__ void __launch_bounds__(kThreads) k_check(const Args a) {
 #define BPDEC_TYPED(NH_, ND_)                                                                       \
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
-      check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], lane, act, first, \
-                                             &synw, &d1w);                                          \
+      check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
+                                             first, &synw, &d1w);                                   \
     else                                                                                            \
       typed = false;                                                                                \
     break;
@@ -1142,7 +1219,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   for (auto& e : ring_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   const int sms = prop.multiProcessorCount;
-  grid_check = sms * 8;
+  grid_check = sms * 16;
   grid_var = sms * 8;
   grid_syn = sms * 8;
   grid_extract = sms * 4;
@@ -1188,9 +1265,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
 #define BPDEC_CHECK_CASE(D)                                                                 \
   if (md <= D) {                                                                            \
     if (want_post)                                                                          \
-      k_check<D, true><<<grid_check, kThreads, 0, st>>>(a);                                 \
+      k_check<D, true><<<grid_check, kCheckThreads, 0, st>>>(a);                                 \
     else                                                                                    \
-      k_check<D, false><<<grid_check, kThreads, 0, st>>>(a);                                \
+      k_check<D, false><<<grid_check, kCheckThreads, 0, st>>>(a);                                \
     return;                                                                                 \
   }
     BPDEC_CHECK_CASE(3)
