@@ -55,8 +55,8 @@ namespace {
   } while (0)
 
 constexpr int kLanes = 32;
-constexpr int kQTile = 256;     // variables per q partial sum (code-fixed order)
-constexpr int kVarWarps = 8;    // warps per k_var block; kQTile = kVarWarps * 32
+constexpr int kQTile = 128;     // variables per q partial sum (code-fixed order)
+constexpr int kVarWarps = 4;    // warps per k_var block; kQTile = kVarWarps * 32
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
 enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kLoad = 4, kExtract = 5, kNumKernels = 6 };
@@ -136,7 +136,7 @@ __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
                : "l"(p), "r"(static_cast<int>(pred)));
   return v;
 }
-__device__ __forceinline__ float ldcs_pred(const float* p, bool pred) {
+[[maybe_unused]] __device__ __forceinline__ float ldcs_pred(const float* p, bool pred) {
   float v = 0.0f;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cs.f32 %0, [%1];\n\t}"
                : "+f"(v)
@@ -315,12 +315,25 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
 // shared memory, and no registers are held for data in flight.  Each lane
 // only reads back the elements it copied itself, so cp.async.wait_group is
 // the only synchronisation needed.
-constexpr int kStageRows = 24;  // rows per batch stage (max over typed shapes)
+constexpr int kStageRows = 12;  // rows per batch stage (check shapes)
+constexpr int kStages = 3;      // ring depth: two batches in flight while one is computed
+constexpr int kRingRows = kStages * kStageRows;
+
+// Waits until at most `pending` (0..2) committed cp.async groups are in flight.
+__device__ __forceinline__ void cp_async_wait_upto(int pending) {
+  if (pending >= 2) {
+    asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+  } else if (pending == 1) {
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+}
 
 template <int NH, int ND>
 struct CheckShape {
   static constexpr int RPC = 2 * NH + ND;  // rows per check
-  static constexpr int K = RPC == 0 ? 32 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
+  static constexpr int K = RPC == 0 ? 8 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
   static_assert(K * RPC <= kStageRows, "stage too small");
 };
 
@@ -418,6 +431,7 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
                                                   const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                   uint32_t* synw, uint32_t* d1w) {
   constexpr int K = CheckShape<NH, ND>::K;
+  constexpr int NB = 32 / K;
   const float* postg = a.post + static_cast<size_t>(g) * a.NV * kLanes + lane;
   float* c2vg = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes + lane;
   const float* llrd = a.llr_d + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane;
@@ -425,26 +439,20 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
   const float clamp = a.clamp;
   const bool rd_c2v = act && !first;
   const uint64_t pol = policy_evict_first();
-  float* st0 = ring + lane;
-  float* st1 = ring + kStageRows * kLanes + lane;
-  check_batch_issue<NH, ND>(st0, postg, c2vg, llrd, hh, 0, act, rd_c2v, pol);
+  float* const ring_l = ring + lane;
+  constexpr int NS = kStages;
+#pragma unroll
+  for (int p = 0; p < NS - 1; ++p)
+    if (p < NB)
+      check_batch_issue<NH, ND>(ring_l + p * kStageRows * kLanes, postg, c2vg, llrd, hh, p * K, act, rd_c2v, pol);
 #pragma unroll 1
-  for (int i0 = 0; i0 < 32; i0 += 2 * K) {
-    if (i0 + K < 32) {
-      check_batch_issue<NH, ND>(st1, postg, c2vg, llrd, hh, i0 + K, act, rd_c2v, pol);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    check_batch_compute<NH, ND, WANT_POST>(st0, c2vg, d1p, ssyn, i0, lane, act, first, clamp, synw, d1w);
-    if (i0 + K >= 32) break;
-    if (i0 + 2 * K < 32) {
-      check_batch_issue<NH, ND>(st0, postg, c2vg, llrd, hh, i0 + 2 * K, act, rd_c2v, pol);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    check_batch_compute<NH, ND, WANT_POST>(st1, c2vg, d1p, ssyn, i0 + K, lane, act, first, clamp, synw, d1w);
+  for (int b = 0; b < NB; ++b) {
+    if (b + NS - 1 < NB)
+      check_batch_issue<NH, ND>(ring_l + ((b + NS - 1) % NS) * kStageRows * kLanes, postg, c2vg, llrd, hh,
+                                (b + NS - 1) * K, act, rd_c2v, pol);
+    cp_async_wait_upto(min(NS - 1, NB - 1 - b));
+    check_batch_compute<NH, ND, WANT_POST>(ring_l + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
+                                           lane, act, first, clamp, synw, d1w);
   }
 }
 
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   __shared__ int4 s_desc[kCheckThreads / 32][32];
   __shared__ uint32_t s_syn[kCheckThreads / 32][32];
   __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
-  __shared__ __align__(16) float s_ring[kCheckThreads / 32][2 * kStageRows * kLanes];
+  __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRingRows * kLanes];
   if (blockIdx.x == 0 && threadIdx.x < a.G) a.fail[threadIdx.x] = 0u;
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
@@ -552,38 +560,76 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
 // Variables are sorted by degree in the device layout, so a chunk is almost
 // always homogeneous: its CSC slice (edge ids of its c2v rows) is staged in
 // shared memory and the typed path gathers K variables' messages at once
-// before the (ordered) sums.  A block covers kQTile = 256 variables and the
+// before the (ordered) sums.  A block covers kQTile = 128 variables and the
 // tile's q partial is the warp partials summed in warp order — a summation
 // order fixed by the code (not by slots, batch size or GPU count).
 constexpr int kVarStage = 32 * 24;  // staged edge ids per warp
 
+// Typed chunk of 32 degree-D variables: K variables per batch of K*(D+1)
+// rows (channel LLR + D messages), copied with cp.async into the per-warp
+// two-stage ring while the previous batch is summed from shared memory.
+template <int D>
+struct VarShape {
+  static constexpr int RPV = D + 1;
+  static constexpr int K = kStageRows / RPV >= 8 ? 8 : (kStageRows / RPV >= 4 ? 4 : (kStageRows / RPV >= 2 ? 2 : 1));
+  static constexpr int ROWS = K * RPV;                                     // rows per batch
+  static constexpr int NS = kRingRows / ROWS >= 3 ? 3 : kRingRows / ROWS;  // ring stages
+  static_assert(NS >= 1, "variable degree too large for the ring");
+};
+
+template <int D>
+__device__ __forceinline__ void var_batch_issue(float* stage, const float* llrh, const float* c2vg, const int32_t* ve,
+                                                int i0, bool act, uint64_t pol) {
+  constexpr int K = VarShape<D>::K;
+  constexpr int RPV = VarShape<D>::RPV;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    cp_async4_ef(stage + (k * RPV) * kLanes, llrh + static_cast<size_t>(i0 + k) * kLanes, act, pol);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      cp_async4_ef(stage + (k * RPV + 1 + j) * kLanes, c2vg + static_cast<size_t>(ve[(i0 + k) * D + j]) * kLanes,
+                   act, pol);
+  }
+  cp_async_commit();
+}
+
 template <int D, int QMODE>
-__device__ __forceinline__ void var_chunk_typed(const Args& a, int g, int h0, const int32_t* ve, int lane,
-                                                bool act, double* acc, uint32_t* hw) {
-  constexpr int K = D <= 4 ? 4 : (D <= 8 ? 2 : 1);
+__device__ __forceinline__ void var_batch_compute(const float* stage, float* postg, int i0, int lane, bool act,
+                                                  double* acc, uint32_t* hw) {
+  constexpr int K = VarShape<D>::K;
+  constexpr int RPV = VarShape<D>::RPV;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    float p = stage[(k * RPV) * kLanes];
+#pragma unroll
+    for (int j = 0; j < D; ++j) p += stage[(k * RPV + 1 + j) * kLanes];  // ascending check order (decoder.cpp:101)
+    st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, act);
+    if (act) *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+    const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
+    if (lane == i0 + k) *hw = word;
+  }
+}
+
+template <int D, int QMODE>
+__device__ __forceinline__ void var_chunk_typed(const Args& a, int g, int h0, const int32_t* ve, float* ring,
+                                                int lane, bool act, double* acc, uint32_t* hw) {
+  constexpr int K = VarShape<D>::K;
+  constexpr int NB = 32 / K;
   const float* llrh = a.llr_h + (static_cast<size_t>(g) * a.NH + h0) * kLanes + lane;
   const float* c2vg = a.c2v + static_cast<size_t>(g) * a.EH * kLanes + lane;
   float* postg = a.post + (static_cast<size_t>(g) * a.NV + h0) * kLanes + lane;
+  const uint64_t pol = policy_evict_first();
+  float* const ring_l = ring + lane;
+  constexpr int NS = VarShape<D>::NS;
+  constexpr int RS = VarShape<D>::ROWS * kLanes;  // stage stride
+#pragma unroll
+  for (int p = 0; p < NS - 1; ++p)
+    if (p < NB) var_batch_issue<D>(ring_l + p * RS, llrh, c2vg, ve, p * K, act, pol);
 #pragma unroll 1
-  for (int i0 = 0; i0 < 32; i0 += K) {
-    float l[K];
-    float v[K][D];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      l[k] = ldcs_pred(llrh + static_cast<size_t>(i0 + k) * kLanes, act);
-#pragma unroll
-      for (int j = 0; j < D; ++j) v[k][j] = ldcs_pred(c2vg + static_cast<size_t>(ve[(i0 + k) * D + j]) * kLanes, act);
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      float p = l[k];
-#pragma unroll
-      for (int j = 0; j < D; ++j) p += v[k][j];  // ascending check order (decoder.cpp:101)
-      st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, act);
-      if (act) *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
-      const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
-      if (lane == i0 + k) *hw = word;
-    }
+  for (int b = 0; b < NB; ++b) {
+    if (b + NS - 1 < NB) var_batch_issue<D>(ring_l + ((b + NS - 1) % NS) * RS, llrh, c2vg, ve, (b + NS - 1) * K, act, pol);
+    cp_async_wait_upto(min(NS - 1, NB - 1 - b));
+    var_batch_compute<D, QMODE>(ring_l + (b % NS) * RS, postg, b * K, lane, act, acc, hw);
   }
 }
 
@@ -604,10 +650,11 @@ __device__ __forceinline__ float var_sum(const Args& a, size_t gl, size_t ge, in
 }
 
 template <int QMODE>
-__global__ void __launch_bounds__(kThreads) k_var(const Args a) {
+__global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
   __shared__ double red[kVarWarps][kLanes];
   __shared__ int32_t s_ptr[kVarWarps][33];
   __shared__ int32_t s_ve[kVarWarps][kVarStage];
+  __shared__ __align__(16) float s_ring[kVarWarps][kRingRows * kLanes];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const long long total = static_cast<long long>(a.G) * a.n_tiles;
@@ -643,7 +690,7 @@ __global__ void __launch_bounds__(kThreads) k_var(const Args a) {
       switch (vt) {
 #define BPDEC_VTYPED(D_) \
   case D_:               \
-    var_chunk_typed<D_, QMODE>(a, g, h0, ve, lane, act, &acc, &hw); \
+    var_chunk_typed<D_, QMODE>(a, g, h0, ve, s_ring[warp], lane, act, &acc, &hw); \
     break;
         BPDEC_VTYPED(2)
         BPDEC_VTYPED(3)
@@ -1220,7 +1267,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
 
   const int sms = prop.multiProcessorCount;
   grid_check = sms * 16;
-  grid_var = sms * 8;
+  grid_var = sms * 16;
   grid_syn = sms * 8;
   grid_extract = sms * 4;
   load_item_blocks = sms * 4;
@@ -1280,9 +1327,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
   });
   launch(kVar, st, [&] {
     if (a.q_mode == 0)
-      k_var<0><<<grid_var, kThreads, 0, st>>>(a);
+      k_var<0><<<grid_var, kVarWarps * 32, 0, st>>>(a);
     else
-      k_var<1><<<grid_var, kThreads, 0, st>>>(a);
+      k_var<1><<<grid_var, kVarWarps * 32, 0, st>>>(a);
   });
   if (a.use_pce) launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 0, st>>>(a); });
   launch(kTerm, st, [&] { k_terminate<<<G, 1024, 0, st>>>(a); });
