@@ -350,6 +350,18 @@ __device__ __forceinline__ void cp_async4_ef(float* sdst, const float* gsrc, boo
                "l"(gsrc), "r"(pred ? 4 : 0), "l"(pol)
                : "memory");
 }
+// 16-byte copy: lane l moves floats [4(l%8), 4(l%8)+4) of row (l/8) of a
+// 4-row group, so one warp instruction moves four 128-byte rows.
+__device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+               "r"(pred ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16_ef(float* sdst, const float* gsrc, bool pred, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(smem_u32(sdst)),
+               "l"(gsrc), "r"(pred ? 16 : 0), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -361,22 +373,33 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
+// Stage layout for a batch of K checks: [K*NH posterior rows][K*NH c2v rows]
+// [K*ND llr rows].  `q4` = this lane's 16-byte quarter within a row group:
+// row offset (lane/8), float offset 4*(lane%8); `qact` = any of the 4 frames
+// covered by that quarter is active.
 template <int NH, int ND>
-__device__ __forceinline__ void check_batch_issue(float* stage, const float* postg, const float* c2vg,
-                                                  const float* llrd, const int32_t* hh, int i0, bool act,
-                                                  bool rd_c2v, uint64_t pol) {
+__device__ __forceinline__ void check_batch_issue(float* stage, const float* post0, const float* c2v0,
+                                                  const float* llr0, const int32_t* hh, int i0, int lrow, int lcol,
+                                                  bool qact, bool qc2v, uint64_t pol) {
   constexpr int K = CheckShape<NH, ND>::K;
-  constexpr int RPC = CheckShape<NH, ND>::RPC;
+  constexpr int NPH = K * NH;  // posterior / c2v rows
+  constexpr int NPD = K * ND;  // degree-1 rows
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-#pragma unroll
-    for (int j = 0; j < NH; ++j) {
-      const int h = hh[(i0 + k) * NH + j];
-      cp_async4(stage + (k * RPC + j) * kLanes, postg + static_cast<size_t>(h) * kLanes, act);
-      cp_async4_ef(stage + (k * RPC + NH + j) * kLanes, c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes,
-                   rd_c2v, pol);
+  for (int r0 = 0; r0 < NPH; r0 += 4) {
+    const int r = r0 + lrow;
+    if (r < NPH) {
+      const int h = hh[i0 * NH + r];
+      cp_async16(stage + r * kLanes + lcol, post0 + static_cast<size_t>(h) * kLanes + lcol, qact);
+      cp_async16_ef(stage + (NPH + r) * kLanes + lcol, c2v0 + static_cast<size_t>(i0 * NH + r) * kLanes + lcol, qc2v,
+                    pol);
     }
-    if (ND) cp_async4_ef(stage + (k * RPC + 2 * NH) * kLanes, llrd + static_cast<size_t>(i0 + k) * kLanes, act, pol);
+  }
+#pragma unroll
+  for (int r0 = 0; r0 < NPD; r0 += 4) {
+    const int r = r0 + lrow;
+    if (r < NPD)
+      cp_async16_ef(stage + (2 * NPH + r) * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol, qact,
+                    pol);
   }
   cp_async_commit();
 }
@@ -384,22 +407,22 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
 template <int NH, int ND, bool WANT_POST>
 __device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p,
                                                     const uint32_t* ssyn, int i0, int lane, bool act, bool first,
-                                                    float clamp, uint32_t* synw, uint32_t* d1w) {
+                                                    float cl, float clamp, uint32_t* synw, uint32_t* d1w) {
   constexpr int D = NH + ND;
   constexpr int K = CheckShape<NH, ND>::K;
-  constexpr int RPC = CheckShape<NH, ND>::RPC;
+  constexpr int NPH = K * NH;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     float m[D > 0 ? D : 1];
     float l = 0.0f;
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const float v = stage[(k * RPC + j) * kLanes] - stage[(k * RPC + NH + j) * kLanes];
-      m[j] = first ? v : clampf(v, clamp);
+      const float co = first ? 0.0f : stage[(NPH + k * NH + j) * kLanes];
+      m[j] = clampf(stage[(k * NH + j) * kLanes] - co, cl);  // cl = inf in the first iteration
     }
     if (ND) {
-      l = stage[(k * RPC + 2 * NH) * kLanes];
-      m[NH] = first ? l : clampf(l, clamp);
+      l = stage[(2 * NPH + k) * kLanes];
+      m[NH] = clampf(l, cl);
     }
     const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
     uint32_t par = sbit;
@@ -429,30 +452,39 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 template <int NH, int ND, bool WANT_POST>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                   const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
-                                                  uint32_t* synw, uint32_t* d1w) {
+                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NB = 32 / K;
-  const float* postg = a.post + static_cast<size_t>(g) * a.NV * kLanes + lane;
+  const float* post0 = a.post + static_cast<size_t>(g) * a.NV * kLanes;
+  const float* c2v0 = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes;
+  const float* llr0 = a.llr_d + (static_cast<size_t>(g) * a.N1 + db) * kLanes;
   float* c2vg = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes + lane;
-  const float* llrd = a.llr_d + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane;
   float* d1p = WANT_POST ? a.d1post + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane : nullptr;
   const float clamp = a.clamp;
-  const bool rd_c2v = act && !first;
+  const float cl = first ? __int_as_float(0x7f800000) : clamp;
+  // this lane's 16-byte quarter: frames 4*(lane%8) .. +3 of row group member lane/8
+  const int lrow = lane >> 3;
+  const int lcol = (lane & 7) * 4;
+  const uint32_t qbits = (amask >> lcol) & 0xFu;
+  const bool qact = qbits != 0u;
+  const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
   const uint64_t pol = policy_evict_first();
-  float* const ring_l = ring + lane;
   constexpr int NS = kStages;
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p)
     if (p < NB)
-      check_batch_issue<NH, ND>(ring_l + p * kStageRows * kLanes, postg, c2vg, llrd, hh, p * K, act, rd_c2v, pol);
+      check_batch_issue<NH, ND>(ring + p * kStageRows * kLanes, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v,
+                                pol);
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
     if (b + NS - 1 < NB)
-      check_batch_issue<NH, ND>(ring_l + ((b + NS - 1) % NS) * kStageRows * kLanes, postg, c2vg, llrd, hh,
-                                (b + NS - 1) * K, act, rd_c2v, pol);
+      check_batch_issue<NH, ND>(ring + ((b + NS - 1) % NS) * kStageRows * kLanes, post0, c2v0, llr0, hh,
+                                (b + NS - 1) * K, lrow, lcol, qact, qc2v, pol);
     cp_async_wait_upto(min(NS - 1, NB - 1 - b));
-    check_batch_compute<NH, ND, WANT_POST>(ring_l + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
-                                           lane, act, first, clamp, synw, d1w);
+    __syncwarp();  // rows were copied by other lanes
+    check_batch_compute<NH, ND, WANT_POST>(ring + lane + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
+                                           lane, act, first, cl, clamp, synw, d1w);
+    __syncwarp();  // stage is refilled in the next round
   }
 }
 
@@ -484,10 +516,11 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
     const bool act = (amask >> lane) & 1u;
     const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
     const bool first = (it == 1);
+    const uint32_t fmask = __ballot_sync(0xffffffffu, act && first);
     const int4 cdk = __ldg(&a.ctype[ch]);
     const int type = kStage ? cdk.x : -1;
     // degree-1 checks only change in a frame's first iteration
-    if ((type == 1 || type == 8) && !__any_sync(0xffffffffu, act && first)) {
+    if ((type == 1 || type == 8) && fmask == 0u) {
       w += nwarps;
       continue;
     }
@@ -512,7 +545,7 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
       check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
-                                             first, &synw, &d1w);                                   \
+                                             first, amask, fmask, &synw, &d1w);                     \
     else                                                                                            \
       typed = false;                                                                                \
     break;
@@ -577,18 +610,22 @@ struct VarShape {
   static_assert(NS >= 1, "variable degree too large for the ring");
 };
 
+// Stage layout for a batch of K variables: [K llr rows][K*D c2v rows].
 template <int D>
-__device__ __forceinline__ void var_batch_issue(float* stage, const float* llrh, const float* c2vg, const int32_t* ve,
-                                                int i0, bool act, uint64_t pol) {
+__device__ __forceinline__ void var_batch_issue(float* stage, const float* llr0, const float* c2v0, const int32_t* ve,
+                                                int i0, int lrow, int lcol, bool qact, uint64_t pol) {
   constexpr int K = VarShape<D>::K;
-  constexpr int RPV = VarShape<D>::RPV;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    cp_async4_ef(stage + (k * RPV) * kLanes, llrh + static_cast<size_t>(i0 + k) * kLanes, act, pol);
+  for (int r0 = 0; r0 < K; r0 += 4) {
+    const int r = r0 + lrow;
+    if (r < K) cp_async16_ef(stage + r * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol, qact, pol);
+  }
 #pragma unroll
-    for (int j = 0; j < D; ++j)
-      cp_async4_ef(stage + (k * RPV + 1 + j) * kLanes, c2vg + static_cast<size_t>(ve[(i0 + k) * D + j]) * kLanes,
-                   act, pol);
+  for (int r0 = 0; r0 < K * D; r0 += 4) {
+    const int r = r0 + lrow;
+    if (r < K * D)
+      cp_async16_ef(stage + (K + r) * kLanes + lcol, c2v0 + static_cast<size_t>(ve[i0 * D + r]) * kLanes + lcol, qact,
+                    pol);
   }
   cp_async_commit();
 }
@@ -597,12 +634,11 @@ template <int D, int QMODE>
 __device__ __forceinline__ void var_batch_compute(const float* stage, float* postg, int i0, int lane, bool act,
                                                   double* acc, uint32_t* hw) {
   constexpr int K = VarShape<D>::K;
-  constexpr int RPV = VarShape<D>::RPV;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    float p = stage[(k * RPV) * kLanes];
+    float p = stage[k * kLanes];
 #pragma unroll
-    for (int j = 0; j < D; ++j) p += stage[(k * RPV + 1 + j) * kLanes];  // ascending check order (decoder.cpp:101)
+    for (int j = 0; j < D; ++j) p += stage[(K + k * D + j) * kLanes];  // ascending check order (decoder.cpp:101)
     st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, act);
     if (act) *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
     const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
@@ -612,24 +648,29 @@ __device__ __forceinline__ void var_batch_compute(const float* stage, float* pos
 
 template <int D, int QMODE>
 __device__ __forceinline__ void var_chunk_typed(const Args& a, int g, int h0, const int32_t* ve, float* ring,
-                                                int lane, bool act, double* acc, uint32_t* hw) {
+                                                int lane, bool act, uint32_t amask, double* acc, uint32_t* hw) {
   constexpr int K = VarShape<D>::K;
   constexpr int NB = 32 / K;
-  const float* llrh = a.llr_h + (static_cast<size_t>(g) * a.NH + h0) * kLanes + lane;
-  const float* c2vg = a.c2v + static_cast<size_t>(g) * a.EH * kLanes + lane;
+  const float* llr0 = a.llr_h + (static_cast<size_t>(g) * a.NH + h0) * kLanes;
+  const float* c2v0 = a.c2v + static_cast<size_t>(g) * a.EH * kLanes;
   float* postg = a.post + (static_cast<size_t>(g) * a.NV + h0) * kLanes + lane;
+  const int lrow = lane >> 3;
+  const int lcol = (lane & 7) * 4;
+  const bool qact = ((amask >> lcol) & 0xFu) != 0u;
   const uint64_t pol = policy_evict_first();
-  float* const ring_l = ring + lane;
   constexpr int NS = VarShape<D>::NS;
   constexpr int RS = VarShape<D>::ROWS * kLanes;  // stage stride
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p)
-    if (p < NB) var_batch_issue<D>(ring_l + p * RS, llrh, c2vg, ve, p * K, act, pol);
+    if (p < NB) var_batch_issue<D>(ring + p * RS, llr0, c2v0, ve, p * K, lrow, lcol, qact, pol);
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
-    if (b + NS - 1 < NB) var_batch_issue<D>(ring_l + ((b + NS - 1) % NS) * RS, llrh, c2vg, ve, (b + NS - 1) * K, act, pol);
+    if (b + NS - 1 < NB)
+      var_batch_issue<D>(ring + ((b + NS - 1) % NS) * RS, llr0, c2v0, ve, (b + NS - 1) * K, lrow, lcol, qact, pol);
     cp_async_wait_upto(min(NS - 1, NB - 1 - b));
-    var_batch_compute<D, QMODE>(ring_l + (b % NS) * RS, postg, b * K, lane, act, acc, hw);
+    __syncwarp();
+    var_batch_compute<D, QMODE>(ring + lane + (b % NS) * RS, postg, b * K, lane, act, acc, hw);
+    __syncwarp();
   }
 }
 
@@ -690,7 +731,7 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
       switch (vt) {
 #define BPDEC_VTYPED(D_) \
   case D_:               \
-    var_chunk_typed<D_, QMODE>(a, g, h0, ve, s_ring[warp], lane, act, &acc, &hw); \
+    var_chunk_typed<D_, QMODE>(a, g, h0, ve, s_ring[warp], lane, act, amask, &acc, &hw); \
     break;
         BPDEC_VTYPED(2)
         BPDEC_VTYPED(3)
