@@ -223,20 +223,21 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
 // Magnitudes of the outgoing messages from the incoming ones (phi domain;
 // prefix/suffix sums, no subtraction).  deg 1: empty product -> clamp;
 // deg 2: phi(phi(x)) = x, passed through.
+// `m` are magnitudes (already clamped to <= msg_clamp except in iteration 1).
 template <int D>
 __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&out)[D], float clamp) {
   if (D == 1) {
     out[0] = clamp;
   } else if (D == 2) {
-    out[0] = fminf(fabsf(m[1]), clamp);
-    out[1] = fminf(fabsf(m[D > 1 ? 0 : 0]), clamp);
+    out[0] = fminf(m[1], clamp);
+    out[1] = fminf(m[D > 1 ? 0 : 0], clamp);
   } else {
     float ph[D];
     float pre[D];
     float run = 0.0f;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      ph[j] = dev::phi(fabsf(m[j]));
+      ph[j] = dev::phi(m[j]);
       pre[j] = run;
       run += ph[j];
     }
@@ -413,31 +414,35 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   constexpr int NPH = K * NH;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    float m[D > 0 ? D : 1];
+    float m[D > 0 ? D : 1];    // |v2c|, clamped (cl = inf in the first iteration)
+    uint32_t sg[D > 0 ? D : 1];  // sign bits of v2c (the clamp keeps the sign)
     float l = 0.0f;
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const float co = first ? 0.0f : stage[(NPH + k * NH + j) * kLanes];
-      m[j] = clampf(stage[(k * NH + j) * kLanes] - co, cl);  // cl = inf in the first iteration
+      const float v = stage[(k * NH + j) * kLanes] - co;
+      m[j] = fminf(fabsf(v), cl);
+      sg[j] = signbit_u(v);
     }
     if (ND) {
       l = stage[(2 * NPH + k) * kLanes];
-      m[NH] = clampf(l, cl);
+      m[NH] = fminf(fabsf(l), cl);
+      sg[NH] = signbit_u(l);
     }
     const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
     uint32_t par = sbit;
 #pragma unroll
-    for (int j = 0; j < D; ++j) par ^= signbit_u(m[j]);
+    for (int j = 0; j < D; ++j) par ^= sg[j];
     float out[D > 0 ? D : 1];
     check_magnitudes<D>(m, out, clamp);
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const float o = with_sign(out[j], par ^ signbit_u(m[j]));
+      const float o = with_sign(out[j], par ^ sg[j]);
       stcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o, act);
     }
     uint32_t dbit = 0u;
     if (ND) {
-      const float o = with_sign(out[NH], par ^ signbit_u(m[NH]));
+      const float o = with_sign(out[NH], par ^ sg[NH]);
       const float pd = l + o;  // posterior of the degree-1 variable
       dbit = (act && pd < 0.0f) ? 1u : 0u;
       if (WANT_POST) st_pred(d1p + static_cast<size_t>(i0 + k) * kLanes, pd, act);
@@ -601,12 +606,14 @@ constexpr int kVarStage = 32 * 24;  // staged edge ids per warp
 // Typed chunk of 32 degree-D variables: K variables per batch of K*(D+1)
 // rows (channel LLR + D messages), copied with cp.async into the per-warp
 // two-stage ring while the previous batch is summed from shared memory.
+constexpr int kVarRingRows = 48;  // per-warp ring of the variable kernel (rows of 128 B)
+
 template <int D>
 struct VarShape {
   static constexpr int RPV = D + 1;
   static constexpr int K = kStageRows / RPV >= 8 ? 8 : (kStageRows / RPV >= 4 ? 4 : (kStageRows / RPV >= 2 ? 2 : 1));
-  static constexpr int ROWS = K * RPV;                                     // rows per batch
-  static constexpr int NS = kRingRows / ROWS >= 3 ? 3 : kRingRows / ROWS;  // ring stages
+  static constexpr int ROWS = K * RPV;  // rows per batch
+  static constexpr int NS = kVarRingRows / ROWS >= 3 ? 3 : kVarRingRows / ROWS;  // ring stages
   static_assert(NS >= 1, "variable degree too large for the ring");
 };
 
@@ -695,7 +702,7 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
   __shared__ double red[kVarWarps][kLanes];
   __shared__ int32_t s_ptr[kVarWarps][33];
   __shared__ int32_t s_ve[kVarWarps][kVarStage];
-  __shared__ __align__(16) float s_ring[kVarWarps][kRingRows * kLanes];
+  __shared__ __align__(16) float s_ring[kVarWarps][kVarRingRows * kLanes];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const long long total = static_cast<long long>(a.G) * a.n_tiles;

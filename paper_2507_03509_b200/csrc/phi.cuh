@@ -31,22 +31,23 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return y;
 }
 
+// 17 instructions, 2 MUFU: both pieces evaluated, selected per lane.
 __device__ __forceinline__ float phi(float x) {
-  // x >= 1 branch
+  // x >= 1: t = e^-x, phi = t * (2 + w*A2(w)), A2 = 2*A (coefficients doubled)
   const float t = ex2_approx(x * -1.4426950408889634f);
   const float w = t * t;
-  float a = 0.14783698262526393f;
-  a = fmaf(a, w, 0.1383879360711249f);
-  a = fmaf(a, w, 0.2002081579507349f);
-  a = fmaf(a, w, 0.3333303414682521f);
-  const float hi = (2.0f * t) * fmaf(a, w, 1.0f);
-  // x < 1 branch
+  float a = 2.0f * 0.14783698262526393f;
+  a = fmaf(a, w, 2.0f * 0.1383879360711249f);
+  a = fmaf(a, w, 2.0f * 0.2002081579507349f);
+  a = fmaf(a, w, 2.0f * 0.3333303414682521f);
+  const float hi = t * fmaf(a, w, 2.0f);
+  // x < 1: phi = ln2 - ln2*log2(x) + z*B(z), z = x^2
   const float z = x * x;
   float b = -2.1672081029454006e-05f;
   b = fmaf(b, z, 0.0003380189508581495f);
   b = fmaf(b, z, -0.0048599077080608115f);
   b = fmaf(b, z, 0.08333320963387135f);
-  const float lo = fmaf(1.0f - lg2_approx(x), 0.6931471805599453f, b * z);
+  const float lo = fmaf(lg2_approx(x), -0.6931471805599453f, fmaf(b, z, 0.6931471805599453f));
   return x < 1.0f ? lo : hi;
 }
 
