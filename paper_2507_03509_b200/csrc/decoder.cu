@@ -320,9 +320,15 @@ constexpr int kStageRows = 12;  // rows per batch stage (check shapes)
 constexpr int kStages = 3;      // ring depth: two batches in flight while one is computed
 constexpr int kRingRows = kStages * kStageRows;
 
-// Waits until at most `pending` (0..2) committed cp.async groups are in flight.
+// Waits until at most `pending` (0..5) committed cp.async groups are in flight.
 __device__ __forceinline__ void cp_async_wait_upto(int pending) {
-  if (pending >= 2) {
+  if (pending >= 5) {
+    asm volatile("cp.async.wait_group 5;\n" ::: "memory");
+  } else if (pending == 4) {
+    asm volatile("cp.async.wait_group 4;\n" ::: "memory");
+  } else if (pending == 3) {
+    asm volatile("cp.async.wait_group 3;\n" ::: "memory");
+  } else if (pending == 2) {
     asm volatile("cp.async.wait_group 2;\n" ::: "memory");
   } else if (pending == 1) {
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -613,7 +619,7 @@ struct VarShape {
   static constexpr int RPV = D + 1;
   static constexpr int K = kStageRows / RPV >= 8 ? 8 : (kStageRows / RPV >= 4 ? 4 : (kStageRows / RPV >= 2 ? 2 : 1));
   static constexpr int ROWS = K * RPV;  // rows per batch
-  static constexpr int NS = kVarRingRows / ROWS >= 3 ? 3 : kVarRingRows / ROWS;  // ring stages
+  static constexpr int NS = kVarRingRows / ROWS >= 6 ? 6 : kVarRingRows / ROWS;  // ring stages
   static_assert(NS >= 1, "variable degree too large for the ring");
 };
 
@@ -1317,9 +1323,10 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   grid_check = sms * 16;
   grid_var = sms * 16;
   grid_syn = sms * 8;
-  grid_extract = sms * 4;
-  load_item_blocks = sms * 4;
-  load_check_blocks = sms * 2;
+  // load / extract are no-ops on most steps: keep their grids small
+  grid_extract = sms;
+  load_item_blocks = sms;
+  load_check_blocks = sms / 2;
 }
 
 GpuDecoder::~GpuDecoder() {
