@@ -278,6 +278,7 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     launches0 = dec.launch_count()
+    host0 = time.perf_counter()
     ev0.record(stream)
     iters_total = 0
     for _ in range(args.steps):
@@ -285,6 +286,7 @@ def run_ours(args):
         iters_total += int(out["iterations"].sum().item())  # result gather (host read of the step's outputs)
     ev1.record(stream)
     torch.cuda.synchronize()
+    host_ms = (time.perf_counter() - host0) * 1e3
     clock = clocks.stop()
     launches = dec.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
@@ -397,6 +399,7 @@ def run_ours(args):
         emit({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "host_ms_per_step": host_ms / args.steps,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE generator, device-generated frames)",
             "config": {"workload": w.name, "frames_per_gpu": F, "slots": dec.slots, "beta": args.beta,

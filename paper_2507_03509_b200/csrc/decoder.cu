@@ -96,7 +96,7 @@ struct Args {
   uint32_t* fail;           // [G]
   uint32_t* stopped;        // [G]
   uint32_t* load_mask;      // [G]
-  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags
+  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -862,6 +862,7 @@ __global__ void __launch_bounds__(1024) k_terminate(const Args a) {
   atomicAnd(&a.group_active[g], ~bit);
   atomicOr(&a.stopped[g], bit);
   atomicAdd(&a.counters[1], 1);
+  atomicSub(&a.counters[3], 1);
   const int nf = atomicAdd(&a.counters[0], 1);
   if (nf < a.batch) {
     a.pending_frame[s] = nf;
@@ -997,6 +998,7 @@ __global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks
         a.slot_iter[s] = 1;
         a.qprev[s] = 0.0;
         atomicOr(&a.group_active[g], bit);
+        atomicAdd(&a.counters[3], 1);
       }
     }
   }
@@ -1007,6 +1009,124 @@ __global__ void k_step_end(const Args a) {
   for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
     a.stopped[g] = 0u;
     a.load_mask[g] = 0u;
+  }
+}
+
+// ---------------------------------------------------------- compaction --
+// When no frames are left to stream in, frames that are still iterating are
+// packed into as few 32-slot groups as possible, so the tail of a batch (a
+// few slow frames spread over many groups) stops paying full-warp compute in
+// every group.  The plan is a pure function of group_active, computed
+// redundantly by every block; k_compact_move copies the per-slot rows,
+// k_compact_commit then moves the slot state and rewrites group_active.
+constexpr int kMaxCompactGroups = 256;
+constexpr int kMaxMoves = 1024;
+
+struct CompactPlan {
+  int n;
+  int16_t src[kMaxMoves];  // slot indices
+  int16_t dst[kMaxMoves];
+};
+
+__device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
+  // single thread
+  pl.n = 0;
+  const int G = a.G;
+  if (G > kMaxCompactGroups) return;
+  int total = 0, alive = 0;
+  for (int g = 0; g < G; ++g) {
+    cnt[g] = __popc(a.group_active[g]);
+    total += cnt[g];
+    alive += cnt[g] > 0;
+  }
+  const int need = (total + 31) / 32;
+  if (alive <= need) return;
+  // targets: the `need` fullest groups (ties -> lower index); the rest are sources
+  bool is_target[kMaxCompactGroups];
+  for (int g = 0; g < G; ++g) is_target[g] = false;
+  for (int t = 0; t < need; ++t) {
+    int best = -1;
+    for (int g = 0; g < G; ++g)
+      if (!is_target[g] && (best < 0 || cnt[g] > cnt[best])) best = g;
+    is_target[best] = true;
+  }
+  int tg = 0;
+  uint32_t tfree = 0u;
+  auto next_target = [&]() {
+    while (tg < G && (!is_target[tg] || (tfree = ~a.group_active[tg]) == 0u)) ++tg;
+  };
+  next_target();
+  for (int g = 0; g < G && pl.n < kMaxMoves; ++g) {
+    if (is_target[g] || cnt[g] == 0) continue;
+    uint32_t m = a.group_active[g];
+    while (m && pl.n < kMaxMoves) {
+      if (tg >= G) return;
+      const int ls = __ffs(m) - 1;
+      m &= m - 1;
+      const int ld = __ffs(tfree) - 1;
+      tfree &= tfree - 1;
+      pl.src[pl.n] = static_cast<int16_t>(g * kLanes + ls);
+      pl.dst[pl.n] = static_cast<int16_t>(tg * kLanes + ld);
+      ++pl.n;
+      if (tfree == 0u) {
+        ++tg;
+        next_target();
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_compact_move(const Args a) {
+  __shared__ CompactPlan pl;
+  __shared__ int cnt[kMaxCompactGroups];
+  if (threadIdx.x == 0) compact_plan(a, pl, cnt);
+  __syncthreads();
+  const int n = pl.n;
+  if (n == 0) return;
+  const long long rows_e = a.EH, rows_v = a.NV, rows_h = a.NH, rows_d = a.N1;
+  const bool post_d = a.d1post != nullptr;
+  const long long total = rows_e + rows_v + rows_h + rows_d * (post_d ? 2 : 1) + a.M;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
+    long long r = t;
+    float* arr;
+    long long R;
+    if (r < rows_e) { arr = a.c2v; R = rows_e; }
+    else if ((r -= rows_e) < rows_v) { arr = a.post; R = rows_v; }
+    else if ((r -= rows_v) < rows_h) { arr = a.llr_h; R = rows_h; }
+    else if ((r -= rows_h) < rows_d) { arr = a.llr_d; R = rows_d; }
+    else if (post_d && (r -= rows_d) < rows_d) { arr = a.d1post; R = rows_d; }
+    else {
+      // syndrome target bits of check cc (one thread does every move into a word)
+      const int cc = static_cast<int>(r - rows_d);
+      for (int k = 0; k < n; ++k) {
+        const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
+        const uint32_t bit = (a.syn_target[static_cast<size_t>(gs) * a.M + cc] >> ls) & 1u;
+        uint32_t& w = a.syn_target[static_cast<size_t>(gd) * a.M + cc];
+        w = (w & ~(1u << ld)) | (bit << ld);
+      }
+      continue;
+    }
+    for (int k = 0; k < n; ++k) {
+      const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
+      arr[(static_cast<size_t>(gd) * R + r) * kLanes + ld] = arr[(static_cast<size_t>(gs) * R + r) * kLanes + ls];
+    }
+  }
+}
+
+__global__ void k_compact_commit(const Args a) {
+  __shared__ CompactPlan pl;
+  __shared__ int cnt[kMaxCompactGroups];
+  if (threadIdx.x == 0) {
+    compact_plan(a, pl, cnt);
+    for (int k = 0; k < pl.n; ++k) {
+      const int s = pl.src[k], d = pl.dst[k];
+      a.slot_iter[d] = a.slot_iter[s];
+      a.slot_frame[d] = a.slot_frame[s];
+      a.qprev[d] = a.qprev[s];
+      a.group_active[s >> 5] &= ~(1u << (s & 31));
+      a.group_active[d >> 5] |= 1u << (d & 31);
+    }
   }
 }
 
@@ -1118,6 +1238,7 @@ class GpuDecoder {
   int64_t prof_launches[kNumKernels] = {};
   double prof_frame_iters = 0.0;
   int64_t launches = 0;
+  int64_t compactions = 0;
 
  private:
   template <typename F>
@@ -1324,9 +1445,9 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   grid_var = sms * 16;
   grid_syn = sms * 8;
   // load / extract are no-ops on most steps: keep their grids small
-  grid_extract = sms;
-  load_item_blocks = sms;
-  load_check_blocks = sms / 2;
+  grid_extract = sms * 4;
+  load_item_blocks = sms * 4;
+  load_check_blocks = sms * 2;
 }
 
 GpuDecoder::~GpuDecoder() {
@@ -1471,7 +1592,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       pend[s] = s;
       lm[s >> 5] |= 1u << (s & 31);
     }
-    int32_t ctr[4] = {first, 0, 0, 0};
+    int32_t ctr[4] = {first, 0, 0, 0};  // active slots counted by k_load
     CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));
@@ -1494,6 +1615,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   constexpr int kLag = 4;
   int64_t step = 0;
   bool done = false;
+  int compact_level = G * kLanes;  // active-slot count at the last compaction attempt
   for (; step < max_steps + kLag && !done; ++step) {
     run_step(a, st, want_post);
     const int slot = static_cast<int>(step % kRing);
@@ -1504,6 +1626,18 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       CUDA_OK(cudaEventSynchronize(ring_ev[old]));
       if (h_counters[4 * old + 2] != 0) break;  // invalid input detected
       if (h_counters[4 * old + 1] >= b.batch) done = true;
+      // queue drained and the live frames fit in fewer groups: compact (the
+      // host view lags kLag steps; the device plan works on current state)
+      const int active = h_counters[4 * old + 3];
+      if (!done && G > 1 && G <= kMaxCompactGroups && h_counters[4 * old] >= b.batch && active > 0 &&
+          active <= 32 * (G - 1) && active <= compact_level - 32) {
+        compact_level = active;
+        k_compact_move<<<grid_extract, kThreads, 0, st>>>(a);
+        k_compact_commit<<<1, 32, 0, st>>>(a);
+        CUDA_OK(cudaGetLastError());
+        launches += 2;
+        ++compactions;
+      }
     }
   }
   CUDA_OK(cudaStreamSynchronize(st));

@@ -286,3 +286,22 @@ def test_device_generator_matches_host(P, cfg1_code):
     assert mism.max() <= 1 and (mism > 0).mean() < 1e-3
     assert np.array_equal(ds.cpu().numpy().view(np.uint32), s)
     assert np.array_equal(P.unpack_bits(dx.cpu().numpy().view(np.uint32), cfg1_code.n_vars), x)
+
+
+def test_tail_compaction_is_transparent(P, cfg1_code):
+    """Group compaction (queue drained, live frames fit in fewer 32-slot
+    groups) moves frames between slots mid-decode; every per-frame output
+    must be bit-identical to decoding each frame alone."""
+    snr = P.snr_for_beta(0.95, cfg1_code.rate())
+    llr, x, s = P.sample_frames(cfg1_code, snr, 4242, 0, 128)
+    cfg = P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    big = P.BatchDecoder(cfg1_code, max_slots=128)  # 4 groups, compaction as frames stop
+    r = big.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True)
+    assert len(set(r.iterations.tolist())) > 5  # stop times spread: the tail compacts
+    one = P.BatchDecoder(cfg1_code, max_slots=32)
+    for f in range(0, 128, 9):
+        o = one.decode_batch(llr[f:f + 1], cfg, syndrome=s[f:f + 1], want_posteriors=True, want_q_trace=True)
+        assert o.iterations[0] == r.iterations[f] and o.reasons[0] == r.reasons[f]
+        assert np.array_equal(o.bits[0], r.bits[f])
+        assert np.array_equal(o.posteriors[0], r.posteriors[f])
+        assert np.array_equal(o.q_trace[0], r.q_trace[f], equal_nan=True)
