@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-pce-compare", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=None)
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period during the timed region")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     return ap.parse_args()
 
 
@@ -65,7 +66,9 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
-    def start(self):
+    def start(self, enabled=True):
+        if not enabled:
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -268,13 +271,18 @@ def run_ours(args):
     def step():
         return dec.decode_batch(d_llr, cfg, syndrome=d_syn, packed=True, out=out, stream=sptr)
 
-    for _ in range(args.warmup):
+    # W warm-up steps, extended to >= 1.5 s so the GPU's clocks have settled
+    # (short timed regions right after start-up measured up to 30% slow)
+    t_warm = time.perf_counter()
+    n_warm = 0
+    while n_warm < args.warmup or time.perf_counter() - t_warm < 1.5:
         step()
+        n_warm += 1
     torch.cuda.synchronize()
     clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local, args.clock_ms)
     barrier(dist)
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.start(not args.no_clocks)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     launches0 = dec.launch_count()
@@ -399,7 +407,7 @@ def run_ours(args):
         emit({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
-            "host_ms_per_step": host_ms / args.steps,
+            "host_ms_per_step": host_ms / args.steps, "warmup_steps_run": n_warm,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE generator, device-generated frames)",
             "config": {"workload": w.name, "frames_per_gpu": F, "slots": dec.slots, "beta": args.beta,

@@ -1,5 +1,7 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench=$?"
-tail -1 gpurun_out/bench.log | cut -c1-600
+for args in "--steps 10 --no-clocks" "--steps 10" "--steps 10 --clock-ms 1000" "--steps 3 --no-clocks" "--steps 30"; do
+  timeout 900 python bench.py --warmup 3 --no-cpu-baseline --no-pce-compare $args > gpurun_out/bench_tmp.log 2>&1
+  echo "$args :: $(tail -1 gpurun_out/bench_tmp.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]/1e9,1), round(d["ms_per_step"],2), round(d["host_ms_per_step"],2), d["clocks"])')"
+done
