@@ -277,6 +277,7 @@ def run_ours(args):
     n_warm = 0
     while n_warm < args.warmup or time.perf_counter() - t_warm < 1.5:
         step()
+        int(out["iterations"].sum().item())  # same host read as the timed steps (loads torch's kernel once)
         n_warm += 1
     torch.cuda.synchronize()
     clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local, args.clock_ms)

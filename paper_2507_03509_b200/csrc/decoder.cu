@@ -500,7 +500,7 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
 }
 
 template <int MAXD, bool WANT_POST>
-__global__ void __launch_bounds__(kCheckThreads, MAXD <= 3 ? 8 : 6) k_check(const Args a) {
+__global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   constexpr bool kStage = MAXD <= 16;
   constexpr int kHH = kStage ? 32 * MAXD : 1;
   __shared__ int4 s_desc[kCheckThreads / 32][32];
