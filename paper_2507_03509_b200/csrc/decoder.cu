@@ -16,18 +16,15 @@
 // residue) and their posterior llr + c2v is formed inside the check kernel.
 //
 // One decoding step = one flooding iteration for every active slot:
-//   k_check     check-node update of iteration k (decoder.cpp:82-96) +
-//               degree-1 posteriors / hard bits; from the posteriors it
-//               gathers anyway it also evaluates the syndrome of iteration
-//               k-1 (decoder.cpp:19-30), bit-sliced, 32 frames per word
-//   k_terminate PCE -> VNR -> d_max decision about iteration k-1
-//               (decoder.cpp:114-123), q from fixed-order partial sums
-//   k_extract   outputs of the frames that stopped at k-1 (:126-128)
-//   k_var       variable-node update of iteration k (decoder.cpp:99-105) for
-//               the frames still running, q partial sums (:32-36, :107)
+//   k_check     check-node update (decoder.cpp:82-96) + degree-1 posteriors,
+//               hard bits and the degree-1 part of the syndrome
+//   k_var       variable-node update (decoder.cpp:99-105) for degree>=2
+//               variables, hard bits, per-tile q partial sums (:32-36, :107)
+//   k_syndrome  bit-sliced parity of every check vs the target syndrome
+//               (decoder.cpp:19-30), 32 frames per 32-bit word
+//   k_terminate PCE -> VNR -> d_max decision per frame (decoder.cpp:114-123)
+//   k_extract   outputs of frames that stopped this step (:126-128)
 //   k_load      streams the next frames into freed slots
-// A frame that stops at k has therefore run one extra (discarded) check
-// pass; in exchange no kernel ever re-reads the hard decisions.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -85,15 +82,10 @@ struct Args {
   float* llr_d;             // [G][N1][32]
   float* post;              // [G][NV][32]
   float* c2v;               // [G][EH][32]
-  // Double-buffered by step parity: k_check of step t writes the "cur"
-  // buffers; step t+1 reads them as "prev" (the syndrome of iteration k is
-  // evaluated inside k_check of iteration k+1).
-  float* d1post;            // [G][N1][32] cur (only when posteriors are requested)
-  const float* d1post_prev;
-  uint32_t* d1bits;         // [G][N1] cur: hard bits of degree-1 variables
-  const uint32_t* d1bits_prev;
-  uint32_t* synp;           // [G][M]  cur: target syndrome ^ degree-1 parity
-  const uint32_t* synp_prev;
+  float* d1post;            // [G][N1][32] (only when posteriors are requested)
+  uint32_t* hbits;          // [G][NV]
+  uint32_t* d1bits;         // [G][N1]
+  uint32_t* synp;           // [G][M]  target syndrome ^ degree-1 parity
   uint32_t* syn_target;     // [G][M]
   double* q_part;           // [G][n_tiles][32]
   double* qprev;            // [S]
@@ -104,8 +96,7 @@ struct Args {
   uint32_t* fail;           // [G]
   uint32_t* stopped;        // [G]
   uint32_t* load_mask;      // [G]
-  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots,
-                            // [4] active slots at the last compaction
+  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -193,7 +184,6 @@ struct CheckState {
   int4 d;
   int deg, nh;
   uint32_t sbit, par;
-  uint32_t pbits;  // parity of the previous iteration's hard bits of the degree>=2 variables
 };
 
 template <int MAXD>
@@ -205,7 +195,6 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
   s.deg = s.nh + (d.w - d.z);
   s.sbit = (sword >> lane) & 1u;
   s.par = s.sbit;
-  s.pbits = 0u;
   const int lim = MAXD <= 16 ? MAXD : s.deg;
 #pragma unroll kUnroll
   for (int j = 0; j < lim; ++j) {
@@ -217,7 +206,6 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
           const float p = a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
           const float co = first ? 0.0f : ld_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane]);
           v = first ? p : clampf(p - co, a.clamp);
-          s.pbits ^= p < 0.0f ? 1u : 0u;  // hard decision of iteration k-1 (decoder.cpp:103)
         }
         s.l1[j] = 0.0f;
       } else {
@@ -425,9 +413,8 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
 
 template <int NH, int ND, bool WANT_POST>
 __device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p,
-                                                    const uint32_t* ssyn, const uint32_t* sprev, int i0, int lane,
-                                                    bool act, bool first, float cl, float clamp, uint32_t* synw,
-                                                    uint32_t* d1w, uint32_t* fl) {
+                                                    const uint32_t* ssyn, int i0, int lane, bool act, bool first,
+                                                    float cl, float clamp, uint32_t* synw, uint32_t* d1w) {
   constexpr int D = NH + ND;
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NPH = K * NH;
@@ -452,13 +439,6 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
     uint32_t par = sbit;
 #pragma unroll
     for (int j = 0; j < D; ++j) par ^= sg[j];
-    // syndrome of the previous iteration: its degree-1 part (+ target) was
-    // left in synp_prev by the previous step, the degree>=2 part is the
-    // parity of the hard decisions post < 0 of the rows gathered right here
-    uint32_t pb = (sprev[i0 + k] >> lane) & 1u;
-#pragma unroll
-    for (int j = 0; j < NH; ++j) pb ^= stage[(k * NH + j) * kLanes] < 0.0f ? 1u : 0u;
-    *fl |= pb;
     float out[D > 0 ? D : 1];
     check_magnitudes<D>(m, out, clamp);
 #pragma unroll
@@ -482,9 +462,8 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 
 template <int NH, int ND, bool WANT_POST>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
-                                                  const uint32_t* ssyn, const uint32_t* sprev, float* ring, int lane,
-                                                  bool act, bool first, uint32_t amask, uint32_t fmask, uint32_t* synw,
-                                                  uint32_t* d1w, uint32_t* fl) {
+                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
+                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NB = 32 / K;
   const float* post0 = a.post + static_cast<size_t>(g) * a.NV * kLanes;
@@ -514,8 +493,8 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
                                 (b + NS - 1) * K, lrow, lcol, qact, qc2v, pol);
     cp_async_wait_upto(min(NS - 1, NB - 1 - b));
     __syncwarp();  // rows were copied by other lanes
-    check_batch_compute<NH, ND, WANT_POST>(ring + lane + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, sprev,
-                                           b * K, lane, act, first, cl, clamp, synw, d1w, fl);
+    check_batch_compute<NH, ND, WANT_POST>(ring + lane + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
+                                           lane, act, first, cl, clamp, synw, d1w);
     __syncwarp();  // stage is refilled in the next round
   }
 }
@@ -526,29 +505,19 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   constexpr int kHH = kStage ? 32 * MAXD : 1;
   __shared__ int4 s_desc[kCheckThreads / 32][32];
   __shared__ uint32_t s_syn[kCheckThreads / 32][32];
-  __shared__ uint32_t s_prev[kCheckThreads / 32][32];
   __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
   __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRingRows * kLanes];
+  if (blockIdx.x == 0 && threadIdx.x < a.G) a.fail[threadIdx.x] = 0u;
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
   const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const int chunks = (a.M + 31) / 32;
   const long long total = static_cast<long long>(a.G) * chunks;
-  // failing checks of the previous iteration, OR-ed per group and flushed
-  // with one atomic per warp and group
-  int fg = -1;
-  uint32_t fl = 0u;
   for (long long w = warp0; w < total;) {
     const int g = static_cast<int>(w / chunks);
     const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
     const int c0 = ch * 32;
-    if (g != fg) {
-      const uint32_t fw = __ballot_sync(0xffffffffu, fl);
-      if (lane == 0 && fw && fg >= 0) atomicOr(&a.fail[fg], fw);
-      fg = g;
-      fl = 0u;
-    }
     const uint32_t amask = a.group_active[g];
     if (amask == 0u) {
       w = skip_group(w, chunks, nwarps);
@@ -558,32 +527,16 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
     const bool act = (amask >> lane) & 1u;
     const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
     const bool first = (it == 1);
-    const bool judged = act && !first;  // lanes whose previous iteration is checked now
     const uint32_t fmask = __ballot_sync(0xffffffffu, act && first);
     const int4 cdk = __ldg(&a.ctype[ch]);
     const int type = kStage ? cdk.x : -1;
-    const size_t cbase = static_cast<size_t>(g) * a.M + c0;
-    // checks whose only edge is a degree-1 variable never change after a
-    // frame's first iteration: carry their words over instead of recomputing
-    if (!WANT_POST && type == 1 && fmask == 0u) {
-      const uint32_t pw = lane < nc ? a.synp_prev[cbase + lane] : 0u;
-      if (lane < nc) {
-        a.synp[cbase + lane] = pw;
-        a.d1bits[static_cast<size_t>(g) * a.N1 + cdk.z + lane] =
-            a.d1bits_prev[static_cast<size_t>(g) * a.N1 + cdk.z + lane];
-      }
-      // lane l's frame fails if any check of the chunk has its bit set
-      uint32_t any = 0u;
-      for (int j = 0; j < nc; ++j) any |= __shfl_sync(0xffffffffu, pw, j);
-      fl |= judged && ((any >> lane) & 1u);
+    // degree-1 checks only change in a frame's first iteration
+    if ((type == 1 || type == 8) && fmask == 0u) {
       w += nwarps;
       continue;
     }
     __syncwarp();
-    if (lane < nc) {
-      s_syn[wi][lane] = a.syn_target[cbase + lane];
-      s_prev[wi][lane] = a.synp_prev[cbase + lane];
-    }
+    if (lane < nc) s_syn[wi][lane] = a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane];
     int hb0 = cdk.y;
     if (type < 0) {  // generic chunk: per-check descriptors
       if (lane < nc) s_desc[wi][lane] = __ldg(&a.cdesc[c0 + lane]);
@@ -595,17 +548,17 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
       for (int i = lane; i < nhh; i += 32) s_hh[wi][i] = __ldg(&a.chk_hi_h[hb0 + i]);
     }
     __syncwarp();
-    uint32_t synw = 0u, d1w = 0u, cf = 0u;
+    uint32_t synw = 0u, d1w = 0u;
     const int db0 = cdk.z;
     bool typed = true;
     switch (type) {
-#define BPDEC_TYPED(NH_, ND_)                                                                          \
-  case NH_ * 8 + ND_:                                                                                  \
-    if (NH_ + ND_ <= MAXD)                                                                             \
-      check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_prev[wi], s_ring[wi], \
-                                             lane, act, first, amask, fmask, &synw, &d1w, &cf);        \
-    else                                                                                               \
-      typed = false;                                                                                   \
+#define BPDEC_TYPED(NH_, ND_)                                                                       \
+  case NH_ * 8 + ND_:                                                                               \
+    if (NH_ + ND_ <= MAXD)                                                                          \
+      check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
+                                             first, amask, fmask, &synw, &d1w);                     \
+    else                                                                                            \
+      typed = false;                                                                                \
     break;
       BPDEC_TYPED(0, 1)
       BPDEC_TYPED(1, 0)
@@ -634,21 +587,16 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
                            act, first);
         }
         const uint32_t wa = check_finish<MAXD, WANT_POST>(a, A, g, lane, act);
-        cf |= ((s_prev[wi][j] >> lane) & 1u) ^ A.pbits;
         if (lane == j) synw = wa;
         if (hasB) {
           const uint32_t wb = check_finish<MAXD, WANT_POST>(a, B, g, lane, act);
-          cf |= ((s_prev[wi][j + 1] >> lane) & 1u) ^ B.pbits;
           if (lane == j + 1) synw = wb;
         }
       }
     }
-    fl |= judged && cf;
-    if (lane < nc) a.synp[cbase + lane] = synw;
+    if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = synw;
     w += nwarps;
   }
-  const uint32_t fw = __ballot_sync(0xffffffffu, fl);
-  if (lane == 0 && fw && fg >= 0) atomicOr(&a.fail[fg], fw);
 }
 
 // --------------------------------------------------------------- k_var --
@@ -823,7 +771,7 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
           if (lane == i) hw = word;
         }
       }
-      (void)hw;
+      if (lane < nv) a.hbits[gv + h0 + lane] = hw;
     }
     red[warp][lane] = acc;
     __syncthreads();
@@ -838,16 +786,43 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
   }
 }
 
+// ---------------------------------------------------------- k_syndrome --
+// Thread = one check x 32 slots (bit-sliced); checks padded to a multiple of
+// 32 per group so a warp never straddles two groups.
+__global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
+  const int lane = threadIdx.x & 31;
+  const long long mpad = (static_cast<long long>(a.M) + 31) / 32 * 32;
+  const long long total = static_cast<long long>(a.G) * mpad;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long w = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < total;) {
+    const int g = static_cast<int>(w / mpad);
+    const int c = static_cast<int>(w - g * mpad);
+    const uint32_t amask = a.group_active[g];
+    const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]);
+    if (amask == 0u || (fl & amask) == amask) {  // nothing left to learn in this group
+      w = skip_group(w, mpad, stride);
+      continue;
+    }
+    uint32_t word = 0u;
+    if (c < a.M) {
+      word = a.synp[static_cast<size_t>(g) * a.M + c];
+      const int4 d = __ldg(&a.cdesc[c]);
+      for (int e = d.x; e < d.y; ++e) word ^= a.hbits[static_cast<size_t>(g) * a.NV + __ldg(&a.chk_hi_h[e])];
+      word &= amask;
+    }
+    word = __reduce_or_sync(0xffffffffu, word);
+    if (lane == 0 && word != 0u && (fl & word) != word) atomicOr(&a.fail[g], word);
+    w += stride;
+  }
+}
+
 // --------------------------------------------------------- k_terminate --
 // Warp = one slot.  q^(k) = fixed-order double sum of the tile partials;
 // decision order PCE, then VNR (k >= 2, strict), then d_max
 // (decoder.cpp:114-123).
 __global__ void __launch_bounds__(1024) k_terminate(const Args a) {
-  // Runs after k_check of iteration it = slot_iter: decides about iteration
-  // k = it - 1, whose syndrome k_check just evaluated (fail bits) and whose
-  // q was summed by k_var in the previous step.  Block = one group; warp w
-  // sums tiles w, w+32, ... for every slot (lane), coalesced over lanes;
-  // warp 0 then adds the 32 warp sums in order.
+  // block = one group; warp w sums tiles w, w+32, ... for every slot (lane),
+  // coalesced over lanes; warp 0 then adds the 32 warp sums in order.
   __shared__ double red[32][kLanes];
   const int g = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -866,20 +841,15 @@ __global__ void __launch_bounds__(1024) k_terminate(const Args a) {
   if (!(amask & bit)) return;
   const int s = g * kLanes + lane;
   const int it = a.slot_iter[s];
-  if (it == 1) {  // first check pass of a freshly loaded frame: nothing to decide yet
-    a.slot_iter[s] = 2;
-    return;
-  }
-  const int k = it - 1;
   const int f = a.slot_frame[s];
   atomicAdd(a.frame_iters, 1ull);
-  if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (k - 1)] = q;
+  if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (it - 1)] = q;
   int reason = -1;
   if (a.use_pce && !(a.fail[g] & bit)) {
     reason = 0;
-  } else if (a.use_vnr && k >= 2 && q < a.qprev[s]) {
+  } else if (a.use_vnr && it >= 2 && q < a.qprev[s]) {
     reason = 1;
-  } else if (k >= a.d_max) {
+  } else if (it >= a.d_max) {
     reason = 2;
   }
   if (reason < 0) {
@@ -887,7 +857,7 @@ __global__ void __launch_bounds__(1024) k_terminate(const Args a) {
     a.qprev[s] = q;
     return;
   }
-  a.out_iters[f] = k;
+  a.out_iters[f] = it;
   a.out_reasons[f] = static_cast<uint8_t>(reason);
   atomicAnd(&a.group_active[g], ~bit);
   atomicOr(&a.stopped[g], bit);
@@ -927,16 +897,16 @@ __global__ void __launch_bounds__(kThreads) k_extract(const Args a) {
           const int vm = __ldg(&a.vmap[i]);
           if (vm >= 0) {
             if (vm < a.NV) {
-              pv = a.post[(static_cast<size_t>(g) * a.NV + vm) * kLanes + l];
-              bit = pv < 0.0f ? 1u : 0u;
+              bit = (a.hbits[static_cast<size_t>(g) * a.NV + vm] >> l) & 1u;
+              if (WANT_POST) pv = a.post[(static_cast<size_t>(g) * a.NV + vm) * kLanes + l];
             } else {  // degree-0 variable: posterior = channel LLR
               pv = a.llr_h[(static_cast<size_t>(g) * a.NH + vm) * kLanes + l];
               bit = pv < 0.0f ? 1u : 0u;
             }
           } else {
             const int dd = -1 - vm;
-            bit = (a.d1bits_prev[static_cast<size_t>(g) * a.N1 + dd] >> l) & 1u;
-            if (WANT_POST) pv = a.d1post_prev[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + l];
+            bit = (a.d1bits[static_cast<size_t>(g) * a.N1 + dd] >> l) & 1u;
+            if (WANT_POST) pv = a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + l];
           }
           if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
           if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
@@ -1039,7 +1009,6 @@ __global__ void k_step_end(const Args a) {
   for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
     a.stopped[g] = 0u;
     a.load_mask[g] = 0u;
-    a.fail[g] = 0u;  // k_check of the next step ORs the failing frames in
   }
 }
 
@@ -1063,8 +1032,7 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   // single thread
   pl.n = 0;
   const int G = a.G;
-  if (G > kMaxCompactGroups || G < 2) return;
-  if (a.counters[0] < a.batch) return;  // frames still queued: freed slots get refilled instead
+  if (G > kMaxCompactGroups) return;
   int total = 0, alive = 0;
   for (int g = 0; g < G; ++g) {
     cnt[g] = __popc(a.group_active[g]);
@@ -1073,7 +1041,6 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   }
   const int need = (total + 31) / 32;
   if (alive <= need) return;
-  if (total > a.counters[4] - 32) return;  // hysteresis: re-pack only after 32 more frames finished
   // targets: the `need` fullest groups (ties -> lower index); the rest are sources
   bool is_target[kMaxCompactGroups];
   for (int g = 0; g < G; ++g) is_target[g] = false;
@@ -1110,56 +1077,39 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_compact_move(const Args a) {
-  // Moves every per-slot quantity the next step reads: float rows (messages,
-  // posteriors, LLRs, degree-1 posteriors of the current parity), lane bits of
-  // 32-bit words (target syndrome, current syndrome/degree-1 words) and the
-  // q partial sums.  Sources and targets are disjoint groups, and all moves
-  // into one word are done by one thread, so no atomics are needed.
   __shared__ CompactPlan pl;
   __shared__ int cnt[kMaxCompactGroups];
   if (threadIdx.x == 0) compact_plan(a, pl, cnt);
   __syncthreads();
   const int n = pl.n;
   if (n == 0) return;
+  const long long rows_e = a.EH, rows_v = a.NV, rows_h = a.NH, rows_d = a.N1;
   const bool post_d = a.d1post != nullptr;
-  float* farr[5] = {a.c2v, a.post, a.llr_h, a.llr_d, a.d1post};
-  const long long frows[5] = {a.EH, a.NV, a.NH, a.N1, post_d ? a.N1 : 0};
-  uint32_t* warr[3] = {a.syn_target, a.synp, a.d1bits};
-  const long long wrows[3] = {a.M, a.M, a.N1};
-  long long total = a.n_tiles;
-  for (int i = 0; i < 5; ++i) total += frows[i];
-  for (int i = 0; i < 3; ++i) total += wrows[i];
+  const long long total = rows_e + rows_v + rows_h + rows_d * (post_d ? 2 : 1) + a.M;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
     long long r = t;
-    int seg = 0;
-    while (seg < 5 && r >= frows[seg]) r -= frows[seg++];
-    if (seg < 5) {
-      float* arr = farr[seg];
-      const long long R = frows[seg];
+    float* arr;
+    long long R;
+    if (r < rows_e) { arr = a.c2v; R = rows_e; }
+    else if ((r -= rows_e) < rows_v) { arr = a.post; R = rows_v; }
+    else if ((r -= rows_v) < rows_h) { arr = a.llr_h; R = rows_h; }
+    else if ((r -= rows_h) < rows_d) { arr = a.llr_d; R = rows_d; }
+    else if (post_d && (r -= rows_d) < rows_d) { arr = a.d1post; R = rows_d; }
+    else {
+      // syndrome target bits of check cc (one thread does every move into a word)
+      const int cc = static_cast<int>(r - rows_d);
       for (int k = 0; k < n; ++k) {
         const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
-        arr[(static_cast<size_t>(gd) * R + r) * kLanes + ld] = arr[(static_cast<size_t>(gs) * R + r) * kLanes + ls];
-      }
-      continue;
-    }
-    int ws = 0;
-    while (ws < 3 && r >= wrows[ws]) r -= wrows[ws++];
-    if (ws < 3) {
-      uint32_t* arr = warr[ws];
-      const long long R = wrows[ws];
-      for (int k = 0; k < n; ++k) {
-        const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
-        const uint32_t bit = (arr[static_cast<size_t>(gs) * R + r] >> ls) & 1u;
-        uint32_t& w = arr[static_cast<size_t>(gd) * R + r];
+        const uint32_t bit = (a.syn_target[static_cast<size_t>(gs) * a.M + cc] >> ls) & 1u;
+        uint32_t& w = a.syn_target[static_cast<size_t>(gd) * a.M + cc];
         w = (w & ~(1u << ld)) | (bit << ld);
       }
       continue;
     }
-    for (int k = 0; k < n; ++k) {  // q partial sums of the current iteration
+    for (int k = 0; k < n; ++k) {
       const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
-      a.q_part[(static_cast<size_t>(gd) * a.n_tiles + r) * kLanes + ld] =
-          a.q_part[(static_cast<size_t>(gs) * a.n_tiles + r) * kLanes + ls];
+      arr[(static_cast<size_t>(gd) * R + r) * kLanes + ld] = arr[(static_cast<size_t>(gs) * R + r) * kLanes + ls];
     }
   }
 }
@@ -1169,11 +1119,6 @@ __global__ void k_compact_commit(const Args a) {
   __shared__ int cnt[kMaxCompactGroups];
   if (threadIdx.x == 0) {
     compact_plan(a, pl, cnt);
-    if (pl.n > 0) {
-      int total = 0;
-      for (int g = 0; g < a.G; ++g) total += cnt[g];
-      a.counters[4] = total;
-    }
     for (int k = 0; k < pl.n; ++k) {
       const int s = pl.src[k], d = pl.dst[k];
       a.slot_iter[d] = a.slot_iter[s];
@@ -1300,22 +1245,7 @@ class GpuDecoder {
   void launch(int kid, cudaStream_t st, F&& f);
   void run_step(const Args& a, cudaStream_t st, bool want_post);
 
-  // Points the "cur"/"prev" views of the double-buffered per-step arrays at
-  // the halves selected by the step parity.
-  void set_parity(Args& a, int par) const {
-    const size_t gm = static_cast<size_t>(G) * a.M, gn = static_cast<size_t>(G) * a.N1;
-    a.synp = synp2 + par * gm;
-    a.synp_prev = synp2 + (par ^ 1) * gm;
-    a.d1bits = d1bits2 + par * gn;
-    a.d1bits_prev = d1bits2 + (par ^ 1) * gn;
-    a.d1post = d1post2 ? d1post2 + par * gn * kLanes : nullptr;
-    a.d1post_prev = d1post2 ? d1post2 + (par ^ 1) * gn * kLanes : nullptr;
-  }
-
   Args base{};
-  uint32_t* synp2 = nullptr;
-  uint32_t* d1bits2 = nullptr;
-  float* d1post2 = nullptr;
   int32_t max_check_deg = 0;
   int32_t* d_check_ptr = nullptr;
   int32_t* d_check_vars = nullptr;
@@ -1486,10 +1416,9 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.post = own(dalloc<float>(static_cast<size_t>(G) * NV * L, &dev_bytes));
   a.c2v = own(dalloc<float>(static_cast<size_t>(G) * EH * L, &dev_bytes));
   a.d1post = nullptr;  // allocated on first request
-  d1bits2 = own(dalloc<uint32_t>(2 * static_cast<size_t>(G) * n1, &dev_bytes));
-  synp2 = own(dalloc<uint32_t>(2 * static_cast<size_t>(G) * M, &dev_bytes));
-  CUDA_OK(cudaMemset(synp2, 0, 2 * static_cast<size_t>(G) * M * sizeof(uint32_t)));
-  CUDA_OK(cudaMemset(d1bits2, 0, 2 * static_cast<size_t>(G) * n1 * sizeof(uint32_t)));
+  a.hbits = own(dalloc<uint32_t>(static_cast<size_t>(G) * NV, &dev_bytes));
+  a.d1bits = own(dalloc<uint32_t>(static_cast<size_t>(G) * n1, &dev_bytes));
+  a.synp = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
   a.syn_target = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
   a.q_part = own(dalloc<double>(static_cast<size_t>(G) * a.n_tiles * L, &dev_bytes));
   a.qprev = own(dalloc<double>(S, &dev_bytes));
@@ -1500,7 +1429,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.fail = own(dalloc<uint32_t>(G, &dev_bytes));
   a.stopped = own(dalloc<uint32_t>(G, &dev_bytes));
   a.load_mask = own(dalloc<uint32_t>(G, &dev_bytes));
-  a.counters = own(dalloc<int32_t>(8, &dev_bytes));
+  a.counters = own(dalloc<int32_t>(4, &dev_bytes));
   a.frame_iters = own(dalloc<unsigned long long>(1, &dev_bytes));
   CUDA_OK(cudaMemset(a.group_active, 0, G * sizeof(uint32_t)));
   CUDA_OK(cudaMemset(a.stopped, 0, G * sizeof(uint32_t)));
@@ -1524,7 +1453,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
 GpuDecoder::~GpuDecoder() {
   cudaSetDevice(device);
   for (void* p : owned) cudaFree(p);
-  if (d1post2) cudaFree(d1post2);
+  if (base.d1post) cudaFree(base.d1post);
   for (auto& e : ring_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : prof_ev) cudaEventDestroy(e);
@@ -1559,9 +1488,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
 #define BPDEC_CHECK_CASE(D)                                                                 \
   if (md <= D) {                                                                            \
     if (want_post)                                                                          \
-      k_check<D, true><<<grid_check, kCheckThreads, 0, st>>>(a);                            \
+      k_check<D, true><<<grid_check, kCheckThreads, 0, st>>>(a);                                 \
     else                                                                                    \
-      k_check<D, false><<<grid_check, kCheckThreads, 0, st>>>(a);                           \
+      k_check<D, false><<<grid_check, kCheckThreads, 0, st>>>(a);                                \
     return;                                                                                 \
   }
     BPDEC_CHECK_CASE(3)
@@ -1572,6 +1501,13 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
     BPDEC_CHECK_CASE(256)
 #undef BPDEC_CHECK_CASE
   });
+  launch(kVar, st, [&] {
+    if (a.q_mode == 0)
+      k_var<0><<<grid_var, kVarWarps * 32, 0, st>>>(a);
+    else
+      k_var<1><<<grid_var, kVarWarps * 32, 0, st>>>(a);
+  });
+  if (a.use_pce) launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 0, st>>>(a); });
   launch(kTerm, st, [&] { k_terminate<<<G, 1024, 0, st>>>(a); });
   launch(kExtract, st, [&] {
     if (want_post)
@@ -1579,23 +1515,10 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
     else
       k_extract<false><<<grid_extract, kThreads, 0, st>>>(a);
   });
-  launch(kVar, st, [&] {
-    if (a.q_mode == 0)
-      k_var<0><<<grid_var, kVarWarps * 32, 0, st>>>(a);
-    else
-      k_var<1><<<grid_var, kVarWarps * 32, 0, st>>>(a);
-  });
   launch(kLoad, st, [&] {
     k_load<<<load_item_blocks + load_check_blocks + 1, kThreads, 0, st>>>(a, load_item_blocks, load_check_blocks);
   });
   k_step_end<<<1, 32, 0, st>>>(a);
-  // tail compaction (no-op unless the queue is drained and live frames fit
-  // in fewer groups; decided on the device, no host round trip)
-  if (G > 1 && G <= kMaxCompactGroups) {
-    k_compact_move<<<grid_extract, kThreads, 0, st>>>(a);
-    k_compact_commit<<<1, 32, 0, st>>>(a);
-    launches += 2;
-  }
   CUDA_OK(cudaGetLastError());
   ++launches;
 }
@@ -1612,8 +1535,10 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   Args a = base;
   const size_t B = static_cast<size_t>(b.batch);
   const bool want_post = b.posteriors != nullptr;
-  if (want_post && d1post2 == nullptr) d1post2 = dalloc<float>(2 * static_cast<size_t>(G) * a.N1 * kLanes, &dev_bytes);
-  a.d1post = want_post ? d1post2 : nullptr;
+  if (want_post && a.d1post == nullptr) {
+    a.d1post = dalloc<float>(static_cast<size_t>(G) * a.N1 * kLanes, &dev_bytes);
+    base.d1post = a.d1post;
+  }
   a.batch = b.batch;
   a.d_max = p.d_max;
   a.use_pce = p.use_pce;
@@ -1667,7 +1592,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       pend[s] = s;
       lm[s >> 5] |= 1u << (s & 31);
     }
-    int32_t ctr[8] = {first, 0, 0, 0, G * kLanes + 32, 0, 0, 0};  // active slots counted by k_load
+    int32_t ctr[4] = {first, 0, 0, 0};  // active slots counted by k_load
     CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));
@@ -1690,8 +1615,8 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   constexpr int kLag = 4;
   int64_t step = 0;
   bool done = false;
+  int compact_level = G * kLanes;  // active-slot count at the last compaction attempt
   for (; step < max_steps + kLag && !done; ++step) {
-    set_parity(a, static_cast<int>(step & 1));
     run_step(a, st, want_post);
     const int slot = static_cast<int>(step % kRing);
     CUDA_OK(cudaMemcpyAsync(h_counters + 4 * slot, a.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -1701,6 +1626,18 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       CUDA_OK(cudaEventSynchronize(ring_ev[old]));
       if (h_counters[4 * old + 2] != 0) break;  // invalid input detected
       if (h_counters[4 * old + 1] >= b.batch) done = true;
+      // queue drained and the live frames fit in fewer groups: compact (the
+      // host view lags kLag steps; the device plan works on current state)
+      const int active = h_counters[4 * old + 3];
+      if (!done && G > 1 && G <= kMaxCompactGroups && h_counters[4 * old] >= b.batch && active > 0 &&
+          active <= 32 * (G - 1) && active <= compact_level - 32) {
+        compact_level = active;
+        k_compact_move<<<grid_extract, kThreads, 0, st>>>(a);
+        k_compact_commit<<<1, 32, 0, st>>>(a);
+        CUDA_OK(cudaGetLastError());
+        launches += 2;
+        ++compactions;
+      }
     }
   }
   CUDA_OK(cudaStreamSynchronize(st));
