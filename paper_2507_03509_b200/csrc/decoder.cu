@@ -96,7 +96,8 @@ struct Args {
   uint32_t* fail;           // [G]
   uint32_t* stopped;        // [G]
   uint32_t* load_mask;      // [G]
-  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots
+  int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots,
+                            // [4] active slots at the last compaction
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -1032,7 +1033,8 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   // single thread
   pl.n = 0;
   const int G = a.G;
-  if (G > kMaxCompactGroups) return;
+  if (G > kMaxCompactGroups || G < 2) return;
+  if (a.counters[0] < a.batch) return;  // frames still queued: freed slots get refilled instead
   int total = 0, alive = 0;
   for (int g = 0; g < G; ++g) {
     cnt[g] = __popc(a.group_active[g]);
@@ -1041,6 +1043,7 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   }
   const int need = (total + 31) / 32;
   if (alive <= need) return;
+  if (total > a.counters[4] - 32) return;  // hysteresis: re-pack only after 32 more frames finished
   // targets: the `need` fullest groups (ties -> lower index); the rest are sources
   bool is_target[kMaxCompactGroups];
   for (int g = 0; g < G; ++g) is_target[g] = false;
@@ -1119,6 +1122,11 @@ __global__ void k_compact_commit(const Args a) {
   __shared__ int cnt[kMaxCompactGroups];
   if (threadIdx.x == 0) {
     compact_plan(a, pl, cnt);
+    if (pl.n > 0) {
+      int total = 0;
+      for (int g = 0; g < a.G; ++g) total += cnt[g];
+      a.counters[4] = total;
+    }
     for (int k = 0; k < pl.n; ++k) {
       const int s = pl.src[k], d = pl.dst[k];
       a.slot_iter[d] = a.slot_iter[s];
@@ -1429,7 +1437,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.fail = own(dalloc<uint32_t>(G, &dev_bytes));
   a.stopped = own(dalloc<uint32_t>(G, &dev_bytes));
   a.load_mask = own(dalloc<uint32_t>(G, &dev_bytes));
-  a.counters = own(dalloc<int32_t>(4, &dev_bytes));
+  a.counters = own(dalloc<int32_t>(8, &dev_bytes));
   a.frame_iters = own(dalloc<unsigned long long>(1, &dev_bytes));
   CUDA_OK(cudaMemset(a.group_active, 0, G * sizeof(uint32_t)));
   CUDA_OK(cudaMemset(a.stopped, 0, G * sizeof(uint32_t)));
@@ -1519,6 +1527,13 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
     k_load<<<load_item_blocks + load_check_blocks + 1, kThreads, 0, st>>>(a, load_item_blocks, load_check_blocks);
   });
   k_step_end<<<1, 32, 0, st>>>(a);
+  // tail compaction (no-op unless the queue is drained and live frames fit
+  // in fewer groups; decided on the device, no host round trip)
+  if (G > 1 && G <= kMaxCompactGroups) {
+    k_compact_move<<<grid_extract, kThreads, 0, st>>>(a);
+    k_compact_commit<<<1, 32, 0, st>>>(a);
+    launches += 2;
+  }
   CUDA_OK(cudaGetLastError());
   ++launches;
 }
@@ -1592,7 +1607,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       pend[s] = s;
       lm[s >> 5] |= 1u << (s & 31);
     }
-    int32_t ctr[4] = {first, 0, 0, 0};  // active slots counted by k_load
+    int32_t ctr[8] = {first, 0, 0, 0, G * kLanes + 32, 0, 0, 0};  // active slots counted by k_load
     CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));
@@ -1615,7 +1630,6 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   constexpr int kLag = 4;
   int64_t step = 0;
   bool done = false;
-  int compact_level = G * kLanes;  // active-slot count at the last compaction attempt
   for (; step < max_steps + kLag && !done; ++step) {
     run_step(a, st, want_post);
     const int slot = static_cast<int>(step % kRing);
@@ -1626,18 +1640,6 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       CUDA_OK(cudaEventSynchronize(ring_ev[old]));
       if (h_counters[4 * old + 2] != 0) break;  // invalid input detected
       if (h_counters[4 * old + 1] >= b.batch) done = true;
-      // queue drained and the live frames fit in fewer groups: compact (the
-      // host view lags kLag steps; the device plan works on current state)
-      const int active = h_counters[4 * old + 3];
-      if (!done && G > 1 && G <= kMaxCompactGroups && h_counters[4 * old] >= b.batch && active > 0 &&
-          active <= 32 * (G - 1) && active <= compact_level - 32) {
-        compact_level = active;
-        k_compact_move<<<grid_extract, kThreads, 0, st>>>(a);
-        k_compact_commit<<<1, 32, 0, st>>>(a);
-        CUDA_OK(cudaGetLastError());
-        launches += 2;
-        ++compactions;
-      }
     }
   }
   CUDA_OK(cudaStreamSynchronize(st));
