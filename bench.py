@@ -34,6 +34,20 @@ UNIT = "edge-updates/s"
 E_BYTES_MODEL_A = None  # filled per code: 16E + 4N + (N+M)/8 per frame-iteration
 
 
+# frames per GPU per step for each BASELINE workload (cfg4/cfg5 are the
+# 8-GPU streams 512..4096 / 8192 frames; per GPU at N=1 the first shard)
+FRAMES = {"cfg1": 16, "cfg2": 64, "cfg3": 32, "cfg4": 512, "cfg5": 1024}
+
+
+def workload_beta(args):
+    """(beta, beta_range) for the workload: fixed beta, or a per-frame range."""
+    if args.workload == "cfg5" and args.beta is None:
+        return None, (0.92, 1.0)
+    if args.beta is not None:
+        return args.beta, None
+    return (0.98 if args.workload == "cfg3" else 0.95), None
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -41,7 +55,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg2")
-    ap.add_argument("--beta", type=float, default=0.95)
+    ap.add_argument("--beta", type=float, default=None,
+                    help="reconciliation efficiency (default 0.95; cfg3 0.98; cfg5 draws U[0.92,1] per frame)")
     ap.add_argument("--frames", type=int, default=None, help="frames per GPU per step")
     ap.add_argument("--slots", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -214,8 +229,11 @@ def run_reference(args):
     code = w.make_code()
     threads = os.cpu_count() or 1
     frames = args.cpu_frames or threads
-    snr = P.snr_for_beta(args.beta, code.rate())
-    llr, x, _ = P.sample_frames(code, snr, P.FRAME_SEED, 0, frames)
+    beta, brange = workload_beta(args)
+    if brange is None:
+        llr, x, _ = P.sample_frames(code, P.snr_for_beta(beta, code.rate()), P.FRAME_SEED, 0, frames)
+    else:
+        llr, x, _, _ = P.sample_frames_beta(code, brange[0], brange[1], P.FRAME_SEED, 0, frames)
     leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float64)
     times, iters = [], []
     for k in range(args.warmup + args.steps):
@@ -225,13 +243,15 @@ def run_reference(args):
             iters.append(it)
     T = float(np.sum(times))
     value = float(np.sum(iters)) * code.n_edges / T
-    sample = (f"{frames} frames of {w.name} (beta={args.beta}, VNR+PCE, D_max={w.d_max}) per step, "
+    sample = (f"{frames} frames of {w.name} (beta={beta if brange is None else brange}, VNR+PCE, "
+              f"D_max={w.d_max}) per step, "
               f"all-zero-equivalent inputs L*(1-2x), s=0 (the reference's semantics)")
     emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
           "data": "synthetic (seeded BASELINE generator)",
-          "config": {"workload": w.name, "frames_per_step": frames, "beta": args.beta, "d_max": w.d_max,
+          "config": {"workload": w.name, "frames_per_step": frames, "beta": beta if brange is None else list(brange),
+                     "d_max": w.d_max,
                      "et": "vnr+pce", "threads": threads},
           "d_bar": float(np.sum(iters)) / (frames * len(times)),
           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
@@ -249,10 +269,11 @@ def run_ours(args):
     torch.cuda.set_device(local)
     w = P.WORKLOADS[args.workload]
     code = w.make_code()
-    F = args.frames or w.frames if args.workload != "cfg4" else (args.frames or 512)
-    slots = args.slots or F
+    F = args.frames or FRAMES[args.workload]
+    slots = args.slots or min(F, 512)
+    beta, brange = workload_beta(args)
     dec = P.BatchDecoder(code, device=local, max_slots=slots)
-    snr = P.snr_for_beta(args.beta, code.rate())
+    snr = P.snr_for_beta(beta, code.rate()) if brange is None else 0.0
     # weak scaling: rank r owns global frames [r*F, (r+1)*F)
     first = rank * F
     N, M = code.n_vars, code.n_checks
@@ -262,7 +283,7 @@ def run_ours(args):
     d_llr = torch.empty((F, N), dtype=torch.float32, device="cuda")
     d_syn = torch.empty((F, MW), dtype=torch.int32, device="cuda")
     d_x = torch.empty((F, NW), dtype=torch.int32, device="cuda")
-    dec.sample_frames_device(snr, P.FRAME_SEED, first, F, d_llr, d_syn, d_x, stream=sptr)
+    dec.sample_frames_device(snr, P.FRAME_SEED, first, F, d_llr, d_syn, d_x, stream=sptr, beta_range=brange)
     out = {"iterations": torch.zeros(F, dtype=torch.int32, device="cuda"),
            "reasons": torch.zeros(F, dtype=torch.uint8, device="cuda"),
            "bits": torch.zeros((F, NW), dtype=torch.int32, device="cuda")}
@@ -399,7 +420,8 @@ def run_ours(args):
                 cpu_reference_time(code, leq[:1], w.d_max, 1)  # first touch warm-up
                 dt, it, _ = cpu_reference_time(code, leq, w.d_max, threads)
                 cpu = {"value": it * code.n_edges / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"{nf} frames of {w.name} (beta={args.beta}, VNR+PCE, D_max={w.d_max}), "
+                       "sample": f"{nf} frames of {w.name} (beta={beta if brange is None else brange}, VNR+PCE, "
+                                 f"D_max={w.d_max}), "
                                  f"one reference BpDecoder per thread, {dt:.1f} s"}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
@@ -411,7 +433,8 @@ def run_ours(args):
             "host_ms_per_step": host_ms / args.steps, "warmup_steps_run": n_warm,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE generator, device-generated frames)",
-            "config": {"workload": w.name, "frames_per_gpu": F, "slots": dec.slots, "beta": args.beta,
+            "config": {"workload": w.name, "frames_per_gpu": F, "slots": dec.slots,
+                       "beta": beta if brange is None else list(brange),
                        "d_max": w.d_max, "et": "vnr+pce", "q_mode": "abs (syndrome mode)",
                        "parallelism": f"frame-shard x{world}",
                        "l2": "working set (~0.7 GB per GPU) >> 126 MB L2; no flush needed"},

@@ -127,6 +127,13 @@ int bpdec_sample_frames(const bpdec_code* code, double snr, uint64_t seed, int64
                         int32_t n_frames, int32_t all_zero, float* llr_out, uint8_t* x_out,
                         uint32_t* syndrome_out);
 
+/* Same, with a per-frame efficiency beta_f ~ U[beta_lo, beta_hi] drawn from a
+ * counter hash keyed by (seed, f) and snr_f = 2^(2R/beta_f) - 1 (BASELINE
+ * config 5, mixed-SNR stream); snr_out [n] (may be NULL) receives snr_f. */
+int bpdec_sample_frames_beta(const bpdec_code* code, double beta_lo, double beta_hi, uint64_t seed,
+                             int64_t first_frame, int32_t n_frames, int32_t all_zero, float* llr_out,
+                             uint8_t* x_out, uint32_t* syndrome_out, double* snr_out);
+
 /* -------------------------------------------------------------- decoder -- */
 /* ≙ BpDecoder::BpDecoder (decoder.hpp:57, decoder.cpp:38-48), batched: a
  * device replica of the code plus message state for max_slots frames in
@@ -165,6 +172,12 @@ int bpdec_decoder_sample_frames_device(bpdec_decoder* dec, double snr, uint64_t 
                                        int64_t first_frame, int32_t n_frames, int32_t all_zero,
                                        float* d_llr, uint32_t* d_syndrome, uint32_t* d_x_packed,
                                        void* stream);
+
+/* Device-side mixed-SNR generator (draws of bpdec_sample_frames_beta). */
+int bpdec_decoder_sample_frames_beta_device(bpdec_decoder* dec, double beta_lo, double beta_hi, uint64_t seed,
+                                            int64_t first_frame, int32_t n_frames, int32_t all_zero,
+                                            float* d_llr, uint32_t* d_syndrome, uint32_t* d_x_packed,
+                                            void* stream);
 
 /* Per-kernel timing of the most recent bpdec_decode_batch calls (CUDA events
  * on the launching stream).  Enable before decoding; kernel ids:

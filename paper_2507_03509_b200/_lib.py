@@ -53,6 +53,12 @@ SIGNATURES = [
     ("bpdec_snr_for_beta", C.c_int, [C.c_double, C.c_double, c_f64p]),
     ("bpdec_sample_frames", C.c_int,
      [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, c_f32p, c_u8p, c_u32p]),
+    ("bpdec_sample_frames_beta", C.c_int,
+     [C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, c_f32p, c_u8p, c_u32p,
+      c_f64p]),
+    ("bpdec_decoder_sample_frames_beta_device", C.c_int,
+     [C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+      C.c_void_p, C.c_void_p]),
     ("bpdec_decoder_create", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     ("bpdec_decoder_destroy", None, [C.c_void_p]),
     ("bpdec_decoder_slots", C.c_int, [C.c_void_p, c_i32p]),

@@ -229,46 +229,84 @@ int bpdec_snr_for_beta(double beta, double rate, double* snr) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Seeded syndrome-mode frames on the host (threaded).  snr_of(f) gives the
+// channel SNR of global frame f.
+template <typename SnrOf>
+void sample_frames_impl(const bpdec::Code& h, SnrOf snr_of, uint64_t seed, int64_t first_frame, int32_t n_frames,
+                        int32_t all_zero, float* llr_out, uint8_t* x_out, uint32_t* syndrome_out, double* snr_out) {
+  if (n_frames < 0) throw bpdec::ValidationError("sample: n_frames must be non-negative");
+  need(llr_out, "llr_out");
+  const int32_t n = h.n_vars;
+  const size_t mw = (h.n_checks + 31) / 32;
+  auto work = [&](int32_t b) {
+    const uint64_t f = static_cast<uint64_t>(first_frame + b);
+    // sample_block's arithmetic (channel.cpp:51-58) with the BPSK sign of x.
+    const double snr = snr_of(f);
+    const double sigma2 = 1.0 / snr;
+    const double sigma = std::sqrt(sigma2);
+    const double scale = 2.0 / sigma2;
+    if (snr_out) snr_out[b] = snr;
+    const uint64_t nkey = bpdec::stream_key(bpdec::kNoiseDomain, seed, f);
+    const uint64_t xkey = bpdec::stream_key(bpdec::kBitDomain, seed, f);
+    std::vector<uint8_t> x(n);
+    float* l = llr_out + static_cast<size_t>(b) * n;
+    for (int32_t i = 0; i < n; ++i) {
+      double u1, u2;
+      bpdec::noise_uniforms(nkey, static_cast<uint64_t>(i), &u1, &u2);
+      const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+      const unsigned xi = all_zero ? 0u : bpdec::message_bit(xkey, static_cast<uint64_t>(i));
+      x[i] = static_cast<uint8_t>(xi);
+      l[i] = static_cast<float>(scale * ((xi ? -1.0 : 1.0) + sigma * g));
+    }
+    if (x_out) std::copy(x.begin(), x.end(), x_out + static_cast<size_t>(b) * n);
+    if (syndrome_out) bpdec::compute_syndrome(h, x.data(), syndrome_out + b * mw);
+  };
+  const int nt = std::max(1, std::min(host_threads(), n_frames));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) {
+    pool.emplace_back([&, t] {
+      for (int32_t b = t; b < n_frames; b += nt) work(b);
+    });
+  }
+  for (auto& th : pool) th.join();
+}
+
+void check_beta_range(double lo, double hi) {
+  if (!(lo > 0.0) || hi > 1.0 || hi < lo) {
+    throw bpdec::ValidationError("sample: need 0 < beta_lo <= beta_hi <= 1");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 int bpdec_sample_frames(const bpdec_code* code, double snr, uint64_t seed, int64_t first_frame,
                         int32_t n_frames, int32_t all_zero, float* llr_out, uint8_t* x_out,
                         uint32_t* syndrome_out) {
   return guarded([&] {
     need(code, "code");
     if (!(snr > 0.0) || !std::isfinite(snr)) throw bpdec::ValidationError("sample: snr must be positive and finite");
-    if (n_frames < 0) throw bpdec::ValidationError("sample: n_frames must be non-negative");
-    need(llr_out, "llr_out");
-    const auto& h = code->code;
-    const int32_t n = h.n_vars;
-    const size_t mw = (h.n_checks + 31) / 32;
-    // sample_block's arithmetic (channel.cpp:51-58) with the BPSK sign of x.
-    const double sigma2 = 1.0 / snr;
-    const double sigma = std::sqrt(sigma2);
-    const double scale = 2.0 / sigma2;
-    auto work = [&](int32_t b) {
-      const uint64_t f = static_cast<uint64_t>(first_frame + b);
-      const uint64_t nkey = bpdec::stream_key(bpdec::kNoiseDomain, seed, f);
-      const uint64_t xkey = bpdec::stream_key(bpdec::kBitDomain, seed, f);
-      std::vector<uint8_t> x(n);
-      float* l = llr_out + static_cast<size_t>(b) * n;
-      for (int32_t i = 0; i < n; ++i) {
-        double u1, u2;
-        bpdec::noise_uniforms(nkey, static_cast<uint64_t>(i), &u1, &u2);
-        const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
-        const unsigned xi = all_zero ? 0u : bpdec::message_bit(xkey, static_cast<uint64_t>(i));
-        x[i] = static_cast<uint8_t>(xi);
-        l[i] = static_cast<float>(scale * ((xi ? -1.0 : 1.0) + sigma * g));
-      }
-      if (x_out) std::copy(x.begin(), x.end(), x_out + static_cast<size_t>(b) * n);
-      if (syndrome_out) bpdec::compute_syndrome(h, x.data(), syndrome_out + b * mw);
-    };
-    const int nt = std::max(1, std::min(host_threads(), n_frames));
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nt; ++t) {
-      pool.emplace_back([&, t] {
-        for (int32_t b = t; b < n_frames; b += nt) work(b);
-      });
-    }
-    for (auto& th : pool) th.join();
+    sample_frames_impl(code->code, [snr](uint64_t) { return snr; }, seed, first_frame, n_frames, all_zero, llr_out,
+                       x_out, syndrome_out, nullptr);
+  });
+}
+
+int bpdec_sample_frames_beta(const bpdec_code* code, double beta_lo, double beta_hi, uint64_t seed,
+                             int64_t first_frame, int32_t n_frames, int32_t all_zero, float* llr_out, uint8_t* x_out,
+                             uint32_t* syndrome_out, double* snr_out) {
+  return guarded([&] {
+    need(code, "code");
+    check_beta_range(beta_lo, beta_hi);
+    const double rate = code->code.rate();
+    sample_frames_impl(
+        code->code,
+        [=](uint64_t f) { return std::exp2(2.0 * rate / bpdec::frame_beta(seed, f, beta_lo, beta_hi)) - 1.0; }, seed,
+        first_frame, n_frames, all_zero, llr_out, x_out, syndrome_out, snr_out);
   });
 }
 
@@ -347,8 +385,22 @@ int bpdec_decoder_sample_frames_device(bpdec_decoder* dec, double snr, uint64_t 
   return guarded([&] {
     need(dec, "decoder");
     need(d_llr, "d_llr");
-    bpdec::gpu_sample_frames_device(dec->impl, snr, seed, first_frame, n_frames, all_zero != 0, d_llr,
+    if (!(snr > 0.0) || !std::isfinite(snr)) throw bpdec::ValidationError("sample: snr must be positive and finite");
+    bpdec::gpu_sample_frames_device(dec->impl, snr, 0.0, 0.0, 0.0, seed, first_frame, n_frames, all_zero != 0, d_llr,
                                     d_syndrome, d_x_packed, stream);
+  });
+}
+
+int bpdec_decoder_sample_frames_beta_device(bpdec_decoder* dec, double beta_lo, double beta_hi, uint64_t seed,
+                                            int64_t first_frame, int32_t n_frames, int32_t all_zero, float* d_llr,
+                                            uint32_t* d_syndrome, uint32_t* d_x_packed, void* stream) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(d_llr, "d_llr");
+    check_beta_range(beta_lo, beta_hi);
+    const double rate = static_cast<double>(dec->n_vars - dec->n_checks) / dec->n_vars;
+    bpdec::gpu_sample_frames_device(dec->impl, 0.0, beta_lo, beta_hi, rate, seed, first_frame, n_frames,
+                                    all_zero != 0, d_llr, d_syndrome, d_x_packed, stream);
   });
 }
 

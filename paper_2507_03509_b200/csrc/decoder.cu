@@ -1141,11 +1141,11 @@ __global__ void k_compact_commit(const Args a) {
 // ---------------------------------------------------------- generators --
 // Syndrome-mode frames on device; same draws as bpdec_sample_frames
 // (channel.cpp:44-61 with the message bit x and s = Hx on top).
-__global__ void k_gen_llr(int32_t N, int32_t NW, double snr, uint64_t seed, int64_t first_frame,
-                          int32_t n_frames, int32_t all_zero, float* llr, uint32_t* xpk) {
-  const double sigma2 = 1.0 / snr;
-  const double sigma = sqrt(sigma2);
-  const double scale = 2.0 / sigma2;
+// snr <= 0 selects per-frame efficiencies beta_f ~ U[beta_lo, beta_hi]
+// (config 5), snr = 2^(2R/beta_f) - 1.
+__global__ void k_gen_llr(int32_t N, int32_t NW, double snr_fixed, double beta_lo, double beta_hi, double rate,
+                          uint64_t seed, int64_t first_frame, int32_t n_frames, int32_t all_zero, float* llr,
+                          uint32_t* xpk) {
   const long long npad = (static_cast<long long>(N) + 31) / 32 * 32;
   const long long total = npad * n_frames;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -1153,6 +1153,11 @@ __global__ void k_gen_llr(int32_t N, int32_t NW, double snr, uint64_t seed, int6
     const int b = static_cast<int>(t / npad);
     const long long i = t - static_cast<long long>(b) * npad;
     const uint64_t f = static_cast<uint64_t>(first_frame + b);
+    const double snr =
+        snr_fixed > 0.0 ? snr_fixed : exp2(2.0 * rate / frame_beta(seed, f, beta_lo, beta_hi)) - 1.0;
+    const double sigma2 = 1.0 / snr;
+    const double sigma = sqrt(sigma2);
+    const double scale = 2.0 / sigma2;
     unsigned x = 0;
     if (i < N) {
       const uint64_t nkey = stream_key(kNoiseDomain, seed, f);
@@ -1234,7 +1239,8 @@ class GpuDecoder {
   GpuDecoder(const Code& code, int device, int max_slots);
   ~GpuDecoder();
   void decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t stream);
-  void sample_device(double snr, uint64_t seed, int64_t first_frame, int32_t n_frames, bool all_zero,
+  void sample_device(double snr, double beta_lo, double beta_hi, double rate, uint64_t seed, int64_t first_frame,
+                     int32_t n_frames, bool all_zero,
                      float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t stream);
 
   int S = 0;
@@ -1668,16 +1674,22 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   CUDA_OK(cudaStreamSynchronize(st));
 }
 
-void GpuDecoder::sample_device(double snr, uint64_t seed, int64_t first_frame, int32_t n_frames, bool all_zero,
+void GpuDecoder::sample_device(double snr, double beta_lo, double beta_hi, double rate, uint64_t seed,
+                               int64_t first_frame, int32_t n_frames, bool all_zero,
                                float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t st_in) {
   CUDA_OK(cudaSetDevice(device));
   const cudaStream_t st = st_in ? st_in : own_stream;
-  if (!(snr > 0.0) || !std::isfinite(snr)) throw ValidationError("sample: snr must be positive and finite");
+  if (snr > 0.0) {
+    if (!std::isfinite(snr)) throw ValidationError("sample: snr must be positive and finite");
+  } else if (!(beta_lo > 0.0) || beta_hi > 1.0 || beta_hi < beta_lo || !(rate > 0.0) || rate >= 1.0) {
+    throw ValidationError("sample: need snr > 0 or 0 < beta_lo <= beta_hi <= 1 and 0 < rate < 1");
+  }
   if (n_frames <= 0) return;
   uint32_t* x = d_x;
   Scratch tmp;
   if (x == nullptr && d_syn != nullptr) x = static_cast<uint32_t*>(tmp.get(static_cast<size_t>(n_frames) * base.NW * 4));
-  k_gen_llr<<<1184, kThreads, 0, st>>>(base.N, base.NW, snr, seed, first_frame, n_frames, all_zero ? 1 : 0, d_llr, x);
+  k_gen_llr<<<1184, kThreads, 0, st>>>(base.N, base.NW, snr > 0.0 ? snr : 0.0, beta_lo, beta_hi, rate, seed,
+                                       first_frame, n_frames, all_zero ? 1 : 0, d_llr, x);
   CUDA_OK(cudaGetLastError());
   ++launches;
   if (d_syn) {
@@ -1698,9 +1710,10 @@ int64_t gpu_decoder_device_bytes(const GpuDecoder* dec) { return dec->dev_bytes;
 void gpu_decode_batch(GpuDecoder* dec, const DecodeParams& p, const DecodeBuffers& b, void* stream) {
   dec->decode(p, b, static_cast<cudaStream_t>(stream));
 }
-void gpu_sample_frames_device(GpuDecoder* dec, double snr, uint64_t seed, int64_t first_frame, int32_t n_frames,
-                              bool all_zero, float* d_llr, uint32_t* d_syndrome, uint32_t* d_x_packed, void* stream) {
-  dec->sample_device(snr, seed, first_frame, n_frames, all_zero, d_llr, d_syndrome, d_x_packed,
+void gpu_sample_frames_device(GpuDecoder* dec, double snr, double beta_lo, double beta_hi, double rate, uint64_t seed,
+                              int64_t first_frame, int32_t n_frames, bool all_zero, float* d_llr, uint32_t* d_syndrome,
+                              uint32_t* d_x_packed, void* stream) {
+  dec->sample_device(snr, beta_lo, beta_hi, rate, seed, first_frame, n_frames, all_zero, d_llr, d_syndrome, d_x_packed,
                      static_cast<cudaStream_t>(stream));
 }
 void gpu_set_profiling(GpuDecoder* dec, bool enable) { dec->profiling = enable; }

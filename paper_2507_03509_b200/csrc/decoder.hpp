@@ -34,9 +34,10 @@ void gpu_decoder_destroy(GpuDecoder* dec);
 int gpu_decoder_slots(const GpuDecoder* dec);
 int64_t gpu_decoder_device_bytes(const GpuDecoder* dec);
 void gpu_decode_batch(GpuDecoder* dec, const DecodeParams& p, const DecodeBuffers& b, void* stream);
-void gpu_sample_frames_device(GpuDecoder* dec, double snr, uint64_t seed, int64_t first_frame,
-                              int32_t n_frames, bool all_zero, float* d_llr, uint32_t* d_syndrome,
-                              uint32_t* d_x_packed, void* stream);
+// snr > 0: fixed SNR; snr <= 0: per-frame beta ~ U[beta_lo, beta_hi] (rate R).
+void gpu_sample_frames_device(GpuDecoder* dec, double snr, double beta_lo, double beta_hi, double rate,
+                              uint64_t seed, int64_t first_frame, int32_t n_frames, bool all_zero, float* d_llr,
+                              uint32_t* d_syndrome, uint32_t* d_x_packed, void* stream);
 void gpu_set_profiling(GpuDecoder* dec, bool enable);
 void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches,
                  double* frame_iterations);

@@ -22,6 +22,8 @@ constexpr std::uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
 constexpr std::uint64_t kNoiseDomain = 0x243f6a8885a308d3ULL;
 // Key domain of the message-bit stream x (new; BASELINE syndrome mode).
 constexpr std::uint64_t kBitDomain = 0x13198a2e03707344ULL;
+// Key domain of the per-frame efficiency draw (BASELINE config 5).
+constexpr std::uint64_t kBetaDomain = 0xa4093822299f31d0ULL;
 
 BPDEC_HD std::uint64_t splitmix64(std::uint64_t z) {
   z += kGolden;
@@ -78,6 +80,13 @@ class SplitMixEngine {
 BPDEC_HD void noise_uniforms(std::uint64_t key, std::uint64_t i, double* u1, double* u2) {
   *u1 = uniform_open01(splitmix64(key ^ splitmix64(2 * i)));
   *u2 = uniform_open01(splitmix64(key ^ splitmix64(2 * i + 1)));
+}
+
+// Per-frame reconciliation efficiency beta_f ~ U[lo, hi] keyed by (seed, f).
+BPDEC_HD double frame_beta(std::uint64_t seed, std::uint64_t frame, double lo, double hi) {
+  if (!(hi > lo)) return lo;
+  const double u = uniform_open01(mix_key(mix_key(kBetaDomain, seed), frame));
+  return lo + (hi - lo) * u;
 }
 
 // Message bit i of a stream keyed `key` (top bit of the hashed counter).

@@ -46,7 +46,7 @@ __all__ = [
     "ParityCheckMatrix", "ActiveVarSet", "active_var_set", "load_alist", "save_alist",
     "lift_protograph", "generate_met", "DecodeConfig", "StopReason", "DecodeOutcome",
     "BatchResult", "BpDecoder", "BatchDecoder", "decode", "syndrome_check", "vnr_statistic",
-    "vnr_should_stop", "snr_for_beta", "sample_frames", "pack_bits", "unpack_bits",
+    "vnr_should_stop", "snr_for_beta", "sample_frames", "sample_frames_beta", "pack_bits", "unpack_bits",
 ]
 
 
@@ -368,10 +368,19 @@ class BatchDecoder:
                            out.get("q_trace"))
 
     def sample_frames_device(self, snr: float, seed: int, first_frame: int, n_frames: int, llr_dev,
-                             syndrome_dev=None, x_packed_dev=None, all_zero: bool = False, stream: int = 0):
+                             syndrome_dev=None, x_packed_dev=None, all_zero: bool = False, stream: int = 0,
+                             beta_range=None):
+        """Device-resident frames; beta_range=(lo, hi) draws beta_f per frame
+        (config 5) and ignores `snr`."""
+        st = C.c_void_p(stream) if stream else None
+        if beta_range is not None:
+            _check(self._lib.bpdec_decoder_sample_frames_beta_device(
+                self._h, float(beta_range[0]), float(beta_range[1]), seed, first_frame, n_frames, int(all_zero),
+                _ptr(llr_dev), _ptr(syndrome_dev), _ptr(x_packed_dev), st))
+            return
         _check(self._lib.bpdec_decoder_sample_frames_device(
             self._h, float(snr), seed, first_frame, n_frames, int(all_zero), _ptr(llr_dev), _ptr(syndrome_dev),
-            _ptr(x_packed_dev), C.c_void_p(stream) if stream else None))
+            _ptr(x_packed_dev), st))
 
     # profiling (CUDA events on the launching stream)
     KERNELS = ("check", "variable", "syndrome", "terminate", "load", "extract")
@@ -472,6 +481,20 @@ def sample_frames(code: ParityCheckMatrix, snr: float, seed: int, first_frame: i
     _check(code._lib.bpdec_sample_frames(code.handle, float(snr), seed, first_frame, n_frames, int(all_zero),
                                          _ptr(llr, _lib.c_f32p), _ptr(x, _lib.c_u8p), _ptr(s, _lib.c_u32p)))
     return llr, x, s
+
+
+def sample_frames_beta(code: ParityCheckMatrix, beta_lo: float, beta_hi: float, seed: int, first_frame: int,
+                       n_frames: int, all_zero: bool = False):
+    """Mixed-SNR frames (config 5): beta_f ~ U[lo, hi] per frame ->
+    (llr, x, s, snr[F])."""
+    llr = np.zeros((n_frames, code.n_vars), dtype=np.float32)
+    x = np.zeros((n_frames, code.n_vars), dtype=np.uint8)
+    s = np.zeros((n_frames, (code.n_checks + 31) // 32), dtype=np.uint32)
+    snr = np.zeros(n_frames, dtype=np.float64)
+    _check(code._lib.bpdec_sample_frames_beta(code.handle, float(beta_lo), float(beta_hi), seed, first_frame, n_frames,
+                                              int(all_zero), _ptr(llr, _lib.c_f32p), _ptr(x, _lib.c_u8p),
+                                              _ptr(s, _lib.c_u32p), _ptr(snr, _lib.c_f64p)))
+    return llr, x, s, snr
 
 
 def pack_bits(bits: np.ndarray) -> np.ndarray:

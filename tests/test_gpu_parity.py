@@ -305,3 +305,35 @@ def test_tail_compaction_is_transparent(P, cfg1_code):
         assert np.array_equal(o.bits[0], r.bits[f])
         assert np.array_equal(o.posteriors[0], r.posteriors[f])
         assert np.array_equal(o.q_trace[0], r.q_trace[f], equal_nan=True)
+
+
+# ------------------------------------------- BASELINE configs at full size --
+@pytest.mark.parametrize("key,frames,beta,modes", [
+    ("cfg2", 4, 0.95, (("vnr", 500), ("pce", 40))),
+    ("cfg3", 3, 0.98, (("vnr", 500), ("pce", 30))),
+    ("cfg5", 2, 0.96, (("vnr", 500),)),
+])
+def test_baseline_config_full_size_vs_reference(P, ref, key, frames, beta, modes):
+    """BASELINE.json configs 2, 3 and 5 at their full code sizes (N = 2^20 /
+    2^21): a few frames in the reference's semantics (L*(1-2x), s = 0, raw
+    q) against the compiled reference, same bar and tie rule.  PCE runs are
+    capped (the reference costs ~60 ns per edge-update)."""
+    w = P.WORKLOADS[key]
+    code = w.make_code()
+    snr = P.snr_for_beta(beta, code.rate())
+    llr, x, s = P.sample_frames(code, snr, P.FRAME_SEED, 0, frames)
+    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float32)
+    rc = _refcode(ref, code)
+    dec = P.BatchDecoder(code, max_slots=32)
+    for mode, d_max in modes:
+        pce, vnr = ET_MODES[mode]
+        r, tie = ref_ties(rc, leq, d_max=d_max, use_pce=pce, use_vnr=vnr, threads=8)
+        g = dec.decode_batch(leq, P.DecodeConfig(d_max=d_max, use_pce=pce, use_vnr=vnr), want_posteriors=True)
+        print(key, mode, compare(g, r, tie, min_nontie_frac=0.3, label=f"{key} {mode}"),
+              "gpu it", g.iterations.tolist(), "ref it", r["iterations"].tolist())
+        # size-independent properties on the same frames in true syndrome mode
+        gs = dec.decode_batch(llr, P.DecodeConfig(d_max=d_max, use_pce=pce, use_vnr=vnr, q_mode=P.decoder.Q_ABS),
+                              syndrome=s)
+        for f in range(frames):
+            if gs.reasons[f] == 0:
+                assert P.syndrome_check(code, gs.bits[f], s[f])  # success => H bits == s
