@@ -55,8 +55,9 @@ namespace {
   } while (0)
 
 constexpr int kLanes = 32;
-constexpr int kQTile = 128;     // variables per q partial sum (code-fixed order)
-constexpr int kVarWarps = 4;    // warps per k_var block; kQTile = kVarWarps * 32
+constexpr int kVarWarps = 4;    // warps per k_var block
+constexpr int kVarChunks = 4;   // consecutive 32-variable chunks per warp and tile
+constexpr int kQTile = kVarWarps * kVarChunks * 32;  // variables per q partial sum (code-fixed order)
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
 enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kLoad = 4, kExtract = 5, kNumKernels = 6 };
@@ -317,7 +318,7 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
 // shared memory, and no registers are held for data in flight.  Each lane
 // only reads back the elements it copied itself, so cp.async.wait_group is
 // the only synchronisation needed.
-constexpr int kStageRows = 12;  // rows per batch stage (check shapes)
+constexpr int kStageRows = 20;  // rows per batch stage (check shapes)
 constexpr int kStages = 3;      // ring depth: two batches in flight while one is computed
 constexpr int kRingRows = kStages * kStageRows;
 
@@ -412,44 +413,47 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
   cp_async_commit();
 }
 
-template <int NH, int ND, bool WANT_POST>
+// FM: some lane of the warp is in its first iteration (v2c = channel LLR,
+// unclamped, no previous c2v).  The steady state runs the FM = false copy.
+template <int NH, int ND, bool WANT_POST, bool FM>
 __device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p,
                                                     const uint32_t* ssyn, int i0, int lane, bool act, bool first,
                                                     float cl, float clamp, uint32_t* synw, uint32_t* d1w) {
   constexpr int D = NH + ND;
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NPH = K * NH;
+  constexpr uint32_t kSign = 0x80000000u;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    float m[D > 0 ? D : 1];    // |v2c|, clamped (cl = inf in the first iteration)
-    uint32_t sg[D > 0 ? D : 1];  // sign bits of v2c (the clamp keeps the sign)
+    float m[D > 0 ? D : 1];      // |v2c|, clamped (cl = inf in the first iteration)
+    uint32_t sm[D > 0 ? D : 1];  // sign masks of v2c (the clamp keeps the sign)
     float l = 0.0f;
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const float co = first ? 0.0f : stage[(NPH + k * NH + j) * kLanes];
-      const float v = stage[(k * NH + j) * kLanes] - co;
-      m[j] = fminf(fabsf(v), cl);
-      sg[j] = signbit_u(v);
+      const float c = stage[(NPH + k * NH + j) * kLanes];
+      const float v = stage[(k * NH + j) * kLanes] - (FM && first ? 0.0f : c);
+      m[j] = fminf(fabsf(v), FM ? cl : clamp);
+      sm[j] = __float_as_uint(v) & kSign;
     }
     if (ND) {
       l = stage[(2 * NPH + k) * kLanes];
-      m[NH] = fminf(fabsf(l), cl);
-      sg[NH] = signbit_u(l);
+      m[NH] = fminf(fabsf(l), FM ? cl : clamp);
+      sm[NH] = __float_as_uint(l) & kSign;
     }
     const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
-    uint32_t par = sbit;
+    uint32_t par = sbit << 31;  // sign of the product times (1 - 2 s_c)
 #pragma unroll
-    for (int j = 0; j < D; ++j) par ^= sg[j];
+    for (int j = 0; j < D; ++j) par ^= sm[j];
     float out[D > 0 ? D : 1];
     check_magnitudes<D>(m, out, clamp);
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const float o = with_sign(out[j], par ^ sg[j]);
+      const float o = __uint_as_float(__float_as_uint(out[j]) | (par ^ sm[j]));
       stcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o, act);
     }
     uint32_t dbit = 0u;
     if (ND) {
-      const float o = with_sign(out[NH], par ^ sg[NH]);
+      const float o = __uint_as_float(__float_as_uint(out[NH]) | (par ^ sm[NH]));
       const float pd = l + o;  // posterior of the degree-1 variable
       dbit = (act && pd < 0.0f) ? 1u : 0u;
       if (WANT_POST) st_pred(d1p + static_cast<size_t>(i0 + k) * kLanes, pd, act);
@@ -461,10 +465,10 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   }
 }
 
-template <int NH, int ND, bool WANT_POST>
-__device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
-                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
-                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
+template <int NH, int ND, bool WANT_POST, bool FM>
+__device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, int db, const int32_t* hh,
+                                                 const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
+                                                 uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NB = 32 / K;
   const float* post0 = a.post + static_cast<size_t>(g) * a.NV * kLanes;
@@ -494,10 +498,22 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
                                 (b + NS - 1) * K, lrow, lcol, qact, qc2v, pol);
     cp_async_wait_upto(min(NS - 1, NB - 1 - b));
     __syncwarp();  // rows were copied by other lanes
-    check_batch_compute<NH, ND, WANT_POST>(ring + lane + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
-                                           lane, act, first, cl, clamp, synw, d1w);
+    check_batch_compute<NH, ND, WANT_POST, FM>(ring + lane + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
+                                               lane, act, first, cl, clamp, synw, d1w);
     __syncwarp();  // stage is refilled in the next round
   }
+}
+
+template <int NH, int ND, bool WANT_POST>
+__device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
+                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
+                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
+  if (fmask)
+    check_chunk_loop<NH, ND, WANT_POST, true>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
+                                              d1w);
+  else
+    check_chunk_loop<NH, ND, WANT_POST, false>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
+                                               d1w);
 }
 
 template <int MAXD, bool WANT_POST>
@@ -614,11 +630,13 @@ constexpr int kVarStage = 32 * 24;  // staged edge ids per warp
 // rows (channel LLR + D messages), copied with cp.async into the per-warp
 // two-stage ring while the previous batch is summed from shared memory.
 constexpr int kVarRingRows = 48;  // per-warp ring of the variable kernel (rows of 128 B)
+constexpr int kVarStageRows = 12;  // rows per batch stage of the variable kernel
 
 template <int D>
 struct VarShape {
   static constexpr int RPV = D + 1;
-  static constexpr int K = kStageRows / RPV >= 8 ? 8 : (kStageRows / RPV >= 4 ? 4 : (kStageRows / RPV >= 2 ? 2 : 1));
+  static constexpr int K =
+      kVarStageRows / RPV >= 8 ? 8 : (kVarStageRows / RPV >= 4 ? 4 : (kVarStageRows / RPV >= 2 ? 2 : 1));
   static constexpr int ROWS = K * RPV;  // rows per batch
   static constexpr int NS = kVarRingRows / ROWS >= 6 ? 6 : kVarRingRows / ROWS;  // ring stages
   static_assert(NS >= 1, "variable degree too large for the ring");
@@ -722,12 +740,13 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
       continue;
     }
     const bool act = (amask >> lane) & 1u;
-    double acc = 0.0;
-    const int h0 = tile * kQTile + warp * kLanes;
-    const int nv = max(0, min(kLanes, a.NV - h0));
+    double acc = 0.0;  // this warp's chunks, summed in variable order
     const size_t gl = static_cast<size_t>(g) * a.NH;
     const size_t gv = static_cast<size_t>(g) * a.NV;
     const size_t ge = static_cast<size_t>(g) * a.EH;
+    for (int cc = 0; cc < kVarChunks; ++cc) {
+    const int h0 = tile * kQTile + (warp * kVarChunks + cc) * kLanes;
+    const int nv = max(0, min(kLanes, a.NV - h0));
     if (nv > 0) {
       if (lane < nv) s_ptr[warp][lane] = __ldg(&a.vptr[h0 + lane]);
       if (lane == 0) s_ptr[warp][nv] = __ldg(&a.vptr[h0 + nv]);
@@ -774,6 +793,8 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
       }
       if (lane < nv) a.hbits[gv + h0 + lane] = hw;
     }
+    __syncwarp();
+    }
     red[warp][lane] = acc;
     __syncthreads();
     if (warp == 0) {
@@ -791,29 +812,42 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
 // Thread = one check x 32 slots (bit-sliced); checks padded to a multiple of
 // 32 per group so a warp never straddles two groups.
 __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
+  // warp = 32 consecutive checks (lane = check) of one group; a group is
+  // skipped as soon as every active frame in it is known to fail
   const int lane = threadIdx.x & 31;
-  const long long mpad = (static_cast<long long>(a.M) + 31) / 32 * 32;
-  const long long total = static_cast<long long>(a.G) * mpad;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long w = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < total;) {
-    const int g = static_cast<int>(w / mpad);
-    const int c = static_cast<int>(w - g * mpad);
+  const int chunks = (a.M + 31) / 32;
+  const long long total = static_cast<long long>(a.G) * chunks;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;) {
+    const int g = static_cast<int>(w / chunks);
+    const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
     const uint32_t amask = a.group_active[g];
     const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]);
     if (amask == 0u || (fl & amask) == amask) {  // nothing left to learn in this group
-      w = skip_group(w, mpad, stride);
+      w = skip_group(w, chunks, nwarps);
       continue;
     }
+    const int c = ch * 32 + lane;
     uint32_t word = 0u;
     if (c < a.M) {
       word = a.synp[static_cast<size_t>(g) * a.M + c];
-      const int4 d = __ldg(&a.cdesc[c]);
-      for (int e = d.x; e < d.y; ++e) word ^= a.hbits[static_cast<size_t>(g) * a.NV + __ldg(&a.chk_hi_h[e])];
+      const int4 cdk = __ldg(&a.ctype[ch]);
+      int e0, e1;
+      if (cdk.x >= 0) {  // homogeneous chunk: NH hi edges per check, contiguous
+        const int nh = cdk.x >> 3;
+        e0 = cdk.y + lane * nh;
+        e1 = e0 + nh;
+      } else {
+        const int4 d = __ldg(&a.cdesc[c]);
+        e0 = d.x;
+        e1 = d.y;
+      }
+      for (int e = e0; e < e1; ++e) word ^= a.hbits[static_cast<size_t>(g) * a.NV + __ldg(&a.chk_hi_h[e])];
       word &= amask;
     }
     word = __reduce_or_sync(0xffffffffu, word);
     if (lane == 0 && word != 0u && (fl & word) != word) atomicOr(&a.fail[g], word);
-    w += stride;
+    w += nwarps;
   }
 }
 
@@ -1271,7 +1305,7 @@ class GpuDecoder {
   std::vector<cudaEvent_t> prof_ev;
   std::vector<int> prof_kid;
   Scratch s_llr, s_syn, s_bits, s_iters, s_reasons, s_post, s_qtrace;
-  int grid_check = 0, grid_var = 0, grid_syn = 0, grid_extract = 0;
+  int grid_check = 0, grid_var = 0, grid_syn = 0, grid_extract = 0, sms_ = 148;
   int load_item_blocks = 0, load_check_blocks = 0;
 };
 
@@ -1455,13 +1489,16 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   for (auto& e : ring_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   const int sms = prop.multiProcessorCount;
+  sms_ = sms;
   grid_check = sms * 16;
   grid_var = sms * 16;
   grid_syn = sms * 8;
   // load / extract are no-ops on most steps: keep their grids small
-  grid_extract = sms * 4;
-  load_item_blocks = sms * 4;
-  load_check_blocks = sms * 2;
+  // extract / load / compaction are no-ops on most steps: moderate grids
+  // (a launch of ~900 idle blocks costs ~15 us per step)
+  grid_extract = sms * 2;
+  load_item_blocks = sms * 2;
+  load_check_blocks = sms / 2;
 }
 
 GpuDecoder::~GpuDecoder() {
@@ -1536,7 +1573,7 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
   // tail compaction (no-op unless the queue is drained and live frames fit
   // in fewer groups; decided on the device, no host round trip)
   if (G > 1 && G <= kMaxCompactGroups) {
-    k_compact_move<<<grid_extract, kThreads, 0, st>>>(a);
+    k_compact_move<<<sms_, kThreads, 0, st>>>(a);
     k_compact_commit<<<1, 32, 0, st>>>(a);
     launches += 2;
   }

@@ -68,9 +68,14 @@ def ref_ties(refc, llr32, **kw):
         if drift[f] > 1.0:
             tie[f] = True
         if kw.get("use_vnr") and a["q_trace"] is not None:
+            # VNR comparisons that decided the run: k' = 2 .. stop-1 (no drop),
+            # and the stop iteration itself only if VNR fired there (PCE is
+            # checked first, decoder.cpp:115-122)
             k = int(a["iterations"][f])
+            last = k if int(a["reasons"][f]) == 1 else k - 1
             q = a["q_trace"][f, :k]
-            if k >= 2 and np.any(np.abs(np.diff(q)) <= Q_GAP_REL * np.maximum(np.abs(q[1:]), 1.0)):
+            gaps = np.abs(np.diff(q))[: max(last - 1, 0)]
+            if gaps.size and np.any(gaps <= Q_GAP_REL * np.maximum(np.abs(q[1:last]), 1.0)):
                 tie[f] = True
     a["drift"] = drift
     return a, tie
