@@ -16,7 +16,7 @@ NVFLAGS  := -O3 -std=c++20 $(ARCH) -lineinfo -Xcompiler -fPIC,-Wall -I$(CSRC) -I
 
 HOST_SRC := $(CSRC)/code.cpp $(CSRC)/c_api.cpp
 HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))
-CU_OBJ   := $(OBJDIR)/decoder.o
+CU_OBJ   := $(OBJDIR)/decoder.o $(OBJDIR)/harness.o
 HDRS     := $(wildcard $(CSRC)/*.hpp $(CSRC)/*.cuh) include/bpdec.h
 
 .PHONY: all lib oracle ref clean
@@ -28,9 +28,13 @@ $(OBJDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(CU_OBJ): $(CSRC)/decoder.cu $(HDRS)
+$(OBJDIR)/decoder.o: $(CSRC)/decoder.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/ptxas.log || (cat $(OBJDIR)/ptxas.log; false)
+
+$(OBJDIR)/harness.o: $(CSRC)/harness.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/ptxas_harness.log || (cat $(OBJDIR)/ptxas_harness.log; false)
 
 $(LIB): $(HOST_OBJ) $(CU_OBJ)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread

@@ -179,6 +179,41 @@ int bpdec_decoder_sample_frames_beta_device(bpdec_decoder* dec, double beta_lo, 
                                             float* d_llr, uint32_t* d_syndrome, uint32_t* d_x_packed,
                                             void* stream);
 
+/* ------------------------------------------------- Monte-Carlo harness -- */
+/* ≙ etdec::StopRule (channel.hpp:42-45) */
+typedef struct {
+  int64_t min_frame_errors; /* stop at this many frame errors (0 disables) */
+  int64_t max_frames;       /* or at this many frames (0 = uncapped)       */
+} bpdec_stop_rule;
+
+/* ≙ etdec::TrialStats (channel.hpp:47-61); the iteration histogram is
+ * returned separately ([d_max+1] counts). */
+typedef struct {
+  int64_t frames, frame_errors, undetected_errors;
+  double fer, fer_ci_low, fer_ci_high, d_bar;
+  int64_t iteration_sum;
+  int64_t stops_syndrome, stops_vnr, stops_max_iter;
+  int32_t hit_max_frames;
+  int32_t _pad;
+} bpdec_trial_stats;
+
+/* ≙ apply_puncture (puncture.hpp:26, puncture.cpp:16-48): positions
+ * [round(N - (N-M)/target)] ascending (caller buffer of N entries);
+ * *count and *effective_rate returned. */
+int bpdec_code_apply_puncture(const bpdec_code* code, double target_rate, uint64_t seed,
+                              int32_t* punctured_out, int32_t* count, double* effective_rate);
+/* ≙ wilson_interval (channel.hpp:63, channel.cpp:63-72) */
+int bpdec_wilson_interval(int64_t k, int64_t n, double* lo, double* hi);
+/* ≙ run_trials (channel.hpp:72-74, channel.cpp:74-156) on the GPU: trials
+ * 0,1,2,... of the all-zero codeword at `snr` (sample_block draws, rounded to
+ * float32), punctured positions at LLR 0, decoded `block` at a time; the stop
+ * rule is applied to the exact trial-index prefix, so results do not depend
+ * on `block` (the reference's worker-count invariance).  A frame error is
+ * bits != 0 or reason != syndrome (channel.cpp:109-112). */
+int bpdec_run_trials(bpdec_decoder* dec, double snr, const int32_t* punctured, int32_t n_punctured,
+                     const bpdec_config* cfg, const bpdec_stop_rule* stop, uint64_t seed, int32_t block,
+                     bpdec_trial_stats* stats_out, int64_t* histogram_out);
+
 /* Per-kernel timing of the most recent bpdec_decode_batch calls (CUDA events
  * on the launching stream).  Enable before decoding; kernel ids:
  * 0 check-node, 1 variable-node, 2 syndrome, 3 termination, 4 load, 5 extract. */

@@ -70,6 +70,10 @@ class Reference:
         L.etref_snr_for_beta.argtypes = [f64, f64]
         L.etref_noise_normal.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(f64)]
         L.etref_sample_block.argtypes = [f64, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(f64)]
+        L.etref_apply_puncture.argtypes = [vp, f64, C.c_uint64, C.POINTER(C.c_int), C.POINTER(f64)]
+        L.etref_run_trials.argtypes = [vp, C.POINTER(C.c_int), C.c_int, f64, C.c_int, C.c_int, C.c_int, f64, C.c_long,
+                                       C.c_long, C.c_uint64, C.c_int, C.POINTER(C.c_int64), C.POINTER(f64),
+                                       C.POINTER(C.c_int64), C.c_int]
         L.etref_vnr_statistic.restype = f64
         L.etref_vnr_statistic.argtypes = [C.POINTER(f64), C.POINTER(C.c_int), C.c_int]
         self.L = L
@@ -145,6 +149,31 @@ class RefCode:
         if r < 0:
             raise OracleError(-r)
         return bool(r)
+
+    def apply_puncture(self, target_rate, seed):
+        out = np.zeros(self.n_vars, dtype=np.int32)
+        eff = C.c_double()
+        n = self.ref.L.etref_apply_puncture(self.h, target_rate, seed, _p(out, C.c_int), C.byref(eff))
+        if n < 0:
+            raise OracleError(-n)
+        return out[:n], eff.value
+
+    def run_trials(self, beta, punctured=None, d_max=100, use_pce=True, use_vnr=False, msg_clamp=30.0,
+                   min_frame_errors=100, max_frames=10000, seed=1, workers=8):
+        """The reference's own run_trials (channel.cpp:74-156)."""
+        p = np.ascontiguousarray(np.zeros(0) if punctured is None else punctured, dtype=np.int32)
+        st = np.zeros(8, dtype=np.int64)
+        ds = np.zeros(4, dtype=np.float64)
+        hist = np.zeros(d_max + 1, dtype=np.int64)
+        r = self.ref.L.etref_run_trials(self.h, _p(p, C.c_int), p.size, beta, d_max, int(use_pce), int(use_vnr),
+                                        msg_clamp, min_frame_errors, max_frames, seed, workers, _p(st, C.c_int64),
+                                        _p(ds, C.c_double), _p(hist, C.c_int64), hist.size)
+        if r:
+            raise OracleError(r)
+        return dict(frames=int(st[0]), frame_errors=int(st[1]), undetected_errors=int(st[2]),
+                    iteration_sum=int(st[3]), stops_syndrome=int(st[4]), stops_vnr=int(st[5]),
+                    stops_max_iter=int(st[6]), hit_max_frames=bool(st[7]), fer=ds[0], fer_ci_low=ds[1],
+                    fer_ci_high=ds[2], d_bar=ds[3], histogram={int(k): int(v) for k, v in enumerate(hist) if v})
 
     def decode_batch(self, llr, d_max=100, use_pce=True, use_vnr=False, msg_clamp=30.0, threads=1,
                      want_posteriors=True, want_q_trace=True):

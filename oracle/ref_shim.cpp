@@ -14,6 +14,7 @@
 #include <etdec/errors.hpp>
 #include <etdec/parity_check_matrix.hpp>
 #include <etdec/protograph.hpp>
+#include <etdec/puncture.hpp>
 #include <etdec/rng.hpp>
 
 #include <algorithm>
@@ -236,6 +237,52 @@ double etref_vnr_statistic(const double* posteriors, const int* members, int cou
   int max_id = 0;
   for (int i = 0; i < count; ++i) max_id = std::max(max_id, members[i]);
   return etdec::vnr_statistic(std::span<const double>(posteriors, static_cast<size_t>(max_id) + 1), a);
+}
+
+// apply_puncture (puncture.cpp:16-48): writes positions, returns count (<0: -status)
+int etref_apply_puncture(const void* code, double target_rate, uint64_t seed, int* out, double* eff) {
+  try {
+    const auto m = etdec::apply_puncture(*static_cast<const etdec::ParityCheckMatrix*>(code), target_rate, seed);
+    std::copy(m.punctured.begin(), m.punctured.end(), out);
+    *eff = m.effective_rate;
+    return static_cast<int>(m.punctured.size());
+  } catch (const std::exception& e) {
+    return -classify(e);
+  }
+}
+
+// run_trials (channel.cpp:74-156) with its own std::thread workers.
+// stats: frames, errors, undetected, iteration_sum, stops_syn, stops_vnr,
+// stops_max, hit_max (int64[8]); dstats: fer, ci_lo, ci_hi, d_bar (double[4]).
+int etref_run_trials(const void* code, const int* punctured, int n_punct, double beta, int d_max, int use_pce,
+                     int use_vnr, double clamp, long min_err, long max_frames, uint64_t seed, int workers,
+                     int64_t* stats, double* dstats, int64_t* hist, int hist_len) {
+  try {
+    const auto& h = *static_cast<const etdec::ParityCheckMatrix*>(code);
+    etdec::PunctureMask mask;
+    mask.punctured.assign(punctured, punctured + n_punct);
+    const auto point = etdec::snr_for_beta(beta, h.rate());
+    etdec::DecodeConfig cfg{d_max, use_pce != 0, use_vnr != 0, clamp};
+    etdec::StopRule stop{min_err, max_frames};
+    const auto st = etdec::run_trials(h, mask, point, cfg, stop, seed, workers);
+    stats[0] = st.frames;
+    stats[1] = st.frame_errors;
+    stats[2] = st.undetected_errors;
+    stats[3] = st.iteration_sum;
+    stats[4] = st.stops_syndrome;
+    stats[5] = st.stops_vnr;
+    stats[6] = st.stops_max_iter;
+    stats[7] = st.hit_max_frames ? 1 : 0;
+    dstats[0] = st.fer;
+    dstats[1] = st.fer_ci_low;
+    dstats[2] = st.fer_ci_high;
+    dstats[3] = st.d_bar;
+    for (const auto& [k, v] : st.iteration_histogram)
+      if (k >= 0 && k < hist_len) hist[k] = v;
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
 }
 
 }  // extern "C"

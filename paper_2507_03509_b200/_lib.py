@@ -32,6 +32,19 @@ class Config(C.Structure):
     ]
 
 
+class StopRule(C.Structure):
+    """bpdec_stop_rule (≙ etdec::StopRule, channel.hpp:42-45)."""
+    _fields_ = [("min_frame_errors", C.c_int64), ("max_frames", C.c_int64)]
+
+
+class TrialStatsC(C.Structure):
+    """bpdec_trial_stats (≙ etdec::TrialStats, channel.hpp:47-61)."""
+    _fields_ = [("frames", C.c_int64), ("frame_errors", C.c_int64), ("undetected_errors", C.c_int64),
+                ("fer", C.c_double), ("fer_ci_low", C.c_double), ("fer_ci_high", C.c_double), ("d_bar", C.c_double),
+                ("iteration_sum", C.c_int64), ("stops_syndrome", C.c_int64), ("stops_vnr", C.c_int64),
+                ("stops_max_iter", C.c_int64), ("hit_max_frames", C.c_int32), ("_pad", C.c_int32)]
+
+
 # (name, restype, argtypes) for every symbol in include/bpdec.h
 SIGNATURES = [
     ("bpdec_abi_version", C.c_int, []),
@@ -69,6 +82,11 @@ SIGNATURES = [
     ("bpdec_decoder_sample_frames_device", C.c_int,
      [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
       C.c_void_p, C.c_void_p]),
+    ("bpdec_code_apply_puncture", C.c_int, [C.c_void_p, C.c_double, C.c_uint64, c_i32p, c_i32p, c_f64p]),
+    ("bpdec_wilson_interval", C.c_int, [C.c_int64, C.c_int64, c_f64p, c_f64p]),
+    ("bpdec_run_trials", C.c_int,
+     [C.c_void_p, C.c_double, c_i32p, C.c_int32, C.POINTER(Config), C.POINTER(StopRule), C.c_uint64, C.c_int32,
+      C.POINTER(TrialStatsC), c_i64p]),
     ("bpdec_decoder_set_profiling", C.c_int, [C.c_void_p, C.c_int32]),
     ("bpdec_decoder_profile", C.c_int, [C.c_void_p, C.c_int32, c_f64p, c_i64p, c_f64p]),
     ("bpdec_decoder_reset_profile", C.c_int, [C.c_void_p]),

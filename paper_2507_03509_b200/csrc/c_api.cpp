@@ -13,6 +13,7 @@
 
 #include "code.hpp"
 #include "decoder.hpp"
+#include "harness.hpp"
 #include "rng.hpp"
 
 struct bpdec_code {
@@ -401,6 +402,72 @@ int bpdec_decoder_sample_frames_beta_device(bpdec_decoder* dec, double beta_lo, 
     const double rate = static_cast<double>(dec->n_vars - dec->n_checks) / dec->n_vars;
     bpdec::gpu_sample_frames_device(dec->impl, 0.0, beta_lo, beta_hi, rate, seed, first_frame, n_frames,
                                     all_zero != 0, d_llr, d_syndrome, d_x_packed, stream);
+  });
+}
+
+int bpdec_code_apply_puncture(const bpdec_code* code, double target_rate, uint64_t seed, int32_t* punctured_out,
+                              int32_t* count, double* effective_rate) {
+  return guarded([&] {
+    need(code, "code");
+    need(count, "count");
+    double eff = 0.0;
+    const auto v = bpdec::apply_puncture(code->code, target_rate, seed, &eff);
+    if (!v.empty()) {
+      need(punctured_out, "punctured_out");
+      std::copy(v.begin(), v.end(), punctured_out);
+    }
+    *count = static_cast<int32_t>(v.size());
+    if (effective_rate) *effective_rate = eff;
+  });
+}
+
+int bpdec_wilson_interval(int64_t k, int64_t n, double* lo, double* hi) {
+  return guarded([&] {
+    if (n <= 0 || k < 0 || k > n) throw bpdec::ValidationError("wilson_interval: need 0 <= k <= n, n > 0");
+    const auto ci = bpdec::wilson_interval(k, n);
+    if (lo) *lo = ci.first;
+    if (hi) *hi = ci.second;
+  });
+}
+
+int bpdec_run_trials(bpdec_decoder* dec, double snr, const int32_t* punctured, int32_t n_punctured,
+                     const bpdec_config* cfg, const bpdec_stop_rule* stop, uint64_t seed, int32_t block,
+                     bpdec_trial_stats* stats_out, int64_t* histogram_out) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(cfg, "cfg");
+    need(stop, "stop");
+    need(stats_out, "stats_out");
+    if (cfg->d_max <= 0) throw bpdec::ValidationError("decode: d_max must be positive");
+    if (!(cfg->msg_clamp > 0.0)) throw bpdec::ValidationError("decode: msg_clamp must be positive");
+    bpdec::DecodeParams p;
+    p.d_max = cfg->d_max;
+    p.use_pce = cfg->use_pce ? 1 : 0;
+    p.use_vnr = cfg->use_vnr ? 1 : 0;
+    p.q_mode = cfg->q_mode;
+    p.msg_clamp = static_cast<float>(cfg->msg_clamp);
+    std::vector<int32_t> punct;
+    if (n_punctured > 0) {
+      need(punctured, "punctured");
+      punct.assign(punctured, punctured + n_punctured);
+    }
+    const auto st = bpdec::run_trials(dec->impl, dec->n_vars, dec->n_checks, snr, punct, p, stop->min_frame_errors,
+                                      stop->max_frames, seed, block);
+    bpdec_trial_stats o{};
+    o.frames = st.frames;
+    o.frame_errors = st.frame_errors;
+    o.undetected_errors = st.undetected_errors;
+    o.fer = st.fer;
+    o.fer_ci_low = st.fer_ci_low;
+    o.fer_ci_high = st.fer_ci_high;
+    o.d_bar = st.d_bar;
+    o.iteration_sum = st.iteration_sum;
+    o.stops_syndrome = st.stops_syndrome;
+    o.stops_vnr = st.stops_vnr;
+    o.stops_max_iter = st.stops_max_iter;
+    o.hit_max_frames = st.hit_max_frames ? 1 : 0;
+    *stats_out = o;
+    if (histogram_out) std::copy(st.histogram.begin(), st.histogram.end(), histogram_out);
   });
 }
 

@@ -422,6 +422,42 @@ Code generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1,
   return Code::from_csr(n_vars, n_checks, ptr.data(), vars.data());
 }
 
+std::vector<int32_t> apply_puncture(const Code& code, double target_rate, uint64_t seed, double* effective_rate) {
+  const double rate = code.rate();
+  if (target_rate >= 1.0) throw ValidationError("puncture: target rate must be below 1");
+  if (target_rate < rate - 1e-12) {
+    throw ValidationError("puncture: target rate " + std::to_string(target_rate) + " is below the code rate " +
+                          std::to_string(rate) + "; puncturing can only raise the rate");
+  }
+  const int32_t n = code.n_vars, m = code.n_checks;
+  const long count = std::lround(n - (n - m) / target_rate);
+  if (count <= 0) {
+    if (effective_rate) *effective_rate = rate;
+    return {};
+  }
+  std::vector<int32_t> eligible;
+  for (int32_t v = 0; v < n; ++v)
+    if (code.var_degree(v) >= 2) eligible.push_back(v);
+  if (count > static_cast<long>(eligible.size())) {
+    throw ValidationError("puncture: need " + std::to_string(count) + " positions but only " +
+                          std::to_string(eligible.size()) + " variables of degree >= 2 are eligible");
+  }
+  // k distinct draws from [0, n_eligible): partial Fisher-Yates in draw order
+  SplitMixEngine rng(seed);
+  const uint32_t pool_n = static_cast<uint32_t>(eligible.size());
+  std::vector<uint32_t> pool(pool_n);
+  for (uint32_t i = 0; i < pool_n; ++i) pool[i] = i;
+  std::vector<int32_t> out(count);
+  for (long i = 0; i < count; ++i) {
+    const uint64_t j = static_cast<uint64_t>(i) + rng.bounded(pool_n - static_cast<uint64_t>(i));
+    std::swap(pool[i], pool[j]);
+    out[i] = eligible[pool[i]];
+  }
+  std::sort(out.begin(), out.end());
+  if (effective_rate) *effective_rate = static_cast<double>(n - m) / static_cast<double>(n - count);
+  return out;
+}
+
 void compute_syndrome(const Code& code, const uint8_t* bits, uint32_t* syndrome) {
   const int32_t words = (code.n_checks + 31) / 32;
   std::fill(syndrome, syndrome + words, 0u);

@@ -77,6 +77,11 @@ Code generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1,
                   const std::vector<int32_t>& degrees, const std::vector<double>& probs,
                   uint64_t seed);
 
+// ≙ apply_puncture (puncture.cpp:16-48): round(N - (N-M)/target) positions
+// drawn uniformly (partial Fisher-Yates, SplitMixEngine(seed)) from the
+// degree>=2 variables, ascending.  Returns the positions; *effective_rate set.
+std::vector<int32_t> apply_puncture(const Code& code, double target_rate, uint64_t seed, double* effective_rate);
+
 // s = H x, packed LSB-first into ceil(M/32) words.
 void compute_syndrome(const Code& code, const uint8_t* bits, uint32_t* syndrome);
 

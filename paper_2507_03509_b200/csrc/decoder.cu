@@ -56,7 +56,7 @@ namespace {
 
 constexpr int kLanes = 32;
 constexpr int kVarWarps = 4;    // warps per k_var block
-constexpr int kVarChunks = 4;   // consecutive 32-variable chunks per warp and tile
+constexpr int kVarChunks = 1;   // consecutive 32-variable chunks per warp and tile
 constexpr int kQTile = kVarWarps * kVarChunks * 32;  // variables per q partial sum (code-fixed order)
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
@@ -1494,11 +1494,9 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   grid_var = sms * 16;
   grid_syn = sms * 8;
   // load / extract are no-ops on most steps: keep their grids small
-  // extract / load / compaction are no-ops on most steps: moderate grids
-  // (a launch of ~900 idle blocks costs ~15 us per step)
-  grid_extract = sms * 2;
-  load_item_blocks = sms * 2;
-  load_check_blocks = sms / 2;
+  grid_extract = sms * 4;
+  load_item_blocks = sms * 4;
+  load_check_blocks = sms * 2;
 }
 
 GpuDecoder::~GpuDecoder() {

@@ -47,6 +47,7 @@ __all__ = [
     "lift_protograph", "generate_met", "DecodeConfig", "StopReason", "DecodeOutcome",
     "BatchResult", "BpDecoder", "BatchDecoder", "decode", "syndrome_check", "vnr_statistic",
     "vnr_should_stop", "snr_for_beta", "sample_frames", "sample_frames_beta", "pack_bits", "unpack_bits",
+    "PunctureMask", "no_puncture", "apply_puncture", "StopRule", "TrialStats", "wilson_interval", "run_trials",
 ]
 
 
@@ -495,6 +496,82 @@ def sample_frames_beta(code: ParityCheckMatrix, beta_lo: float, beta_hi: float, 
                                               int(all_zero), _ptr(llr, _lib.c_f32p), _ptr(x, _lib.c_u8p),
                                               _ptr(s, _lib.c_u32p), _ptr(snr, _lib.c_f64p)))
     return llr, x, s, snr
+
+
+# ------------------------------------------------------- Monte-Carlo harness --
+@dataclass
+class PunctureMask:
+    """≙ etdec::PunctureMask (puncture.hpp:14-21)."""
+    punctured: np.ndarray
+    effective_rate: float
+
+    def empty(self) -> bool:
+        return self.punctured.size == 0
+
+
+def no_puncture(code: ParityCheckMatrix) -> PunctureMask:
+    return PunctureMask(np.zeros(0, dtype=np.int32), code.rate())
+
+
+def apply_puncture(code: ParityCheckMatrix, target_rate: float, seed: int) -> PunctureMask:
+    """≙ apply_puncture (puncture.cpp:16-48), same positions for the same seed."""
+    out = np.zeros(code.n_vars, dtype=np.int32)
+    cnt = C.c_int32()
+    eff = C.c_double()
+    _check(code._lib.bpdec_code_apply_puncture(code.handle, float(target_rate), seed, _ptr(out, _lib.c_i32p),
+                                               C.byref(cnt), C.byref(eff)))
+    return PunctureMask(out[: cnt.value].copy(), eff.value)
+
+
+@dataclass
+class StopRule:
+    """≙ etdec::StopRule (channel.hpp:42-45)."""
+    min_frame_errors: int = 100
+    max_frames: int = 10000
+
+
+@dataclass
+class TrialStats:
+    """≙ etdec::TrialStats (channel.hpp:47-61)."""
+    frames: int
+    frame_errors: int
+    undetected_errors: int
+    fer: float
+    fer_ci_low: float
+    fer_ci_high: float
+    d_bar: float
+    iteration_sum: int
+    iteration_histogram: dict
+    stops_syndrome: int
+    stops_vnr: int
+    stops_max_iter: int
+    hit_max_frames: bool
+
+
+def wilson_interval(k: int, n: int):
+    """≙ wilson_interval (channel.cpp:63-72)."""
+    lo, hi = C.c_double(), C.c_double()
+    _check(_lib.load().bpdec_wilson_interval(int(k), int(n), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def run_trials(dec: "BatchDecoder", snr: float, cfg: DecodeConfig, stop: StopRule, master_seed: int,
+               mask: Optional[PunctureMask] = None, block: Optional[int] = None) -> TrialStats:
+    """≙ run_trials (channel.cpp:74-156) on the GPU: trials 0,1,2,... of the
+    all-zero codeword, prefix-exact stop rule; results do not depend on
+    `block` (frames decoded per device batch, default = the decoder's slots)."""
+    lib = dec._lib
+    p = None if mask is None or mask.empty() else np.ascontiguousarray(mask.punctured, dtype=np.int32)
+    st = _lib.TrialStatsC()
+    hist = np.zeros(cfg.d_max + 1, dtype=np.int64)
+    c = cfg.c_struct()
+    sr = _lib.StopRule(int(stop.min_frame_errors), int(stop.max_frames))
+    _check(lib.bpdec_run_trials(dec.handle, float(snr), _ptr(p, _lib.c_i32p), 0 if p is None else p.size, C.byref(c),
+                                C.byref(sr), master_seed, int(block or dec.slots), C.byref(st),
+                                _ptr(hist, _lib.c_i64p)))
+    return TrialStats(st.frames, st.frame_errors, st.undetected_errors, st.fer, st.fer_ci_low, st.fer_ci_high,
+                      st.d_bar, st.iteration_sum, {int(k): int(v) for k, v in enumerate(hist) if v},
+                      st.stops_syndrome, st.stops_vnr, st.stops_max_iter, bool(st.hit_max_frames))
 
 
 def pack_bits(bits: np.ndarray) -> np.ndarray:
