@@ -23,8 +23,9 @@
 //   k_syndrome  bit-sliced parity of every check vs the target syndrome
 //               (decoder.cpp:19-30), 32 frames per 32-bit word
 //   k_terminate PCE -> VNR -> d_max decision per frame (decoder.cpp:114-123)
-//   k_extract   outputs of frames that stopped this step (:126-128)
-//   k_load      streams the next frames into freed slots
+//   k_turnover  outputs of frames that stopped this step (:126-128) and
+//               the next queued frames streamed into the freed slots
+//   k_compact   tail compaction of the live frames into fewer groups
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -60,7 +61,9 @@ constexpr int kVarChunks = 1;   // consecutive 32-variable chunks per warp and t
 constexpr int kQTile = kVarWarps * kVarChunks * 32;  // variables per q partial sum (code-fixed order)
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
-enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kLoad = 4, kExtract = 5, kNumKernels = 6 };
+enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompact = 5, kNumKernels = 6 };
+constexpr int kTermBlocks = 16;   // k_terminate blocks per group (q partial tree: fixed by the code)
+constexpr int kTermThreads = 256;
 
 // ------------------------------------------------------------ arguments --
 struct Args {
@@ -72,8 +75,7 @@ struct Args {
   const int32_t* vptr;      // [NV+1]
   const int32_t* vedge;     // [EH] c2v row of each edge of variable h, ascending check
   const int32_t* vmap;      // [N] original var -> h (>=0) or -1-d (degree 1)
-  const int32_t* dorig;     // [N] device item (H then D1) -> original var
-  const int32_t* corig;     // [M] device check -> original check
+  const int32_t* cdev;      // [M] original check -> device check
   const int4* ctype;        // [ceil(M/32)] {type NH*8+ND (homogeneous full chunk) or -1,
                             //  first hi edge, first degree-1 row, hi edge end}
   const int32_t* vtype;     // [ceil(NV/32)] chunk degree (homogeneous, full) or -1
@@ -89,6 +91,9 @@ struct Args {
   uint32_t* synp;           // [G][M]  target syndrome ^ degree-1 parity
   uint32_t* syn_target;     // [G][M]
   double* q_part;           // [G][n_tiles][32]
+  double* q_mid;            // [G][kTermBlocks][32]
+  int32_t* term_cnt;        // [G] k_terminate blocks done (last block decides)
+  int32_t* stop_frame;      // [S] frame that stopped in the slot this step (read by k_turnover)
   double* qprev;            // [S]
   int32_t* slot_iter;       // [S] iteration the slot runs next (1-based)
   int32_t* slot_frame;      // [S]
@@ -524,7 +529,8 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   __shared__ uint32_t s_syn[kCheckThreads / 32][32];
   __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
   __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRingRows * kLanes];
-  if (blockIdx.x == 0 && threadIdx.x < a.G) a.fail[threadIdx.x] = 0u;
+  if (blockIdx.x == 0)
+    for (int t = threadIdx.x; t < a.G; t += blockDim.x) a.fail[t] = 0u;
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
   const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -811,220 +817,380 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
 // ---------------------------------------------------------- k_syndrome --
 // Thread = one check x 32 slots (bit-sliced); checks padded to a multiple of
 // 32 per group so a warp never straddles two groups.
+// Parity of one check's degree>=2 part in group g: XOR of the gathered
+// hard-bit words (indices already in registers, loads independent).
+template <int NH>
+__device__ __forceinline__ uint32_t syn_hi_fixed(const uint32_t* __restrict__ hb, const int32_t (&idx)[4]) {
+  uint32_t w[NH];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) w[j] = hb[idx[j]];
+  uint32_t x = 0u;
+#pragma unroll
+  for (int j = 0; j < NH; ++j) x ^= w[j];
+  return x;
+}
+
 __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
-  // warp = 32 consecutive checks (lane = check) of one group; a group is
-  // skipped as soon as every active frame in it is known to fail
+  // warp = 32 consecutive checks (lane = check), all groups: the gather
+  // indices are loaded once and reused by every live group.  Failing frames
+  // are OR-ed into a block-local word per group (shared memory) and pushed
+  // to the global mask once per block; a group is skipped as soon as every
+  // active frame in it is known to fail.
+  extern __shared__ uint32_t s_fail[];  // [G]
+  for (int t = threadIdx.x; t < a.G; t += blockDim.x) s_fail[t] = 0u;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int chunks = (a.M + 31) / 32;
-  const long long total = static_cast<long long>(a.G) * chunks;
-  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  for (long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;) {
-    const int g = static_cast<int>(w / chunks);
-    const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
-    const uint32_t amask = a.group_active[g];
-    const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]);
-    if (amask == 0u || (fl & amask) == amask) {  // nothing left to learn in this group
-      w = skip_group(w, chunks, nwarps);
-      continue;
+  const int nwarps = static_cast<int>((static_cast<long long>(gridDim.x) * blockDim.x) >> 5);
+  for (int ch = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); ch < chunks;
+       ch += nwarps) {
+    bool live = false;
+    for (int g = 0; g < a.G && !live; ++g) {
+      const uint32_t amask = a.group_active[g];
+      const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
+      live = amask != 0u && (fl & amask) != amask;
     }
+    if (!live) continue;  // warp-uniform
     const int c = ch * 32 + lane;
-    uint32_t word = 0u;
-    if (c < a.M) {
-      word = a.synp[static_cast<size_t>(g) * a.M + c];
-      const int4 cdk = __ldg(&a.ctype[ch]);
-      int e0, e1;
-      if (cdk.x >= 0) {  // homogeneous chunk: NH hi edges per check, contiguous
-        const int nh = cdk.x >> 3;
-        e0 = cdk.y + lane * nh;
-        e1 = e0 + nh;
-      } else {
-        const int4 d = __ldg(&a.cdesc[c]);
-        e0 = d.x;
-        e1 = d.y;
-      }
-      for (int e = e0; e < e1; ++e) word ^= a.hbits[static_cast<size_t>(g) * a.NV + __ldg(&a.chk_hi_h[e])];
-      word &= amask;
+    const bool valid = c < a.M;
+    const int4 cdk = __ldg(&a.ctype[ch]);
+    int nh, e0;
+    if (cdk.x >= 0) {  // homogeneous chunk: NH hi edges per check, contiguous
+      nh = cdk.x >> 3;
+      e0 = cdk.y + lane * nh;
+    } else if (valid) {
+      const int4 d = __ldg(&a.cdesc[c]);
+      e0 = d.x;
+      nh = d.y - d.x;
+    } else {
+      e0 = 0;
+      nh = 0;
     }
-    word = __reduce_or_sync(0xffffffffu, word);
-    if (lane == 0 && word != 0u && (fl & word) != word) atomicOr(&a.fail[g], word);
-    w += nwarps;
+    const bool fixed = cdk.x >= 0 && nh <= 4;
+    int32_t idx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) idx[j] = (fixed && j < nh) ? __ldg(&a.chk_hi_h[e0 + j]) : 0;
+    for (int g = 0; g < a.G; ++g) {
+      const uint32_t amask = a.group_active[g];
+      const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
+      if (amask == 0u || (fl & amask) == amask) continue;  // warp-uniform
+      const uint32_t* hb = a.hbits + static_cast<size_t>(g) * a.NV;
+      uint32_t word = 0u;
+      if (valid) {
+        word = a.synp[static_cast<size_t>(g) * a.M + c];
+        if (fixed) {
+          switch (nh) {
+            case 0: break;
+            case 1: word ^= syn_hi_fixed<1>(hb, idx); break;
+            case 2: word ^= syn_hi_fixed<2>(hb, idx); break;
+            case 3: word ^= syn_hi_fixed<3>(hb, idx); break;
+            default: word ^= syn_hi_fixed<4>(hb, idx); break;
+          }
+        } else {
+          for (int j = 0; j < nh; ++j) word ^= hb[__ldg(&a.chk_hi_h[e0 + j])];
+        }
+        word &= amask;
+      }
+      word = __reduce_or_sync(0xffffffffu, word);
+      if (lane == 0 && (word & ~fl) != 0u) atomicOr(&s_fail[g], word);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < a.G; t += blockDim.x) {
+    const uint32_t w = s_fail[t];
+    if (w != 0u && (w & ~*reinterpret_cast<volatile uint32_t*>(&a.fail[t])) != 0u) atomicOr(&a.fail[t], w);
   }
 }
 
 // --------------------------------------------------------- k_terminate --
-// Warp = one slot.  q^(k) = fixed-order double sum of the tile partials;
-// decision order PCE, then VNR (k >= 2, strict), then d_max
-// (decoder.cpp:114-123).
-__global__ void __launch_bounds__(1024) k_terminate(const Args a) {
-  // block = one group; warp w sums tiles w, w+32, ... for every slot (lane),
-  // coalesced over lanes; warp 0 then adds the 32 warp sums in order.
-  __shared__ double red[32][kLanes];
-  const int g = blockIdx.x;
+// kTermBlocks blocks per group.  q^(k) = fixed-order double sum of the k_var
+// tile partials: block p sums its tile range (warps interleaved, then the 8
+// warp sums in order), the last block of the group to finish adds the block
+// sums in order and takes the decision for every slot of the group: PCE,
+// then VNR (k >= 2, strict), then d_max (decoder.cpp:114-123).  It rewrites
+// stopped[g] / load_mask[g] for k_turnover (no separate clear).
+__global__ void __launch_bounds__(kTermThreads) k_terminate(const Args a) {
+  constexpr int kW = kTermThreads / 32;
+  __shared__ double red[kW][kLanes];
+  __shared__ int s_last;
+  const int g = blockIdx.x / kTermBlocks;
+  const int p = blockIdx.x - g * kTermBlocks;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const uint32_t amask = a.group_active[g];
-  if (amask == 0u) return;
-  double q = 0.0;
-  for (int t = warp; t < a.n_tiles; t += 32) q += a.q_part[(static_cast<size_t>(g) * a.n_tiles + t) * kLanes + lane];
-  red[warp][lane] = q;
-  __syncthreads();
-  if (warp != 0) return;
-  q = red[0][lane];
-#pragma unroll
-  for (int k = 1; k < 32; ++k) q += red[k][lane];
-  const uint32_t bit = 1u << lane;
-  if (!(amask & bit)) return;
-  const int s = g * kLanes + lane;
-  const int it = a.slot_iter[s];
-  const int f = a.slot_frame[s];
-  atomicAdd(a.frame_iters, 1ull);
-  if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (it - 1)] = q;
-  int reason = -1;
-  if (a.use_pce && !(a.fail[g] & bit)) {
-    reason = 0;
-  } else if (a.use_vnr && it >= 2 && q < a.qprev[s]) {
-    reason = 1;
-  } else if (it >= a.d_max) {
-    reason = 2;
-  }
-  if (reason < 0) {
-    a.slot_iter[s] = it + 1;
-    a.qprev[s] = q;
+  if (amask == 0u) {
+    if (p == 0 && threadIdx.x == 0) {
+      a.stopped[g] = 0u;
+      a.load_mask[g] = 0u;
+    }
     return;
   }
-  a.out_iters[f] = it;
-  a.out_reasons[f] = static_cast<uint8_t>(reason);
-  atomicAnd(&a.group_active[g], ~bit);
-  atomicOr(&a.stopped[g], bit);
-  atomicAdd(&a.counters[1], 1);
-  atomicSub(&a.counters[3], 1);
-  const int nf = atomicAdd(&a.counters[0], 1);
-  if (nf < a.batch) {
-    a.pending_frame[s] = nf;
-    atomicOr(&a.load_mask[g], bit);
+  const int t_lo = static_cast<int>(static_cast<long long>(a.n_tiles) * p / kTermBlocks);
+  const int t_hi = static_cast<int>(static_cast<long long>(a.n_tiles) * (p + 1) / kTermBlocks);
+  const double* qp = a.q_part + static_cast<size_t>(g) * a.n_tiles * kLanes + lane;
+  double q = 0.0;
+  for (int t0 = t_lo + warp; t0 < t_hi; t0 += kW * 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = t0 + kW * k;
+      v[k] = t < t_hi ? qp[static_cast<size_t>(t) * kLanes] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (t0 + kW * k < t_hi) q += v[k];
+    }
+  }
+  red[warp][lane] = q;
+  __syncthreads();
+  if (warp == 0) {
+    q = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < kW; ++k) q += red[k][lane];
+    a.q_mid[(static_cast<size_t>(g) * kTermBlocks + p) * kLanes + lane] = q;
+    __threadfence();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&a.term_cnt[g], 1) == kTermBlocks - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last || warp != 0) return;
+  __threadfence();
+  double v[kTermBlocks];
+#pragma unroll
+  for (int k = 0; k < kTermBlocks; ++k) v[k] = __ldcg(&a.q_mid[(static_cast<size_t>(g) * kTermBlocks + k) * kLanes + lane]);
+  q = v[0];
+#pragma unroll
+  for (int k = 1; k < kTermBlocks; ++k) q += v[k];
+  if (lane == 0) {
+    a.term_cnt[g] = 0;
+    atomicAdd(a.frame_iters, static_cast<unsigned long long>(__popc(amask)));
+  }
+  const uint32_t bit = 1u << lane;
+  const bool act = (amask & bit) != 0u;
+  const int s = g * kLanes + lane;
+  int reason = -1, it = 0, f = 0;
+  if (act) {
+    it = a.slot_iter[s];
+    f = a.slot_frame[s];
+    if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (it - 1)] = q;
+    if (a.use_pce && !(a.fail[g] & bit)) {
+      reason = 0;
+    } else if (a.use_vnr && it >= 2 && q < a.qprev[s]) {
+      reason = 1;
+    } else if (it >= a.d_max) {
+      reason = 2;
+    }
+    if (reason < 0) {
+      a.slot_iter[s] = it + 1;
+      a.qprev[s] = q;
+    } else {
+      a.out_iters[f] = it;
+      a.out_reasons[f] = static_cast<uint8_t>(reason);
+      a.stop_frame[s] = f;
+    }
+  }
+  const uint32_t stop = __ballot_sync(0xffffffffu, reason >= 0);
+  const int nstop = __popc(stop);
+  int base = 0;
+  if (lane == 0 && nstop > 0) {
+    a.group_active[g] = amask & ~stop;
+    atomicAdd(&a.counters[1], nstop);
+    atomicSub(&a.counters[3], nstop);
+    base = atomicAdd(&a.counters[0], nstop);
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  // refill: the stopping slots take the next queued frames, in lane order
+  const int nf = base + __popc(stop & ((1u << lane) - 1u));
+  const bool refill = reason >= 0 && nf < a.batch;
+  if (refill) a.pending_frame[s] = nf;
+  const uint32_t load = __ballot_sync(0xffffffffu, refill);
+  if (lane == 0) {
+    a.stopped[g] = stop;
+    a.load_mask[g] = load;
   }
 }
 
-// ----------------------------------------------------------- k_extract --
-// Outputs (hard bits, posteriors) of the frames that stopped this step, in
-// the original variable order.  Thread = one variable; a warp covers 32
-// consecutive variables so packed bit words come from one ballot.
+// ---------------------------------------------------------- k_turnover --
+// Frame turnover after the decision of a step, one launch:
+//  * extract — outputs (hard bits, posteriors) of the frames that stopped
+//    (decoder.cpp:126-128), in the original variable order;
+//  * load — the next queued frames into the freed slots.
+// Item block b owns the chunk quads q = b, b + item_blocks, ... (4 x 32
+// original variables).  Phase A: its warps extract the stopped lanes of
+// those chunks (warp = chunk, lane = variable; the variable map and the
+// bit-sliced hard-decision word serve every stopped lane; packed words come
+// from one ballot).  Barrier.  Phase B: the same rows are overwritten with
+// the new frames' LLRs — 32 frames x 128 variables read row-coalesced,
+// transposed in shared memory, written as one 128-byte [item][32 lanes] row
+// per variable at its device position (vmap); a slot is recycled in the
+// step it frees.  Check blocks: the target syndrome, one 32-check input word
+// per warp bit-transposed with 32 ballots into the device-order words (cdev).
+// One block: slot state.
+constexpr int kTurnChunks = 4;
+
 template <bool WANT_POST>
-__global__ void __launch_bounds__(kThreads) k_extract(const Args a) {
-  {
-    uint32_t any = 0u;
-    for (int g = 0; g < a.G; ++g) any |= a.stopped[g];
-    if (any == 0u) return;  // nothing stopped this step
-  }
-  const int lane = threadIdx.x & 31;
-  const long long npad = (static_cast<long long>(a.N) + 31) / 32 * 32;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+__device__ __forceinline__ void extract_chunk(const Args& a, int ch, int lane) {
+  const int i = ch * 32 + lane;
+  const bool valid = i < a.N;
+  const int vm = valid ? __ldg(&a.vmap[i]) : 0;
   for (int g = 0; g < a.G; ++g) {
     uint32_t sm = a.stopped[g];
+    if (sm == 0u) continue;
+    uint32_t word = 0u;
+    const float* prow = nullptr;  // row of 32 lanes holding this variable's posterior
+    const bool deg0 = valid && vm >= a.NV;
+    if (valid) {
+      if (vm >= 0) {
+        if (vm < a.NV) {
+          word = a.hbits[static_cast<size_t>(g) * a.NV + vm];
+          prow = a.post + (static_cast<size_t>(g) * a.NV + vm) * kLanes;
+        } else {  // degree-0 variable: posterior = channel LLR
+          prow = a.llr_h + (static_cast<size_t>(g) * a.NH + vm) * kLanes;
+        }
+      } else {
+        const int dd = -1 - vm;
+        word = a.d1bits[static_cast<size_t>(g) * a.N1 + dd];
+        if (WANT_POST) prow = a.d1post + (static_cast<size_t>(g) * a.N1 + dd) * kLanes;
+      }
+    }
     while (sm) {
       const int l = __ffs(sm) - 1;
       sm &= sm - 1;
-      const int f = a.slot_frame[g * kLanes + l];
-      for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < npad; i += stride) {
-        uint32_t bit = 0u;
-        float pv = 0.0f;
-        if (i < a.N) {
-          const int vm = __ldg(&a.vmap[i]);
-          if (vm >= 0) {
-            if (vm < a.NV) {
-              bit = (a.hbits[static_cast<size_t>(g) * a.NV + vm] >> l) & 1u;
-              if (WANT_POST) pv = a.post[(static_cast<size_t>(g) * a.NV + vm) * kLanes + l];
-            } else {  // degree-0 variable: posterior = channel LLR
-              pv = a.llr_h[(static_cast<size_t>(g) * a.NH + vm) * kLanes + l];
-              bit = pv < 0.0f ? 1u : 0u;
-            }
-          } else {
-            const int dd = -1 - vm;
-            bit = (a.d1bits[static_cast<size_t>(g) * a.N1 + dd] >> l) & 1u;
-            if (WANT_POST) pv = a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + l];
-          }
-          if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
-          if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
-        }
-        if (a.out_bits_pk) {
-          const uint32_t word = __ballot_sync(0xffffffffu, bit);
-          if (lane == 0) a.out_bits_pk[static_cast<size_t>(f) * a.NW + (i >> 5)] = word;
-        }
+      const int f = a.stop_frame[g * kLanes + l];
+      uint32_t bit = (word >> l) & 1u;
+      float pv = 0.0f;
+      if (deg0) {
+        pv = prow[l];
+        bit = pv < 0.0f ? 1u : 0u;
+      } else if (WANT_POST && valid) {
+        pv = prow[l];
+      }
+      if (valid) {
+        if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
+        if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
+      }
+      if (a.out_bits_pk) {
+        const uint32_t pw = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) a.out_bits_pk[static_cast<size_t>(f) * a.NW + ch] = pw;
       }
     }
   }
 }
 
-// -------------------------------------------------------------- k_load --
-// Streams frames into the slots flagged in load_mask: LLR transpose
-// [frame][var] -> [group][item][lane] through shared memory, target syndrome
-// bits, slot state.  Grid: (item tiles of 32) + (check tiles) + 1 state block.
-__global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks, int check_blocks) {
-  __shared__ float tile[32][33];
-  {
-    uint32_t any = 0u;
-    for (int g = 0; g < a.G; ++g) any |= a.load_mask[g];
-    if (any == 0u) return;  // no slot to (re)fill this step
+template <bool WANT_POST>
+__global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_blocks, int check_blocks) {
+  __shared__ float tile[kTurnChunks][32][33];
+  uint32_t any_stop = 0u, any_load = 0u;
+  for (int g = 0; g < a.G; ++g) {
+    any_stop |= a.stopped[g];
+    any_load |= a.load_mask[g];
   }
+  if ((any_stop | any_load) == 0u) return;  // nothing to hand over this step
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  constexpr int kW = kThreads / 32;
   const int b = blockIdx.x;
   if (b < item_blocks) {
-    const int n_tiles_items = (a.N + 31) / 32;
-    for (long long w = b; w < static_cast<long long>(a.G) * n_tiles_items; w += item_blocks) {
-      const int g = static_cast<int>(w / n_tiles_items);
-      const int it0 = static_cast<int>(w - static_cast<long long>(g) * n_tiles_items) * 32;
-      const uint32_t lm = a.load_mask[g];
-      if (lm == 0u) continue;
-      // read: warp = slot lane r, lanes = consecutive items
-      for (int r = warp; r < 32; r += kThreads / 32) {
-        if (!((lm >> r) & 1u)) continue;
-        const int f = a.pending_frame[g * kLanes + r];
-        const int item = it0 + lane;
-        float v = 0.0f;
-        if (item < a.N) {
-          v = a.in_llr[static_cast<size_t>(f) * a.N + __ldg(&a.dorig[item])];
-          if (!isfinite(v)) atomicOr(&a.counters[2], 1);
-        }
-        tile[lane][r] = v;
+    const int quads = (a.NW + kTurnChunks - 1) / kTurnChunks;
+    if (any_stop) {
+      // phase A: (quad, chunk) pairs of this block dealt over its warps
+      const int per_block = (quads - b + item_blocks - 1) / item_blocks * kTurnChunks;
+      for (int k = warp; k < per_block; k += kW) {
+        const int ch = (b + (k / kTurnChunks) * item_blocks) * kTurnChunks + (k % kTurnChunks);
+        if (ch < a.NW) extract_chunk<WANT_POST>(a, ch, lane);
       }
-      __syncthreads();
-      for (int j = warp; j < 32; j += kThreads / 32) {
-        const int item = it0 + j;
-        if (item < a.N && ((lm >> lane) & 1u)) {
-          const float v = tile[j][lane];
-          if (item < a.NH) {
-            a.llr_h[(static_cast<size_t>(g) * a.NH + item) * kLanes + lane] = v;
-            // posterior state starts at the channel LLR (v2c of iteration 1)
-            if (item < a.NV) a.post[(static_cast<size_t>(g) * a.NV + item) * kLanes + lane] = v;
-          } else {
-            a.llr_d[(static_cast<size_t>(g) * a.N1 + (item - a.NH)) * kLanes + lane] = v;
+      if (!any_load) return;
+      __syncthreads();  // outputs read before the rows are refilled
+    }
+    for (int qd = b; qd < quads; qd += item_blocks) {
+      const int ch0 = qd * kTurnChunks;
+      for (int g = 0; g < a.G; ++g) {
+        const uint32_t lm = a.load_mask[g];
+        if (lm == 0u) continue;  // block-uniform
+        // read: warp = slot lanes r = warp + 8m, lanes = consecutive original
+        // variables; all 4 x 4 loads in flight before any use
+        constexpr int kRpw = 32 / kW;
+        float v[kTurnChunks][kRpw];
+#pragma unroll
+        for (int m = 0; m < kRpw; ++m) {
+          const int r = warp + kW * m;
+          const bool on = (lm >> r) & 1u;
+          const int f = on ? a.pending_frame[g * kLanes + r] : 0;
+          const float* src = a.in_llr + static_cast<size_t>(f) * a.N;
+#pragma unroll
+          for (int c = 0; c < kTurnChunks; ++c) {
+            const int i = (ch0 + c) * 32 + lane;
+            v[c][m] = (on && i < a.N) ? src[i] : 0.0f;
           }
         }
+        bool bad = false;
+#pragma unroll
+        for (int m = 0; m < kRpw; ++m) {
+#pragma unroll
+          for (int c = 0; c < kTurnChunks; ++c) {
+            bad |= !isfinite(v[c][m]);
+            tile[c][warp + kW * m][lane] = v[c][m];
+          }
+        }
+        if (bad) atomicOr(&a.counters[2], 1);
+        __syncthreads();
+        // write: warp = variable j, lanes = slots (one 128-byte row)
+        for (int jj = warp; jj < 32 * kTurnChunks; jj += kW) {
+          const int i = ch0 * 32 + jj;
+          if (i < a.N && ((lm >> lane) & 1u)) {
+            const float v = tile[jj >> 5][lane][jj & 31];
+            const int vj = __ldg(&a.vmap[i]);
+            if (vj >= 0) {
+              a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + lane] = v;
+              // posterior state starts at the channel LLR (v2c of iteration 1)
+              if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + lane] = v;
+            } else {
+              a.llr_d[(static_cast<size_t>(g) * a.N1 + (-1 - vj)) * kLanes + lane] = v;
+            }
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   } else if (b < item_blocks + check_blocks) {
-    const long long total = static_cast<long long>(a.G) * a.M;
-    const long long stride = static_cast<long long>(check_blocks) * blockDim.x;
-    for (long long w = static_cast<long long>(b - item_blocks) * blockDim.x + threadIdx.x; w < total; w += stride) {
-      const int g = static_cast<int>(w / a.M);
-      const int c = static_cast<int>(w - static_cast<long long>(g) * a.M);
-      uint32_t lm = a.load_mask[g];
-      if (lm == 0u) continue;
-      uint32_t word = a.syn_target[w] & ~lm;
-      if (a.in_syn) {
-        const int co = __ldg(&a.corig[c]);  // syndrome input is in original check order
-        while (lm) {
-          const int r = __ffs(lm) - 1;
-          lm &= lm - 1;
-          const int f = a.pending_frame[g * kLanes + r];
-          word |= ((__ldg(&a.in_syn[static_cast<size_t>(f) * a.MW + (co >> 5)]) >> (co & 31)) & 1u) << r;
+    if (any_load == 0u) return;
+    if (a.in_syn) {
+      const int nw = check_blocks * kW;
+      for (long long w = static_cast<long long>(b - item_blocks) * kW + warp; w < static_cast<long long>(a.G) * a.MW;
+           w += nw) {
+        const int g = static_cast<int>(w / a.MW);
+        const int wi = static_cast<int>(w - static_cast<long long>(g) * a.MW);
+        const uint32_t lm = a.load_mask[g];
+        if (lm == 0u) continue;
+        uint32_t mine = 0u;  // lane r: input word wi of the frame entering slot r
+        if ((lm >> lane) & 1u) {
+          const int f = a.pending_frame[g * kLanes + lane];
+          mine = __ldg(&a.in_syn[static_cast<size_t>(f) * a.MW + wi]);
+        }
+        uint32_t col = 0u;  // lane k: check wi*32+k over the 32 slots
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t t = __ballot_sync(0xffffffffu, (mine >> k) & 1u);
+          if (lane == k) col = t;
+        }
+        const int c = wi * 32 + lane;
+        if (c < a.M) {
+          const size_t idx = static_cast<size_t>(g) * a.M + __ldg(&a.cdev[c]);
+          a.syn_target[idx] = (a.syn_target[idx] & ~lm) | (col & lm);
         }
       }
-      a.syn_target[w] = word;
+    } else {
+      const long long total = static_cast<long long>(a.G) * a.M;
+      const long long stride = static_cast<long long>(check_blocks) * blockDim.x;
+      for (long long w = static_cast<long long>(b - item_blocks) * blockDim.x + threadIdx.x; w < total; w += stride) {
+        const uint32_t lm = a.load_mask[static_cast<int>(w / a.M)];
+        if (lm != 0u) a.syn_target[w] &= ~lm;
+      }
     }
   } else {
+    if (any_load == 0u) return;
     for (int s = threadIdx.x; s < a.G * kLanes; s += blockDim.x) {
       const int g = s >> 5;
       const uint32_t bit = 1u << (s & 31);
@@ -1039,21 +1205,13 @@ __global__ void __launch_bounds__(kThreads) k_load(const Args a, int item_blocks
   }
 }
 
-// Clears the per-step masks consumed by k_extract / k_load.
-__global__ void k_step_end(const Args a) {
-  for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
-    a.stopped[g] = 0u;
-    a.load_mask[g] = 0u;
-  }
-}
-
 // ---------------------------------------------------------- compaction --
 // When no frames are left to stream in, frames that are still iterating are
 // packed into as few 32-slot groups as possible, so the tail of a batch (a
 // few slow frames spread over many groups) stops paying full-warp compute in
 // every group.  The plan is a pure function of group_active, computed
-// redundantly by every block; k_compact_move copies the per-slot rows,
-// k_compact_commit then moves the slot state and rewrites group_active.
+// redundantly by every block; k_compact copies the per-slot rows and its
+// last block moves the slot state and rewrites group_active.
 constexpr int kMaxCompactGroups = 256;
 constexpr int kMaxMoves = 1024;
 
@@ -1113,62 +1271,87 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_compact_move(const Args a) {
+// One launch: every block computes the (identical) plan, moves its share of
+// rows — warp = one row, lane = one move, so a row moves as one 128-byte
+// read and write — and the last block to finish commits the slot state
+// (counters[5] counts finished blocks).
+__global__ void __launch_bounds__(kThreads) k_compact(const Args a) {
   __shared__ CompactPlan pl;
   __shared__ int cnt[kMaxCompactGroups];
+  __shared__ int s_last;
   if (threadIdx.x == 0) compact_plan(a, pl, cnt);
   __syncthreads();
   const int n = pl.n;
-  if (n == 0) return;
+  if (n == 0) return;  // same decision in every block
+  const int lane = threadIdx.x & 31;
   const long long rows_e = a.EH, rows_v = a.NV, rows_h = a.NH, rows_d = a.N1;
   const bool post_d = a.d1post != nullptr;
-  const long long total = rows_e + rows_v + rows_h + rows_d * (post_d ? 2 : 1) + a.M;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
-    long long r = t;
-    float* arr;
-    long long R;
-    if (r < rows_e) { arr = a.c2v; R = rows_e; }
-    else if ((r -= rows_e) < rows_v) { arr = a.post; R = rows_v; }
-    else if ((r -= rows_v) < rows_h) { arr = a.llr_h; R = rows_h; }
-    else if ((r -= rows_h) < rows_d) { arr = a.llr_d; R = rows_d; }
-    else if (post_d && (r -= rows_d) < rows_d) { arr = a.d1post; R = rows_d; }
-    else {
-      // syndrome target bits of check cc (one thread does every move into a word)
-      const int cc = static_cast<int>(r - rows_d);
-      for (int k = 0; k < n; ++k) {
-        const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
-        const uint32_t bit = (a.syn_target[static_cast<size_t>(gs) * a.M + cc] >> ls) & 1u;
-        uint32_t& w = a.syn_target[static_cast<size_t>(gd) * a.M + cc];
-        w = (w & ~(1u << ld)) | (bit << ld);
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  // per array: warp = 8 rows per pass, lane = one move; sources and
+  // targets are disjoint groups, so all 8 reads are issued before the writes
+  constexpr int kRowsPer = 8;
+  const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  float* arrs[5] = {a.c2v, a.post, a.llr_h, a.llr_d, a.d1post};
+  const long long rows[5] = {rows_e, rows_v, rows_h, rows_d, post_d ? rows_d : 0};
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    const int k = k0 + lane;
+    const bool mv = k < n;
+    const int gs = mv ? pl.src[k] >> 5 : 0, ls = mv ? pl.src[k] & 31 : 0;
+    const int gd = mv ? pl.dst[k] >> 5 : 0, ld = mv ? pl.dst[k] & 31 : 0;
+    for (int q = 0; q < 5; ++q) {
+      const long long R = rows[q];
+      if (R == 0) continue;
+      const float* src = arrs[q] + static_cast<size_t>(gs) * R * kLanes + ls;
+      float* dst = arrs[q] + static_cast<size_t>(gd) * R * kLanes + ld;
+      for (long long base = warp0 * kRowsPer; base < R; base += nwarps * kRowsPer) {
+        float v[kRowsPer];
+#pragma unroll
+        for (int j = 0; j < kRowsPer; ++j) v[j] = (mv && base + j < R) ? src[(base + j) * kLanes] : 0.0f;
+#pragma unroll
+        for (int j = 0; j < kRowsPer; ++j)
+          if (mv && base + j < R) dst[(base + j) * kLanes] = v[j];
       }
-      continue;
-    }
-    for (int k = 0; k < n; ++k) {
-      const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
-      arr[(static_cast<size_t>(gd) * R + r) * kLanes + ld] = arr[(static_cast<size_t>(gs) * R + r) * kLanes + ls];
     }
   }
-}
-
-__global__ void k_compact_commit(const Args a) {
-  __shared__ CompactPlan pl;
-  __shared__ int cnt[kMaxCompactGroups];
-  if (threadIdx.x == 0) {
-    compact_plan(a, pl, cnt);
-    if (pl.n > 0) {
-      int total = 0;
-      for (int g = 0; g < a.G; ++g) total += cnt[g];
-      a.counters[4] = total;
+  // syndrome target bits: thread = one check; moves are ordered by source
+  // and by target group, so each source word is read once and each target
+  // word is read and written once
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long cc = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; cc < a.M; cc += stride) {
+    int cur_s = -1, cur_d = -1;
+    uint32_t ws = 0u, wd = 0u;
+    for (int k = 0; k < n; ++k) {
+      const int gs = pl.src[k] >> 5, ls = pl.src[k] & 31, gd = pl.dst[k] >> 5, ld = pl.dst[k] & 31;
+      if (gs != cur_s) {
+        cur_s = gs;
+        ws = a.syn_target[static_cast<size_t>(gs) * a.M + cc];
+      }
+      if (gd != cur_d) {
+        if (cur_d >= 0) a.syn_target[static_cast<size_t>(cur_d) * a.M + cc] = wd;
+        cur_d = gd;
+        wd = a.syn_target[static_cast<size_t>(gd) * a.M + cc];
+      }
+      wd = (wd & ~(1u << ld)) | (((ws >> ls) & 1u) << ld);
     }
-    for (int k = 0; k < pl.n; ++k) {
-      const int s = pl.src[k], d = pl.dst[k];
-      a.slot_iter[d] = a.slot_iter[s];
-      a.slot_frame[d] = a.slot_frame[s];
-      a.qprev[d] = a.qprev[s];
-      a.group_active[s >> 5] &= ~(1u << (s & 31));
-      a.group_active[d >> 5] |= 1u << (d & 31);
-    }
+    if (cur_d >= 0) a.syn_target[static_cast<size_t>(cur_d) * a.M + cc] = wd;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[5], 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  a.counters[5] = 0;
+  int total = 0;
+  for (int g = 0; g < a.G; ++g) total += cnt[g];
+  a.counters[4] = total;
+  for (int k = 0; k < n; ++k) {
+    const int s = pl.src[k], d = pl.dst[k];
+    a.slot_iter[d] = a.slot_iter[s];
+    a.slot_frame[d] = a.slot_frame[s];
+    a.qprev[d] = a.qprev[s];
+    a.group_active[s >> 5] &= ~(1u << (s & 31));
+    a.group_active[d >> 5] |= 1u << (d & 31);
   }
 }
 
@@ -1292,6 +1475,7 @@ class GpuDecoder {
   template <typename F>
   void launch(int kid, cudaStream_t st, F&& f);
   void run_step(const Args& a, cudaStream_t st, bool want_post);
+  void launch_turnover(const Args& a, cudaStream_t st, bool want_post);
 
   Args base{};
   int32_t max_check_deg = 0;
@@ -1305,8 +1489,8 @@ class GpuDecoder {
   std::vector<cudaEvent_t> prof_ev;
   std::vector<int> prof_kid;
   Scratch s_llr, s_syn, s_bits, s_iters, s_reasons, s_post, s_qtrace;
-  int grid_check = 0, grid_var = 0, grid_syn = 0, grid_extract = 0, sms_ = 148;
-  int load_item_blocks = 0, load_check_blocks = 0;
+  int grid_check = 0, grid_var = 0, grid_syn = 0, sms_ = 148;
+  int turn_item_blocks = 0, turn_check_blocks = 0;
 };
 
 GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
@@ -1447,8 +1631,9 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.vptr = up(vptr, static_cast<int32_t*>(nullptr));
   a.vedge = up(vedge, static_cast<int32_t*>(nullptr));
   a.vmap = up(vmap, static_cast<int32_t*>(nullptr));
-  a.dorig = up(dorig, static_cast<int32_t*>(nullptr));
-  a.corig = up(corig, static_cast<int32_t*>(nullptr));
+  std::vector<int32_t> cdev(M);
+  for (int32_t cd = 0; cd < M; ++cd) cdev[corig[cd]] = cd;
+  a.cdev = up(cdev, static_cast<int32_t*>(nullptr));
   a.ctype = up(ctype, static_cast<int4*>(nullptr));
   a.vtype = up(vtype, static_cast<int32_t*>(nullptr));
   d_check_ptr = up(code.check_ptr, static_cast<int32_t*>(nullptr));
@@ -1469,6 +1654,10 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.synp = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
   a.syn_target = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
   a.q_part = own(dalloc<double>(static_cast<size_t>(G) * a.n_tiles * L, &dev_bytes));
+  a.q_mid = own(dalloc<double>(static_cast<size_t>(G) * kTermBlocks * L, &dev_bytes));
+  a.term_cnt = own(dalloc<int32_t>(G, &dev_bytes));
+  a.stop_frame = own(dalloc<int32_t>(S, &dev_bytes));
+  CUDA_OK(cudaMemset(a.term_cnt, 0, G * sizeof(int32_t)));
   a.qprev = own(dalloc<double>(S, &dev_bytes));
   a.slot_iter = own(dalloc<int32_t>(S, &dev_bytes));
   a.slot_frame = own(dalloc<int32_t>(S, &dev_bytes));
@@ -1494,9 +1683,8 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   grid_var = sms * 16;
   grid_syn = sms * 8;
   // load / extract are no-ops on most steps: keep their grids small
-  grid_extract = sms * 4;
-  load_item_blocks = sms * 4;
-  load_check_blocks = sms * 2;
+  turn_item_blocks = sms * 8;
+  turn_check_blocks = sms * 2;
 }
 
 GpuDecoder::~GpuDecoder() {
@@ -1531,6 +1719,14 @@ void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
   }
 }
 
+void GpuDecoder::launch_turnover(const Args& a, cudaStream_t st, bool want_post) {
+  const int grid = turn_item_blocks + turn_check_blocks + 1;
+  if (want_post)
+    k_turnover<true><<<grid, kThreads, 0, st>>>(a, turn_item_blocks, turn_check_blocks);
+  else
+    k_turnover<false><<<grid, kThreads, 0, st>>>(a, turn_item_blocks, turn_check_blocks);
+}
+
 void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
   const int md = max_check_deg;
   launch(kCheck, st, [&] {
@@ -1556,27 +1752,13 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
     else
       k_var<1><<<grid_var, kVarWarps * 32, 0, st>>>(a);
   });
-  if (a.use_pce) launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 0, st>>>(a); });
-  launch(kTerm, st, [&] { k_terminate<<<G, 1024, 0, st>>>(a); });
-  launch(kExtract, st, [&] {
-    if (want_post)
-      k_extract<true><<<grid_extract, kThreads, 0, st>>>(a);
-    else
-      k_extract<false><<<grid_extract, kThreads, 0, st>>>(a);
-  });
-  launch(kLoad, st, [&] {
-    k_load<<<load_item_blocks + load_check_blocks + 1, kThreads, 0, st>>>(a, load_item_blocks, load_check_blocks);
-  });
-  k_step_end<<<1, 32, 0, st>>>(a);
+  if (a.use_pce)
+    launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, G * sizeof(uint32_t), st>>>(a); });
+  launch(kTerm, st, [&] { k_terminate<<<G * kTermBlocks, kTermThreads, 0, st>>>(a); });
+  launch(kTurnover, st, [&] { launch_turnover(a, st, want_post); });
   // tail compaction (no-op unless the queue is drained and live frames fit
   // in fewer groups; decided on the device, no host round trip)
-  if (G > 1 && G <= kMaxCompactGroups) {
-    k_compact_move<<<sms_, kThreads, 0, st>>>(a);
-    k_compact_commit<<<1, 32, 0, st>>>(a);
-    launches += 2;
-  }
-  CUDA_OK(cudaGetLastError());
-  ++launches;
+  if (G > 1 && G <= kMaxCompactGroups) launch(kCompact, st, [&] { k_compact<<<sms_ * 4, kThreads, 0, st>>>(a); });
 }
 
 void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t st_in) {
@@ -1648,7 +1830,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       pend[s] = s;
       lm[s >> 5] |= 1u << (s & 31);
     }
-    int32_t ctr[8] = {first, 0, 0, 0, G * kLanes + 32, 0, 0, 0};  // active slots counted by k_load
+    int32_t ctr[8] = {first, 0, 0, 0, G * kLanes + 32, 0, 0, 0};  // active slots counted by k_turnover
     CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));
@@ -1658,12 +1840,8 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
     // the host vectors die at scope end: make the copies complete first
     CUDA_OK(cudaStreamSynchronize(st));
   }
-  launch(kLoad, st, [&] {
-    k_load<<<load_item_blocks + load_check_blocks + 1, kThreads, 0, st>>>(a, load_item_blocks, load_check_blocks);
-  });
-  k_step_end<<<1, 32, 0, st>>>(a);
-  CUDA_OK(cudaGetLastError());
-  ++launches;
+  launch(kTurnover, st, [&] { launch_turnover(a, st, false); });
+  CUDA_OK(cudaMemsetAsync(a.load_mask, 0, G * sizeof(uint32_t), st));
 
   // step loop: poll the frames-done counter with a lag so the GPU never idles
   const int64_t waves = (static_cast<int64_t>(B) + S - 1) / S;

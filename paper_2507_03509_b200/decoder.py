@@ -384,7 +384,7 @@ class BatchDecoder:
             _ptr(x_packed_dev), st))
 
     # profiling (CUDA events on the launching stream)
-    KERNELS = ("check", "variable", "syndrome", "terminate", "load", "extract")
+    KERNELS = ("check", "variable", "syndrome", "terminate", "turnover", "compact")
 
     def set_profiling(self, enable: bool):
         _check(self._lib.bpdec_decoder_set_profiling(self._h, int(enable)))

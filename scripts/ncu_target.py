@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Short, deterministic decode used as the ncu capture target: config-2 code,
-64 device-generated frames, PCE-ET, D_max=6 (every frame runs 6 iterations)."""
+64 device-generated frames, PCE-ET, D_max=6 (every frame runs 6 iterations).
+Third argument "vnr": the bench decode instead (VNR+PCE, the workload's D_max)."""
 import os
 import sys
 
@@ -22,7 +23,10 @@ dec.sample_frames_device(P.snr_for_beta(0.95, code.rate()), P.FRAME_SEED, 0, fra
 out = {"iterations": torch.zeros(frames, dtype=torch.int32, device="cuda"),
        "reasons": torch.zeros(frames, dtype=torch.uint8, device="cuda"),
        "bits": torch.zeros((frames, (N + 31) // 32), dtype=torch.int32, device="cuda")}
-r = dec.decode_batch(d_llr, P.DecodeConfig(d_max=6, use_pce=True, use_vnr=False, q_mode=Q_ABS), syndrome=d_syn,
+mode = sys.argv[3] if len(sys.argv) > 3 else "pce6"
+cfg = (P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS) if mode == "vnr"
+       else P.DecodeConfig(d_max=6, use_pce=True, use_vnr=False, q_mode=Q_ABS))
+r = dec.decode_batch(d_llr, cfg, syndrome=d_syn,
                      packed=True, out=out)
 torch.cuda.synchronize()
 print("iterations", int(out["iterations"].sum().item()), "launches", dec.launch_count())
