@@ -12,7 +12,7 @@ OBJDIR   := build/obj
 
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -I$(CSRC) -Iinclude -I/usr/local/cuda/include
 NVFLAGS  := -O3 -std=c++20 $(ARCH) -lineinfo -Xcompiler -fPIC,-Wall -I$(CSRC) -Iinclude \
-            -Xptxas -v
+            -Xptxas -v $(NVFLAGS_EXTRA)
 
 HOST_SRC := $(CSRC)/code.cpp $(CSRC)/c_api.cpp
 HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))

@@ -57,8 +57,7 @@ namespace {
 
 constexpr int kLanes = 32;
 constexpr int kVarWarps = 4;    // warps per k_var block
-constexpr int kVarChunks = 1;   // consecutive 32-variable chunks per warp and tile
-constexpr int kQTile = kVarWarps * kVarChunks * 32;  // variables per q partial sum (code-fixed order)
+constexpr int kQTile = 64;     // variables per k_var tile and q partial sum (code-fixed order)
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
 enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompact = 5, kNumKernels = 6 };
@@ -78,7 +77,10 @@ struct Args {
   const int32_t* cdev;      // [M] original check -> device check
   const int4* ctype;        // [ceil(M/32)] {type NH*8+ND (homogeneous full chunk) or -1,
                             //  first hi edge, first degree-1 row, hi edge end}
-  const int32_t* vtype;     // [ceil(NV/32)] chunk degree (homogeneous, full) or -1
+  const int2* vtile;        // [n_tiles] {tile degree D (typed path) or -1 (generic), first slot in vedge_t}
+  const int32_t* vedge_t;   // tile-padded CSC: per typed tile 64 x D edge ids, -1 = padding
+  const int32_t* vsched;    // [n_tiles] k_var hand-out order: generic tiles first, then by degree
+  const int32_t* csched;    // [ceil(M/32)] k_check hand-out order: generic chunks first
   // state
   int32_t G;
   float* llr_h;             // [G][NH][32]
@@ -87,6 +89,7 @@ struct Args {
   float* c2v;               // [G][EH][32]
   float* d1post;            // [G][N1][32] (only when posteriors are requested)
   uint32_t* hbits;          // [G][NV]
+  uint32_t* ebits;          // [G][EH] hard-decision word of each degree>=2 edge's variable (check-major)
   uint32_t* d1bits;         // [G][N1]
   uint32_t* synp;           // [G][M]  target syndrome ^ degree-1 parity
   uint32_t* syn_target;     // [G][M]
@@ -103,7 +106,8 @@ struct Args {
   uint32_t* stopped;        // [G]
   uint32_t* load_mask;      // [G]
   int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots,
-                            // [4] active slots at the last compaction
+                            // [4] active slots at the last compaction, [5] k_compact blocks done,
+                            // [6] k_var tiles handed out, [7] k_check chunks handed out
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -168,6 +172,40 @@ __device__ __forceinline__ long long skip_group(long long w, long long per_group
   const long long next = (w / per_group + 1) * per_group;
   const long long k = (next - w + stride - 1) / stride;
   return w + k * stride;
+}
+
+// ------------------------------------------------------- work schedulers --
+// k_check and k_var hand out work dynamically: a warp grabs the next index k
+// from counters[ctr] (k_check resets k_var's counter and vice versa) and k
+// maps to item sched[k % per_group] of the (k / per_group)-th group that
+// has active slots.  The schedules put latency-bound generic items first so
+// they overlap the streamed bulk instead of forming the tail.  The grab is
+// split so the atomic can be issued one item ahead of its use.
+__device__ __forceinline__ int sched_issue(const Args& a, int ctr, int lane) {
+  int k = 0;
+  if (lane == 0) k = atomicAdd(&a.counters[ctr], 1);
+  return k;  // valid in lane 0 only
+}
+
+__device__ __forceinline__ long long sched_resolve(const Args& a, int k, int lane, int per_group,
+                                                   const int32_t* __restrict__ sched) {
+  k = __shfl_sync(0xffffffffu, k, 0);
+  const long long total = static_cast<long long>(a.G) * per_group;
+  int gi = k / per_group;
+  if (gi >= a.G) return total;
+  const int t = __ldg(&sched[k - gi * per_group]);
+  for (int g0 = 0; g0 < a.G; g0 += 32) {
+    const int g = g0 + lane;
+    const uint32_t live = __ballot_sync(0xffffffffu, g < a.G && a.group_active[g] != 0u);
+    const int n = __popc(live);
+    if (gi < n) {
+      uint32_t m = live;
+      for (int i = 0; i < gi; ++i) m &= m - 1;
+      return static_cast<long long>(g0 + __ffs(m) - 1) * per_group + t;
+    }
+    gi -= n;
+  }
+  return total;
 }
 
 // ------------------------------------------------------------- k_check --
@@ -239,21 +277,23 @@ __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&ou
     out[0] = fminf(m[1], clamp);
     out[1] = fminf(m[D > 1 ? 0 : 0], clamp);
   } else {
+    // prefix / suffix sums without the additions of 0 (phi >= 0, so the
+    // results are bit-identical to starting both sums at 0)
     float ph[D];
     float pre[D];
-    float run = 0.0f;
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      ph[j] = dev::phi(m[j]);
-      pre[j] = run;
-      run += ph[j];
-    }
-    float suf = 0.0f;
+    for (int j = 0; j < D; ++j) ph[j] = dev::phi(m[j]);
+    pre[1] = ph[0];
 #pragma unroll
-    for (int j = D - 1; j >= 0; --j) {
+    for (int j = 2; j < D; ++j) pre[j] = pre[j - 1] + ph[j - 1];
+    out[D - 1] = fminf(dev::phi(pre[D - 1]), clamp);
+    float suf = ph[D - 1];
+#pragma unroll
+    for (int j = D - 2; j >= 1; --j) {
       out[j] = fminf(dev::phi(pre[j] + suf), clamp);
       suf += ph[j];
     }
+    out[0] = fminf(dev::phi(suf), clamp);
   }
 }
 
@@ -529,23 +569,22 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
   __shared__ uint32_t s_syn[kCheckThreads / 32][32];
   __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
   __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRingRows * kLanes];
-  if (blockIdx.x == 0)
+  if (blockIdx.x == 0) {
     for (int t = threadIdx.x; t < a.G; t += blockDim.x) a.fail[t] = 0u;
+    if (threadIdx.x == 0) a.counters[6] = 0;  // k_var tile scheduler (this step)
+  }
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
-  const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const int chunks = (a.M + 31) / 32;
   const long long total = static_cast<long long>(a.G) * chunks;
-  for (long long w = warp0; w < total;) {
+  // dynamic chunk schedule (counters[7], generic chunks first), one grab ahead
+  long long w = sched_resolve(a, sched_issue(a, 7, lane), lane, chunks, a.csched);
+  while (w < total) {
+    const int kpend = sched_issue(a, 7, lane);
     const int g = static_cast<int>(w / chunks);
     const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
     const int c0 = ch * 32;
     const uint32_t amask = a.group_active[g];
-    if (amask == 0u) {
-      w = skip_group(w, chunks, nwarps);
-      continue;
-    }
     const int nc = min(32, a.M - c0);
     const bool act = (amask >> lane) & 1u;
     const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
@@ -555,7 +594,7 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
     const int type = kStage ? cdk.x : -1;
     // degree-1 checks only change in a frame's first iteration
     if ((type == 1 || type == 8) && fmask == 0u) {
-      w += nwarps;
+      w = sched_resolve(a, kpend, lane, chunks, a.csched);
       continue;
     }
     __syncwarp();
@@ -618,25 +657,27 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
       }
     }
     if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = synw;
-    w += nwarps;
+    w = sched_resolve(a, kpend, lane, chunks, a.csched);
   }
 }
 
 // --------------------------------------------------------------- k_var --
-// One warp = 32 consecutive (device-order) degree>=2 variables x 32 slots.
-// Variables are sorted by degree in the device layout, so a chunk is almost
-// always homogeneous: its CSC slice (edge ids of its c2v rows) is staged in
-// shared memory and the typed path gathers K variables' messages at once
-// before the (ordered) sums.  A block covers kQTile = 128 variables and the
-// tile's q partial is the warp partials summed in warp order — a summation
-// order fixed by the code (not by slots, batch size or GPU count).
-constexpr int kVarStage = 32 * 24;  // staged edge ids per warp
-
-// Typed chunk of 32 degree-D variables: K variables per batch of K*(D+1)
-// rows (channel LLR + D messages), copied with cp.async into the per-warp
-// two-stage ring while the previous batch is summed from shared memory.
-constexpr int kVarRingRows = 48;  // per-warp ring of the variable kernel (rows of 128 B)
-constexpr int kVarStageRows = 12;  // rows per batch stage of the variable kernel
+// A warp owns tiles of kQTile = 64 consecutive (device-order) degree>=2
+// variables x 32 slots (tiles w, w + warps, ...).  Variables are sorted by
+// degree, so almost every tile is homogeneous (degree D): the warp then runs
+// ONE continuous cp.async pipeline over the batches of all its consecutive
+// degree-D tiles — the CSC slice (edge ids) of the next tile is prefetched
+// into the second half of a double buffer while the current tile is summed,
+// and the first batches of the next tile are issued while the current one
+// drains, so the random c2v row gathers stay in flight across tile
+// boundaries.  Per variable: post = llr + sum of c2v in ascending original
+// check order (decoder.cpp:99-105), the hard-decision word (ballot over the
+// 32 slots) to hbits and to every edge of the variable (ebits, the
+// check-major copy the syndrome kernel streams).  The tile's q partial is
+// chunk0 + chunk1, each summed in variable order — an order fixed by the code
+// (not by slots, batch size or GPU count).
+constexpr int kVarRingRows = 40;   // per-warp ring of the variable kernel (rows of 128 B)
+constexpr int kVarStageRows = 12;  // rows per batch of the variable kernel
 
 template <int D>
 struct VarShape {
@@ -645,71 +686,209 @@ struct VarShape {
       kVarStageRows / RPV >= 8 ? 8 : (kVarStageRows / RPV >= 4 ? 4 : (kVarStageRows / RPV >= 2 ? 2 : 1));
   static constexpr int ROWS = K * RPV;  // rows per batch
   static constexpr int NS = kVarRingRows / ROWS >= 6 ? 6 : kVarRingRows / ROWS;  // ring stages
-  static_assert(NS >= 1, "variable degree too large for the ring");
+  static_assert(NS >= 2, "variable degree too large for the ring");
+  static_assert(D <= 16, "chunk edge ids must fit the stage buffer");
 };
 
-// Stage layout for a batch of K variables: [K llr rows][K*D c2v rows].
+// Batch b of a chunk: K variables; stage layout [K llr rows][K*D c2v rows].
+// Edge id -1 pads a variable of lower degree to the tile degree D, and
+// variables at or beyond `nval` pad the last tile: their copies are
+// predicated off, which zero-fills the stage rows (+0.0 leaves the ordered
+// sum unchanged).
 template <int D>
-__device__ __forceinline__ void var_batch_issue(float* stage, const float* llr0, const float* c2v0, const int32_t* ve,
-                                                int i0, int lrow, int lcol, bool qact, uint64_t pol) {
+__device__ __forceinline__ void var_batch_issue(float* stage, const float* llr0, const float* c2vg, const int32_t* ve,
+                                                int i0, int nval, int lrow, int lcol, bool qact, uint64_t pol) {
   constexpr int K = VarShape<D>::K;
 #pragma unroll
   for (int r0 = 0; r0 < K; r0 += 4) {
     const int r = r0 + lrow;
-    if (r < K) cp_async16_ef(stage + r * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol, qact, pol);
+    if (r < K)
+      cp_async16_ef(stage + r * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol,
+                    qact && i0 + r < nval, pol);
   }
 #pragma unroll
   for (int r0 = 0; r0 < K * D; r0 += 4) {
     const int r = r0 + lrow;
-    if (r < K * D)
-      cp_async16_ef(stage + (K + r) * kLanes + lcol, c2v0 + static_cast<size_t>(ve[i0 * D + r]) * kLanes + lcol, qact,
-                    pol);
+    if (r < K * D) {
+      const int e = ve[i0 * D + r];
+      cp_async16_ef(stage + (K + r) * kLanes + lcol, c2vg + static_cast<size_t>(e < 0 ? 0 : e) * kLanes + lcol,
+                    qact && e >= 0, pol);
+    }
   }
-  cp_async_commit();
 }
 
 template <int D, int QMODE>
-__device__ __forceinline__ void var_batch_compute(const float* stage, float* postg, int i0, int lane, bool act,
-                                                  double* acc, uint32_t* hw) {
+__device__ __forceinline__ void var_batch_compute(const float* stage, float* postg, uint32_t* ebg, const int32_t* ve,
+                                                  int i0, int nval, int lane, bool act, double& acc, uint32_t& hw) {
   constexpr int K = VarShape<D>::K;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
+    const bool on = act && i0 + k < nval;
     float p = stage[k * kLanes];
 #pragma unroll
     for (int j = 0; j < D; ++j) p += stage[(K + k * D + j) * kLanes];  // ascending check order (decoder.cpp:101)
-    st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, act);
-    if (act) *acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
-    const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
-    if (lane == i0 + k) *hw = word;
+    st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, on);
+    if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+    const uint32_t word = __ballot_sync(0xffffffffu, on && p < 0.0f);
+    if (lane == ((i0 + k) & 31)) hw = word;
+    if (lane < D) {
+      const int e = ve[(i0 + k) * D + lane];
+      if (e >= 0) ebg[e] = word;
+    }
   }
 }
 
+struct VarTile {
+  int g, tile, h0, kb;
+};
+
+__device__ __forceinline__ VarTile var_tile(const Args& a, long long w, int kb) {
+  VarTile t;
+  t.g = static_cast<int>(w / a.n_tiles);
+  t.tile = static_cast<int>(w - static_cast<long long>(t.g) * a.n_tiles);
+  t.h0 = t.tile * kQTile;
+  t.kb = kb;
+  return t;
+}
+__device__ __forceinline__ VarTile var_tile(const Args& a, long long w) {
+  return var_tile(a, w, __ldg(&a.vtile[static_cast<int>(w % a.n_tiles)]).y);
+}
+
+// k_var tiles: counters[6], schedule vsched (generic tiles first).
+__device__ __forceinline__ int var_grab_issue(const Args& a, int lane) { return sched_issue(a, 6, lane); }
+__device__ __forceinline__ long long var_grab_resolve(const Args& a, int k, int lane) {
+  return sched_resolve(a, k, lane, a.n_tiles, a.vsched);
+}
+__device__ __forceinline__ long long var_grab(const Args& a, int lane) {
+  return var_grab_resolve(a, var_grab_issue(a, lane), lane);
+}
+
+// Stages one chunk's edge ids (32*D contiguous ints from kb) with 16-byte
+// cp.async (4-byte copies when kb is not 16-byte aligned).
+template <int D>
+__device__ __forceinline__ void var_stage_ve(int32_t* dst, const int32_t* vedge, int kb, int lane) {
+  constexpr int n = 32 * D;
+  if ((kb & 3) == 0) {
+#pragma unroll
+    for (int i = lane * 4; i < n; i += 128)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst + i)), "l"(vedge + kb + i)
+                   : "memory");
+  } else {
+    for (int i = lane; i < n; i += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst + i)), "l"(vedge + kb + i)
+                   : "memory");
+  }
+}
+
+// One 32-variable chunk of a homogeneous degree-D tile, with its base pointers.
+struct VarChunk {
+  int g, tile, half, kb, nval;
+  uint32_t am;
+  const float* llr0;  // llr_h row of the chunk's first variable
+  const float* c2v0;  // c2v of the group
+};
+
+template <int D>
+__device__ __forceinline__ VarChunk var_chunk(const Args& a, const VarTile& t, int half) {
+  VarChunk c;
+  c.g = t.g;
+  c.tile = t.tile;
+  c.half = half;
+  c.kb = t.kb + half * 32 * D;
+  c.nval = max(0, min(32, a.NV - (t.h0 + half * 32)));
+  c.am = a.group_active[t.g];
+  c.llr0 = a.llr_h + (static_cast<size_t>(t.g) * a.NH + t.h0 + half * 32) * kLanes;
+  c.c2v0 = a.c2v + static_cast<size_t>(t.g) * a.EH * kLanes;
+  return c;
+}
+
+// Runs this warp's degree-D tiles (starting with grabbed tile w) as one
+// pipeline over their chunks; returns the next grabbed tile it did not take.
 template <int D, int QMODE>
-__device__ __forceinline__ void var_chunk_typed(const Args& a, int g, int h0, const int32_t* ve, float* ring,
-                                                int lane, bool act, uint32_t amask, double* acc, uint32_t* hw) {
+__device__ long long var_stream(const Args& a, long long w, long long total, int32_t (*sve)[32 * 16], float* ring,
+                                int lane) {
   constexpr int K = VarShape<D>::K;
-  constexpr int NB = 32 / K;
-  const float* llr0 = a.llr_h + (static_cast<size_t>(g) * a.NH + h0) * kLanes;
-  const float* c2v0 = a.c2v + static_cast<size_t>(g) * a.EH * kLanes;
-  float* postg = a.post + (static_cast<size_t>(g) * a.NV + h0) * kLanes + lane;
+  constexpr int NS = VarShape<D>::NS;
+  constexpr int NB = 32 / K;  // batches per chunk
+  constexpr int RS = VarShape<D>::ROWS * kLanes;  // stage stride
+  static_assert(NB >= 2 * NS - 1, "the next chunk's edge ids must land before its first batch is issued");
   const int lrow = lane >> 3;
   const int lcol = (lane & 7) * 4;
-  const bool qact = ((amask >> lcol) & 0xFu) != 0u;
   const uint64_t pol = policy_evict_first();
-  constexpr int NS = VarShape<D>::NS;
-  constexpr int RS = VarShape<D>::ROWS * kLanes;  // stage stride
-#pragma unroll
-  for (int p = 0; p < NS - 1; ++p)
-    if (p < NB) var_batch_issue<D>(ring + p * RS, llr0, c2v0, ve, p * K, lrow, lcol, qact, pol);
+
+  VarTile tile = var_tile(a, w);
+  VarChunk cur = var_chunk<D>(a, tile, 0), nxt = cur;
+  bool has_nxt = false;
+  long long w_after = total;  // the tile grabbed after the current one
+  int2 desc_after = make_int2(-1, 0);
+  int kpend = var_grab_issue(a, lane);  // grabbed one chunk ahead of its use
+  int wb = 0;  // edge-id buffer of cur
+  var_stage_ve<D>(sve[wb], a.vedge_t, cur.kb, lane);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  int slot_issue = 0, slot_comp = 0;  // ring slots of the next batch to issue / compute
+  // one commit group per pipeline step (possibly empty); pos counts batches from cur's batch 0
+  auto issue_at = [&](int pos) {
+    const bool in_cur = pos < NB;
+    if (in_cur || has_nxt) {
+      const VarChunk& c = in_cur ? cur : nxt;
+      var_batch_issue<D>(ring + slot_issue * RS, c.llr0, c.c2v0, in_cur ? sve[wb] : sve[wb ^ 1],
+                         (in_cur ? pos : pos - NB) * K, c.nval, lrow, lcol, ((c.am >> lcol) & 0xFu) != 0u, pol);
+    }
+    cp_async_commit();
+    if (++slot_issue == NS) slot_issue = 0;
+  };
 #pragma unroll 1
-  for (int b = 0; b < NB; ++b) {
-    if (b + NS - 1 < NB)
-      var_batch_issue<D>(ring + ((b + NS - 1) % NS) * RS, llr0, c2v0, ve, (b + NS - 1) * K, lrow, lcol, qact, pol);
-    cp_async_wait_upto(min(NS - 1, NB - 1 - b));
-    __syncwarp();
-    var_batch_compute<D, QMODE>(ring + lane + (b % NS) * RS, postg, b * K, lane, act, acc, hw);
-    __syncwarp();
+  for (int p = 0; p < NS - 1; ++p) issue_at(p);
+  double acc0 = 0.0;
+  for (;;) {
+    // the chunk after cur: the second half of the tile, or the grabbed tile
+    // if it has the same degree.  The grab was issued a chunk earlier and its
+    // descriptor loaded during the first half, so neither latency is exposed.
+    if (cur.half == 0) {
+      nxt = var_chunk<D>(a, tile, 1);
+      has_nxt = true;
+      w_after = var_grab_resolve(a, kpend, lane);
+      if (w_after < total) desc_after = __ldg(&a.vtile[static_cast<int>(w_after % a.n_tiles)]);
+    } else {
+      has_nxt = w_after < total && desc_after.x == D;
+      if (has_nxt) {
+        tile = var_tile(a, w_after, desc_after.y);
+        nxt = var_chunk<D>(a, tile, 0);
+        kpend = var_grab_issue(a, lane);
+      }
+    }
+    if (has_nxt) var_stage_ve<D>(sve[wb ^ 1], a.vedge_t, nxt.kb, lane);  // travels with this step's group
+    const bool act = (cur.am >> lane) & 1u;
+    const size_t hv = static_cast<size_t>(cur.g) * a.NV + static_cast<size_t>(cur.tile) * kQTile + cur.half * 32;
+    float* postg = a.post + hv * kLanes + lane;
+    uint32_t* ebg = a.ebits + static_cast<size_t>(cur.g) * a.EH;
+    double acc = 0.0;
+    uint32_t hw = 0u;
+#pragma unroll 1
+    for (int b = 0; b < NB; ++b) {
+      issue_at(b + NS - 1);
+      cp_async_wait<NS - 1>();
+      __syncwarp();  // rows (and the next chunk's edge ids) were copied by other lanes
+      var_batch_compute<D, QMODE>(ring + lane + slot_comp * RS, postg, ebg, sve[wb], b * K, cur.nval, lane, act,
+                                  acc, hw);
+      if (++slot_comp == NS) slot_comp = 0;
+      __syncwarp();  // stage is refilled in the next round
+    }
+    if (lane < cur.nval) a.hbits[hv + lane] = hw;
+    if (cur.half == 0) {
+      acc0 = acc;
+    } else {
+      a.q_part[(static_cast<size_t>(cur.g) * a.n_tiles + cur.tile) * kLanes + lane] = acc0 + acc;
+    }
+    if (!has_nxt) break;
+    cur = nxt;
+    wb ^= 1;
   }
+  cp_async_wait<0>();
+  __syncwarp();
+  return w_after;
 }
 
 // ve points at the edge ids of CSC slot `kb` (staged copy or global array).
@@ -728,102 +907,95 @@ __device__ __forceinline__ float var_sum(const Args& a, size_t gl, size_t ge, in
   return p;
 }
 
+// Generic tile (mixed degrees, partial, or degree > 12): per variable,
+// register gathers.
+template <int QMODE>
+__device__ void var_tile_generic(const Args& a, long long w, int32_t* sptr, int lane) {
+  const VarTile t = var_tile(a, w);
+  const uint32_t amask = a.group_active[t.g];
+  const bool act = (amask >> lane) & 1u;
+  const size_t gl = static_cast<size_t>(t.g) * a.NH;
+  const size_t gv = static_cast<size_t>(t.g) * a.NV;
+  const size_t ge = static_cast<size_t>(t.g) * a.EH;
+  double acc = 0.0, acc0 = 0.0;
+  for (int cc = 0; cc < kQTile / 32; ++cc) {
+    const int h0 = t.h0 + cc * 32;
+    const int nv = max(0, min(kLanes, a.NV - h0));
+    if (cc == 1) {
+      acc0 = acc;
+      acc = 0.0;
+    }
+    if (nv == 0) continue;
+    __syncwarp();
+    if (lane < nv) sptr[lane] = __ldg(&a.vptr[h0 + lane]);
+    if (lane == 0) sptr[nv] = __ldg(&a.vptr[h0 + nv]);
+    __syncwarp();
+    uint32_t hw = 0u;
+    for (int i = 0; i < nv; ++i) {
+      const int h = h0 + i;
+      const int k0 = sptr[i], k1 = sptr[i + 1];
+      float p = 0.0f;
+      if (act) {
+        p = var_sum(a, gl, ge, h, k0, k1, a.vedge + k0, k0, lane);
+        a.post[(gv + h) * kLanes + lane] = p;
+        acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
+      if (lane == i) hw = word;
+      for (int k = k0 + lane; k < k1; k += 32) a.ebits[ge + __ldg(&a.vedge[k])] = word;
+    }
+    if (lane < nv) a.hbits[gv + h0 + lane] = hw;
+  }
+  a.q_part[(static_cast<size_t>(t.g) * a.n_tiles + t.tile) * kLanes + lane] = acc0 + acc;
+}
+
 template <int QMODE>
 __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
-  __shared__ double red[kVarWarps][kLanes];
+  __shared__ int32_t s_ve[kVarWarps][2][32 * 16];
   __shared__ int32_t s_ptr[kVarWarps][33];
-  __shared__ int32_t s_ve[kVarWarps][kVarStage];
   __shared__ __align__(16) float s_ring[kVarWarps][kVarRingRows * kLanes];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const long long total = static_cast<long long>(a.G) * a.n_tiles;
-  for (long long w = blockIdx.x; w < total;) {
-    const int g = static_cast<int>(w / a.n_tiles);
-    const int tile = static_cast<int>(w - static_cast<long long>(g) * a.n_tiles);
-    const uint32_t amask = a.group_active[g];
-    if (amask == 0u) {
-      w = skip_group(w, a.n_tiles, gridDim.x);
-      continue;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[7] = 0;  // k_check chunk scheduler (next step)
+  long long w = var_grab(a, lane);
+  while (w < total) {
+    const int d = __ldg(&a.vtile[static_cast<int>(w % a.n_tiles)]).x;
+    switch (d) {
+#define BPDEC_VSTREAM(D_)                                                   \
+  case D_:                                                                  \
+    w = var_stream<D_, QMODE>(a, w, total, s_ve[warp], s_ring[warp], lane); \
+    continue;
+      BPDEC_VSTREAM(2)
+      BPDEC_VSTREAM(3)
+      BPDEC_VSTREAM(4)
+      BPDEC_VSTREAM(6)
+      BPDEC_VSTREAM(8)
+      BPDEC_VSTREAM(12)
+      BPDEC_VSTREAM(16)
+#undef BPDEC_VSTREAM
+      default:
+        break;
     }
-    const bool act = (amask >> lane) & 1u;
-    double acc = 0.0;  // this warp's chunks, summed in variable order
-    const size_t gl = static_cast<size_t>(g) * a.NH;
-    const size_t gv = static_cast<size_t>(g) * a.NV;
-    const size_t ge = static_cast<size_t>(g) * a.EH;
-    for (int cc = 0; cc < kVarChunks; ++cc) {
-    const int h0 = tile * kQTile + (warp * kVarChunks + cc) * kLanes;
-    const int nv = max(0, min(kLanes, a.NV - h0));
-    if (nv > 0) {
-      if (lane < nv) s_ptr[warp][lane] = __ldg(&a.vptr[h0 + lane]);
-      if (lane == 0) s_ptr[warp][nv] = __ldg(&a.vptr[h0 + nv]);
-      __syncwarp();
-      const int kb = s_ptr[warp][0];
-      const int nk = s_ptr[warp][nv] - kb;
-      const bool staged = nk <= kVarStage;
-      if (staged)
-        for (int i = lane; i < nk; i += 32) s_ve[warp][i] = __ldg(&a.vedge[kb + i]);
-      __syncwarp();
-      const int32_t* ve = staged ? &s_ve[warp][0] : a.vedge + kb;
-      const int vt = staged ? __ldg(&a.vtype[h0 / 32]) : -1;
-      uint32_t hw = 0u;
-      bool typed = true;
-      switch (vt) {
-#define BPDEC_VTYPED(D_) \
-  case D_:               \
-    var_chunk_typed<D_, QMODE>(a, g, h0, ve, s_ring[warp], lane, act, amask, &acc, &hw); \
-    break;
-        BPDEC_VTYPED(2)
-        BPDEC_VTYPED(3)
-        BPDEC_VTYPED(4)
-        BPDEC_VTYPED(6)
-        BPDEC_VTYPED(8)
-        BPDEC_VTYPED(12)
-        BPDEC_VTYPED(16)
-        BPDEC_VTYPED(20)
-#undef BPDEC_VTYPED
-        default:
-          typed = false;
-      }
-      if (!typed) {
-        for (int i = 0; i < nv; ++i) {
-          const int h = h0 + i;
-          float p = 0.0f;
-          if (act) {
-            p = var_sum(a, gl, ge, h, s_ptr[warp][i], s_ptr[warp][i + 1], ve, kb, lane);
-            a.post[(gv + h) * kLanes + lane] = p;
-            acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
-          }
-          const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
-          if (lane == i) hw = word;
-        }
-      }
-      if (lane < nv) a.hbits[gv + h0 + lane] = hw;
-    }
-    __syncwarp();
-    }
-    red[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0) {
-      double q = red[0][lane];
-#pragma unroll
-      for (int k = 1; k < kVarWarps; ++k) q += red[k][lane];
-      a.q_part[(static_cast<size_t>(g) * a.n_tiles + tile) * kLanes + lane] = q;
-    }
-    __syncthreads();
-    w += gridDim.x;
+    var_tile_generic<QMODE>(a, w, s_ptr[warp], lane);
+    w = var_grab(a, lane);
   }
 }
 
 // ---------------------------------------------------------- k_syndrome --
-// Thread = one check x 32 slots (bit-sliced); checks padded to a multiple of
-// 32 per group so a warp never straddles two groups.
-// Parity of one check's degree>=2 part in group g: XOR of the gathered
-// hard-bit words (indices already in registers, loads independent).
+// Warp = 32 consecutive (device-order) checks, lane = check, all groups.
+// Parity of a check = target syndrome ^ degree-1 part (synp, from k_check)
+// ^ the hard-decision words of its degree>=2 edges, which k_var stored per
+// edge in check-major order (ebits): the check's words are contiguous, so
+// the pass streams instead of gathering.  A group is skipped as soon as
+// every active frame in it is known to fail; new failing frames are
+// published at once (block-local copy first, so about one global atomic per
+// block and group).
 template <int NH>
-__device__ __forceinline__ uint32_t syn_hi_fixed(const uint32_t* __restrict__ hb, const int32_t (&idx)[4]) {
-  uint32_t w[NH];
+__device__ __forceinline__ uint32_t xor_words(const uint32_t* __restrict__ p) {
+  uint32_t w[NH > 0 ? NH : 1];
 #pragma unroll
-  for (int j = 0; j < NH; ++j) w[j] = hb[idx[j]];
+  for (int j = 0; j < NH; ++j) w[j] = p[j];
   uint32_t x = 0u;
 #pragma unroll
   for (int j = 0; j < NH; ++j) x ^= w[j];
@@ -831,11 +1003,6 @@ __device__ __forceinline__ uint32_t syn_hi_fixed(const uint32_t* __restrict__ hb
 }
 
 __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
-  // warp = 32 consecutive checks (lane = check), all groups: the gather
-  // indices are loaded once and reused by every live group.  Failing frames
-  // are OR-ed into a block-local word per group (shared memory) and pushed
-  // to the global mask once per block; a group is skipped as soon as every
-  // active frame in it is known to fail.
   extern __shared__ uint32_t s_fail[];  // [G]
   for (int t = threadIdx.x; t < a.G; t += blockDim.x) s_fail[t] = 0u;
   __syncthreads();
@@ -844,11 +1011,16 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
   const int nwarps = static_cast<int>((static_cast<long long>(gridDim.x) * blockDim.x) >> 5);
   for (int ch = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); ch < chunks;
        ch += nwarps) {
-    bool live = false;
-    for (int g = 0; g < a.G && !live; ++g) {
-      const uint32_t amask = a.group_active[g];
-      const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
-      live = amask != 0u && (fl & amask) != amask;
+    bool live = false;  // any group with an active frame not yet known to fail (lanes scan groups)
+    for (int g0 = 0; g0 < a.G && !live; g0 += 32) {
+      const int g = g0 + lane;
+      bool l = false;
+      if (g < a.G) {
+        const uint32_t amask = a.group_active[g];
+        const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
+        l = amask != 0u && (fl & amask) != amask;
+      }
+      live = __any_sync(0xffffffffu, l);
     }
     if (!live) continue;  // warp-uniform
     const int c = ch * 32 + lane;
@@ -866,39 +1038,32 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
       e0 = 0;
       nh = 0;
     }
-    const bool fixed = cdk.x >= 0 && nh <= 4;
-    int32_t idx[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) idx[j] = (fixed && j < nh) ? __ldg(&a.chk_hi_h[e0 + j]) : 0;
+    const int fixed = cdk.x >= 0 ? nh : -1;
     for (int g = 0; g < a.G; ++g) {
       const uint32_t amask = a.group_active[g];
       const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
       if (amask == 0u || (fl & amask) == amask) continue;  // warp-uniform
-      const uint32_t* hb = a.hbits + static_cast<size_t>(g) * a.NV;
+      const uint32_t* eb = a.ebits + static_cast<size_t>(g) * a.EH + e0;
       uint32_t word = 0u;
       if (valid) {
         word = a.synp[static_cast<size_t>(g) * a.M + c];
-        if (fixed) {
-          switch (nh) {
-            case 0: break;
-            case 1: word ^= syn_hi_fixed<1>(hb, idx); break;
-            case 2: word ^= syn_hi_fixed<2>(hb, idx); break;
-            case 3: word ^= syn_hi_fixed<3>(hb, idx); break;
-            default: word ^= syn_hi_fixed<4>(hb, idx); break;
-          }
-        } else {
-          for (int j = 0; j < nh; ++j) word ^= hb[__ldg(&a.chk_hi_h[e0 + j])];
+        switch (fixed) {
+          case 0: break;
+          case 1: word ^= xor_words<1>(eb); break;
+          case 2: word ^= xor_words<2>(eb); break;
+          case 3: word ^= xor_words<3>(eb); break;
+          case 4: word ^= xor_words<4>(eb); break;
+          default:
+            for (int j = 0; j < nh; ++j) word ^= eb[j];
         }
         word &= amask;
       }
       word = __reduce_or_sync(0xffffffffu, word);
-      if (lane == 0 && (word & ~fl) != 0u) atomicOr(&s_fail[g], word);
+      if (lane == 0 && (word & ~fl) != 0u) {
+        atomicOr(&s_fail[g], word);
+        atomicOr(&a.fail[g], word);
+      }
     }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < a.G; t += blockDim.x) {
-    const uint32_t w = s_fail[t];
-    if (w != 0u && (w & ~*reinterpret_cast<volatile uint32_t*>(&a.fail[t])) != 0u) atomicOr(&a.fail[t], w);
   }
 }
 
@@ -1589,6 +1754,16 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
     }
     ctype[k] = t;
   }
+  // k_check hand-out order: generic chunks (register path, latency-bound)
+  // first, degree-1-only chunks (skipped after a frame's first iteration) last
+  std::vector<int32_t> csched;
+  csched.reserve(ctype.size());
+  for (int pass = 0; pass < 3; ++pass)
+    for (size_t k = 0; k < ctype.size(); ++k) {
+      const int x = ctype[k].x;
+      const int cls = x < 0 ? 0 : ((x == 1 || x == 8) ? 2 : 1);
+      if (cls == pass) csched.push_back(static_cast<int32_t>(k));
+    }
   const int64_t EH = static_cast<int64_t>(chk_hi_h.size());
   std::vector<int32_t> vptr(NV + 1, 0), vedge;
   vedge.reserve(EH);
@@ -1598,15 +1773,38 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
     for (int32_t k = code.var_ptr[v]; k < code.var_ptr[v + 1]; ++k) vedge.push_back(hi_of_edge[code.var_edges[k]]);
     vptr[h + 1] = static_cast<int32_t>(vedge.size());
   }
-  std::vector<int32_t> vtype((NV + 31) / 32, -1);
-  for (size_t k = 0; k < vtype.size(); ++k) {
-    const int32_t h0 = static_cast<int32_t>(k * 32);
-    if (h0 + 32 > NV) continue;
-    const int32_t d0 = deg[horig[h0]];
-    bool same = true;
-    for (int32_t i = 1; i < 32 && same; ++i) same = deg[horig[h0 + i]] == d0;
-    if (same) vtype[k] = d0;
+  const int32_t n_tiles = std::max(1, (NV + kQTile - 1) / kQTile);
+  // k_var tiles: a tile of max degree <= 16 runs the typed path at the next
+  // supported degree D, its variables' CSC slices padded with -1 to D (and
+  // missing variables of the last tile padded entirely)
+  std::vector<int2> vtile(n_tiles);
+  std::vector<int32_t> vedge_t;
+  for (int32_t t = 0; t < n_tiles; ++t) {
+    const int32_t h0 = t * kQTile, h1 = std::min(NV, h0 + kQTile);
+    int32_t dmax = 0;
+    for (int32_t h = h0; h < h1; ++h) dmax = std::max(dmax, vptr[h + 1] - vptr[h]);
+    int32_t D = -1;
+    for (int32_t d : {2, 3, 4, 6, 8, 12, 16})
+      if (D < 0 && dmax <= d) D = d;
+    vtile[t] = make_int2(D, D < 0 ? vptr[std::min(h0, NV)] : static_cast<int32_t>(vedge_t.size()));
+    if (D < 0) continue;
+    for (int32_t i = 0; i < kQTile; ++i) {
+      const int32_t h = h0 + i;
+      int32_t k = 0;
+      if (h < NV)
+        for (; k < vptr[h + 1] - vptr[h]; ++k) vedge_t.push_back(vedge[vptr[h] + k]);
+      for (; k < D; ++k) vedge_t.push_back(-1);
+    }
   }
+  // keep 16-byte alignment of every tile slice (cp.async 16)
+  for (int32_t t = 0; t < n_tiles; ++t)
+    if (vtile[t].x >= 0 && (vtile[t].y & 3) != 0) throw CudaError("decoder: internal layout error (vedge_t alignment)");
+  std::vector<int32_t> vsched;
+  vsched.reserve(n_tiles);
+  for (int32_t t = 0; t < n_tiles; ++t)
+    if (vtile[t].x < 0) vsched.push_back(t);
+  for (int32_t t = 0; t < n_tiles; ++t)
+    if (vtile[t].x >= 0) vsched.push_back(t);
 
   Args& a = base;
   a.N = N;
@@ -1615,7 +1813,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.NV = NV;
   a.N1 = n1;
   a.EH = EH;
-  a.n_tiles = std::max(1, (NV + kQTile - 1) / kQTile);
+  a.n_tiles = n_tiles;
   a.G = G;
   a.MW = (M + 31) / 32;
   a.NW = (N + 31) / 32;
@@ -1635,7 +1833,10 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   for (int32_t cd = 0; cd < M; ++cd) cdev[corig[cd]] = cd;
   a.cdev = up(cdev, static_cast<int32_t*>(nullptr));
   a.ctype = up(ctype, static_cast<int4*>(nullptr));
-  a.vtype = up(vtype, static_cast<int32_t*>(nullptr));
+  a.csched = up(csched, static_cast<int32_t*>(nullptr));
+  a.vtile = up(vtile, static_cast<int2*>(nullptr));
+  a.vsched = up(vsched, static_cast<int32_t*>(nullptr));
+  a.vedge_t = up(vedge_t, static_cast<int32_t*>(nullptr));
   d_check_ptr = up(code.check_ptr, static_cast<int32_t*>(nullptr));
   d_check_vars = up(code.check_vars, static_cast<int32_t*>(nullptr));
 
@@ -1650,6 +1851,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.c2v = own(dalloc<float>(static_cast<size_t>(G) * EH * L, &dev_bytes));
   a.d1post = nullptr;  // allocated on first request
   a.hbits = own(dalloc<uint32_t>(static_cast<size_t>(G) * NV, &dev_bytes));
+  a.ebits = own(dalloc<uint32_t>(static_cast<size_t>(G) * EH, &dev_bytes));
   a.d1bits = own(dalloc<uint32_t>(static_cast<size_t>(G) * n1, &dev_bytes));
   a.synp = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
   a.syn_target = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
@@ -1679,8 +1881,37 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
 
   const int sms = prop.multiProcessorCount;
   sms_ = sms;
-  grid_check = sms * 16;
-  grid_var = sms * 16;
+  {
+    // k_check warps run dynamically scheduled chunk loops: one wave
+    int per_sm = 0, per_sm2 = 0;
+    auto occ = [&](auto kern) {
+      int n = 0;
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kCheckThreads, 0));
+      return n;
+    };
+#define BPDEC_OCC(D)                                              \
+  if (per_sm == 0 && max_check_deg <= D) {                        \
+    per_sm = occ(k_check<D, false>);                              \
+    per_sm2 = occ(k_check<D, true>);                              \
+  }
+    BPDEC_OCC(3)
+    BPDEC_OCC(4)
+    BPDEC_OCC(6)
+    BPDEC_OCC(8)
+    BPDEC_OCC(16)
+    BPDEC_OCC(256)
+#undef BPDEC_OCC
+    grid_check = sms * std::max(1, std::min(per_sm, per_sm2));
+  }
+  {
+    // k_var warps run persistent, dynamically scheduled tile streams: one wave
+    int per_sm = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_var<1>, kVarWarps * 32, 0));
+    grid_var = sms * std::max(1, per_sm);
+#ifdef BPDEC_EXP_GRID16
+    grid_var = sms * 16;
+#endif
+  }
   grid_syn = sms * 8;
   // load / extract are no-ops on most steps: keep their grids small
   turn_item_blocks = sms * 8;
