@@ -167,6 +167,13 @@ __device__ __forceinline__ void st_pred(float* p, float v, bool pred) {
                : "memory");
 }
 
+__device__ __forceinline__ void st_pred_u32(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}"
+               :
+               : "l"(p), "r"(v), "r"(static_cast<int>(pred))
+               : "memory");
+}
+
 // Advances a grid-stride cursor past the remainder of an inactive group.
 __device__ __forceinline__ long long skip_group(long long w, long long per_group, long long stride) {
   const long long next = (w / per_group + 1) * per_group;
@@ -711,8 +718,8 @@ __device__ __forceinline__ void var_batch_issue(float* stage, const float* llr0,
     const int r = r0 + lrow;
     if (r < K * D) {
       const int e = ve[i0 * D + r];
-      cp_async16_ef(stage + (K + r) * kLanes + lcol, c2vg + static_cast<size_t>(e < 0 ? 0 : e) * kLanes + lcol,
-                    qact && e >= 0, pol);
+      cp_async16_ef(stage + (K + r) * kLanes + lcol,
+                    c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0)) * kLanes) + lcol, qact && e >= 0, pol);
     }
   }
 }
@@ -731,10 +738,8 @@ __device__ __forceinline__ void var_batch_compute(const float* stage, float* pos
     if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
     const uint32_t word = __ballot_sync(0xffffffffu, on && p < 0.0f);
     if (lane == ((i0 + k) & 31)) hw = word;
-    if (lane < D) {
-      const int e = ve[(i0 + k) * D + lane];
-      if (e >= 0) ebg[e] = word;
-    }
+    const int e = ve[(i0 + k) * D + (lane < D ? lane : 0)];
+    st_pred_u32(ebg + static_cast<uint32_t>(max(e, 0)), word, lane < D && e >= 0);
   }
 }
 
@@ -828,13 +833,22 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
   cp_async_wait<0>();
   __syncwarp();
   int slot_issue = 0, slot_comp = 0;  // ring slots of the next batch to issue / compute
+  // issue contexts of cur and nxt as scalars (no struct selected at run time)
+  const float* llr_c = cur.llr0;
+  const float* c2v_c = cur.c2v0;
+  int nval_c = cur.nval;
+  bool qact_c = ((cur.am >> lcol) & 0xFu) != 0u;
+  const float* llr_n = llr_c;
+  const float* c2v_n = c2v_c;
+  int nval_n = 0;
+  bool qact_n = false;
   // one commit group per pipeline step (possibly empty); pos counts batches from cur's batch 0
   auto issue_at = [&](int pos) {
     const bool in_cur = pos < NB;
     if (in_cur || has_nxt) {
-      const VarChunk& c = in_cur ? cur : nxt;
-      var_batch_issue<D>(ring + slot_issue * RS, c.llr0, c.c2v0, in_cur ? sve[wb] : sve[wb ^ 1],
-                         (in_cur ? pos : pos - NB) * K, c.nval, lrow, lcol, ((c.am >> lcol) & 0xFu) != 0u, pol);
+      var_batch_issue<D>(ring + slot_issue * RS, in_cur ? llr_c : llr_n, in_cur ? c2v_c : c2v_n,
+                         in_cur ? sve[wb] : sve[wb ^ 1], (in_cur ? pos : pos - NB) * K, in_cur ? nval_c : nval_n, lrow,
+                         lcol, in_cur ? qact_c : qact_n, pol);
     }
     cp_async_commit();
     if (++slot_issue == NS) slot_issue = 0;
@@ -859,7 +873,13 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
         kpend = var_grab_issue(a, lane);
       }
     }
-    if (has_nxt) var_stage_ve<D>(sve[wb ^ 1], a.vedge_t, nxt.kb, lane);  // travels with this step's group
+    if (has_nxt) {
+      var_stage_ve<D>(sve[wb ^ 1], a.vedge_t, nxt.kb, lane);  // travels with this step's group
+      llr_n = nxt.llr0;
+      c2v_n = nxt.c2v0;
+      nval_n = nxt.nval;
+      qact_n = ((nxt.am >> lcol) & 0xFu) != 0u;
+    }
     const bool act = (cur.am >> lane) & 1u;
     const size_t hv = static_cast<size_t>(cur.g) * a.NV + static_cast<size_t>(cur.tile) * kQTile + cur.half * 32;
     float* postg = a.post + hv * kLanes + lane;
@@ -884,6 +904,10 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
     }
     if (!has_nxt) break;
     cur = nxt;
+    llr_c = llr_n;
+    c2v_c = c2v_n;
+    nval_c = nval_n;
+    qact_c = qact_n;
     wb ^= 1;
   }
   cp_async_wait<0>();
@@ -1908,9 +1932,6 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
     int per_sm = 0;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_var<1>, kVarWarps * 32, 0));
     grid_var = sms * std::max(1, per_sm);
-#ifdef BPDEC_EXP_GRID16
-    grid_var = sms * 16;
-#endif
   }
   grid_syn = sms * 8;
   // load / extract are no-ops on most steps: keep their grids small
