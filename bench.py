@@ -68,22 +68,54 @@ def parse():
 
 
 # ------------------------------------------------------------ clocks --
+def gpu_uuid(dev):
+    """NVML / nvidia-smi identity of CUDA device `dev` (robust to
+    CUDA_VISIBLE_DEVICES renumbering); the CUDA ordinal if unknown."""
+    import torch
+    try:
+        u = str(torch.cuda.get_device_properties(dev).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return dev
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML
+    polled every few ms from a thread (pynvml), else `nvidia-smi -lms`."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int, period_ms: int = 200):
         self.index = index
         self.period = period_ms
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons set) from NVML
+        self.running = False
 
     def start(self, enabled=True):
         if not enabled:
             return
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = (pynvml.nvmlDeviceGetHandleByUUID(self.index) if isinstance(self.index, str)
+                      else pynvml.nvmlDeviceGetHandleByIndex(self.index))
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.running = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            while not self.samples and self.t.is_alive():
+                time.sleep(0.001)
+            self.samples.clear()
+            return
+        except Exception:  # no pynvml / NVML: fall back to nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -98,11 +130,33 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def _poll(self):
+        p = self.nvml
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        get_reasons = getattr(p, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            p.nvmlDeviceGetCurrentClocksThrottleReasons
+        while self.running:
+            try:
+                sm = p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM)
+                r = get_reasons(self.h)
+                self.samples.append((float(sm), float(self.max_sm), {n for n, b in bits.items() if r & b}))
+            except Exception:
+                break
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self.running = False
+            self.t.join(timeout=2)
+            smp = list(self.samples)
+            reasons = set().union(*[x[2] for x in smp]) if smp else set()
+            return {"sm_mhz": float(np.median([x[0] for x in smp])) if smp else None,
+                    "sm_max_mhz": max(x[1] for x in smp) if smp else None,
+                    "reasons": sorted(reasons), "samples": len(smp), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         self.proc.terminate()
@@ -111,7 +165,6 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 9:
@@ -121,11 +174,11 @@ class ClockSampler:
                 mx.append(float(p[2]))
             except ValueError:
                 continue
-            for k, nm in enumerate(names):
+            for k, nm in enumerate(self.NAMES):
                 if p[5 + k].lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # -------------------------------------------------------- distributed --
@@ -301,7 +354,7 @@ def run_ours(args):
         int(out["iterations"].sum().item())  # same host read as the timed steps (loads torch's kernel once)
         n_warm += 1
     torch.cuda.synchronize()
-    clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local, args.clock_ms)
+    clocks = ClockSampler(gpu_uuid(torch.cuda.current_device()), args.clock_ms)
     barrier(dist)
     torch.cuda.synchronize()
     clocks.start(not args.no_clocks)

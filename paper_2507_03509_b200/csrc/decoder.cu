@@ -1015,78 +1015,87 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
 // every active frame in it is known to fail; new failing frames are
 // published at once (block-local copy first, so about one global atomic per
 // block and group).
-template <int NH>
-__device__ __forceinline__ uint32_t xor_words(const uint32_t* __restrict__ p) {
-  uint32_t w[NH > 0 ? NH : 1];
-#pragma unroll
-  for (int j = 0; j < NH; ++j) w[j] = p[j];
-  uint32_t x = 0u;
-#pragma unroll
-  for (int j = 0; j < NH; ++j) x ^= w[j];
-  return x;
+__device__ __forceinline__ uint32_t ldu32_pred(const uint32_t* p, bool pred) {
+  uint32_t v = 0u;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.u32 %0, [%1];\n\t}"
+               : "+r"(v)
+               : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
 }
 
+constexpr int kSynChunks = 4;  // chunks per warp pass (their loads are in flight together)
+
 __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
-  extern __shared__ uint32_t s_fail[];  // [G]
-  for (int t = threadIdx.x; t < a.G; t += blockDim.x) s_fail[t] = 0u;
+  // group state cached per block: active masks (constant during the pass)
+  // and the failing frames known so far (global at block start | this block)
+  extern __shared__ uint32_t s_grp[];  // [2][G]: active, fail
+  uint32_t* s_act = s_grp;
+  uint32_t* s_fail = s_grp + a.G;
+  for (int t = threadIdx.x; t < a.G; t += blockDim.x) {
+    s_act[t] = a.group_active[t];
+    s_fail[t] = *reinterpret_cast<volatile uint32_t*>(&a.fail[t]);
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int chunks = (a.M + 31) / 32;
+  const int passes = (chunks + kSynChunks - 1) / kSynChunks;
   const int nwarps = static_cast<int>((static_cast<long long>(gridDim.x) * blockDim.x) >> 5);
-  for (int ch = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); ch < chunks;
-       ch += nwarps) {
+  for (int q = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); q < passes;
+       q += nwarps) {
     bool live = false;  // any group with an active frame not yet known to fail (lanes scan groups)
     for (int g0 = 0; g0 < a.G && !live; g0 += 32) {
       const int g = g0 + lane;
-      bool l = false;
-      if (g < a.G) {
-        const uint32_t amask = a.group_active[g];
-        const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
-        l = amask != 0u && (fl & amask) != amask;
-      }
-      live = __any_sync(0xffffffffu, l);
+      live = __any_sync(0xffffffffu, g < a.G && s_act[g] != 0u && (s_fail[g] & s_act[g]) != s_act[g]);
     }
     if (!live) continue;  // warp-uniform
-    const int c = ch * 32 + lane;
-    const bool valid = c < a.M;
-    const int4 cdk = __ldg(&a.ctype[ch]);
-    int nh, e0;
-    if (cdk.x >= 0) {  // homogeneous chunk: NH hi edges per check, contiguous
-      nh = cdk.x >> 3;
-      e0 = cdk.y + lane * nh;
-    } else if (valid) {
-      const int4 d = __ldg(&a.cdesc[c]);
-      e0 = d.x;
-      nh = d.y - d.x;
-    } else {
-      e0 = 0;
-      nh = 0;
+    int e0[kSynChunks], nh[kSynChunks], fixed[kSynChunks];
+    bool valid[kSynChunks];
+#pragma unroll
+    for (int u = 0; u < kSynChunks; ++u) {
+      const int ch = q * kSynChunks + u;
+      const int c = ch * 32 + lane;
+      valid[u] = ch < chunks && c < a.M;
+      const int4 cdk = ch < chunks ? __ldg(&a.ctype[ch]) : make_int4(0, 0, 0, 0);
+      if (cdk.x >= 0) {  // homogeneous chunk: NH hi edges per check, contiguous
+        nh[u] = cdk.x >> 3;
+        e0[u] = cdk.y + lane * nh[u];
+        fixed[u] = 1;
+      } else {
+        const int4 d = valid[u] ? __ldg(&a.cdesc[c]) : make_int4(0, 0, 0, 0);
+        e0[u] = d.x;
+        nh[u] = d.y - d.x;
+        fixed[u] = 0;
+      }
+      if (!valid[u]) nh[u] = 0;
     }
-    const int fixed = cdk.x >= 0 ? nh : -1;
     for (int g = 0; g < a.G; ++g) {
-      const uint32_t amask = a.group_active[g];
-      const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&a.fail[g]) | s_fail[g];
+      const uint32_t amask = s_act[g];
+      const uint32_t fl = s_fail[g];
       if (amask == 0u || (fl & amask) == amask) continue;  // warp-uniform
-      const uint32_t* eb = a.ebits + static_cast<size_t>(g) * a.EH + e0;
-      uint32_t word = 0u;
-      if (valid) {
-        word = a.synp[static_cast<size_t>(g) * a.M + c];
-        switch (fixed) {
-          case 0: break;
-          case 1: word ^= xor_words<1>(eb); break;
-          case 2: word ^= xor_words<2>(eb); break;
-          case 3: word ^= xor_words<3>(eb); break;
-          case 4: word ^= xor_words<4>(eb); break;
-          default:
-            for (int j = 0; j < nh; ++j) word ^= eb[j];
-        }
-        word &= amask;
+      const uint32_t* eb = a.ebits + static_cast<size_t>(g) * a.EH;
+      const uint32_t* sp = a.synp + static_cast<size_t>(g) * a.M;
+      uint32_t word[kSynChunks];
+#pragma unroll
+      for (int u = 0; u < kSynChunks; ++u) {
+        const int c = (q * kSynChunks + u) * 32 + lane;
+        word[u] = ldu32_pred(sp + (valid[u] ? c : 0), valid[u]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) word[u] ^= ldu32_pred(eb + e0[u] + (j < nh[u] ? j : 0), j < nh[u]);
       }
-      word = __reduce_or_sync(0xffffffffu, word);
-      if (lane == 0 && (word & ~fl) != 0u) {
-        atomicOr(&s_fail[g], word);
-        atomicOr(&a.fail[g], word);
+      uint32_t any = 0u;
+#pragma unroll
+      for (int u = 0; u < kSynChunks; ++u) {
+        for (int j = 4; j < nh[u]; ++j) word[u] ^= eb[e0[u] + j];  // checks with more than 4 such edges
+        (void)fixed[u];
+        any |= word[u];
       }
+      any = __reduce_or_sync(0xffffffffu, any & amask);
+      // new failing frames: block-local copy first, published at once
+      if (lane == 0 && (any & ~fl) != 0u) {
+        atomicOr(&s_fail[g], any);
+        atomicOr(&a.fail[g], any);
+      }
+      __syncwarp();
     }
   }
 }
@@ -2005,7 +2014,7 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
       k_var<1><<<grid_var, kVarWarps * 32, 0, st>>>(a);
   });
   if (a.use_pce)
-    launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, G * sizeof(uint32_t), st>>>(a); });
+    launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 2 * G * sizeof(uint32_t), st>>>(a); });
   launch(kTerm, st, [&] { k_terminate<<<G * kTermBlocks, kTermThreads, 0, st>>>(a); });
   launch(kTurnover, st, [&] { launch_turnover(a, st, want_post); });
   // tail compaction (no-op unless the queue is drained and live frames fit

@@ -1,0 +1,8 @@
+#!/bin/bash
+# tests (non full-size) + probe + cfg2/cfg3 bench lines + launch list
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+bash scripts/gpu_quick.sh
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_cfg2.log 2>&1; echo "bench_cfg2=$?"
+timeout 600 python bench.py --workload cfg3 --no-cpu-baseline > gpurun_out/bench_cfg3.log 2>&1; echo "bench_cfg3=$?"
+bash scripts/gpu_launches.sh
