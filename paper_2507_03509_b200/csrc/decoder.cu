@@ -538,20 +538,30 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
   const uint64_t pol = policy_evict_first();
   constexpr int NS = kStages;
+  // one commit group per step (empty past the last batch), so the wait
+  // count is a constant
 #pragma unroll
-  for (int p = 0; p < NS - 1; ++p)
+  for (int p = 0; p < NS - 1; ++p) {
     if (p < NB)
       check_batch_issue<NH, ND>(ring + p * kStageRows * kLanes, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v,
                                 pol);
+    else
+      cp_async_commit();
+  }
+  int slot_i = NS - 1, slot_c = 0;  // ring stages of the next batch to issue / compute
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
     if (b + NS - 1 < NB)
-      check_batch_issue<NH, ND>(ring + ((b + NS - 1) % NS) * kStageRows * kLanes, post0, c2v0, llr0, hh,
-                                (b + NS - 1) * K, lrow, lcol, qact, qc2v, pol);
-    cp_async_wait_upto(min(NS - 1, NB - 1 - b));
+      check_batch_issue<NH, ND>(ring + slot_i * kStageRows * kLanes, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow,
+                                lcol, qact, qc2v, pol);
+    else
+      cp_async_commit();
+    if (++slot_i == NS) slot_i = 0;
+    cp_async_wait<NS - 1>();
     __syncwarp();  // rows were copied by other lanes
-    check_batch_compute<NH, ND, WANT_POST, FM>(ring + lane + (b % NS) * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
+    check_batch_compute<NH, ND, WANT_POST, FM>(ring + lane + slot_c * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
                                                lane, act, first, cl, clamp, synw, d1w);
+    if (++slot_c == NS) slot_c = 0;
     __syncwarp();  // stage is refilled in the next round
   }
 }
