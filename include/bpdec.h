@@ -165,6 +165,17 @@ int bpdec_decode_batch(bpdec_decoder* dec, int32_t batch, const float* llr,
                        void* bits_out, int32_t* iterations_out, uint8_t* reason_out,
                        float* posteriors_out, double* q_trace_out, void* stream);
 
+/* Pipelined host input: starts the host->device copy of a batch (pinned host
+ * memory for full overlap) on the decoder's copy stream and returns at once.
+ * A later bpdec_decode_batch with the same llr / syndrome pointers and batch
+ * decodes from the staged copy, so staging batch k+1 before decoding batch k
+ * overlaps its upload with the decode.  Two staging slots; staging a third
+ * batch replaces the older unconsumed one (whose decode then copies again).
+ * The host buffers must stay unchanged until that decode returns.  No
+ * reference counterpart (the reference decodes host spans on the CPU). */
+int bpdec_decoder_stage_inputs(bpdec_decoder* dec, int32_t batch, const float* llr_host,
+                               const uint32_t* syndrome_host);
+
 /* Device-side frame generator for resident-input benchmarks: same draws as
  * bpdec_sample_frames, written to DEVICE buffers (llr [n][N], syndrome
  * [n][ceil(M/32)], x packed [n][ceil(N/32)]; x/syndrome may be NULL). */

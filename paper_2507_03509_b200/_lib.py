@@ -79,6 +79,7 @@ SIGNATURES = [
     ("bpdec_decode_batch", C.c_int,
      [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(Config), C.c_uint32, C.c_void_p,
       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("bpdec_decoder_stage_inputs", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     ("bpdec_decoder_sample_frames_device", C.c_int,
      [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
       C.c_void_p, C.c_void_p]),

@@ -471,6 +471,14 @@ int bpdec_run_trials(bpdec_decoder* dec, double snr, const int32_t* punctured, i
   });
 }
 
+int bpdec_decoder_stage_inputs(bpdec_decoder* dec, int32_t batch, const float* llr_host,
+                               const uint32_t* syndrome_host) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_stage_inputs(dec->impl, batch, llr_host, syndrome_host);
+  });
+}
+
 int bpdec_decoder_set_profiling(bpdec_decoder* dec, int32_t enable) {
   return guarded([&] {
     need(dec, "decoder");

@@ -1664,6 +1664,7 @@ class GpuDecoder {
   GpuDecoder(const Code& code, int device, int max_slots);
   ~GpuDecoder();
   void decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t stream);
+  void stage_inputs(int32_t batch, const float* llr_host, const uint32_t* syn_host);
   void sample_device(double snr, double beta_lo, double beta_hi, double rate, uint64_t seed, int64_t first_frame,
                      int32_t n_frames, bool all_zero,
                      float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t stream);
@@ -1697,6 +1698,20 @@ class GpuDecoder {
   std::vector<cudaEvent_t> prof_ev;
   std::vector<int> prof_kid;
   Scratch s_llr, s_syn, s_bits, s_iters, s_reasons, s_post, s_qtrace;
+  // host-input staging (bpdec_decoder_stage_inputs): the H2D copy of a later
+  // batch runs on copy_stream while the current batch decodes
+  struct Staged {
+    const float* llr_host = nullptr;
+    const uint32_t* syn_host = nullptr;
+    int32_t batch = 0;
+    Scratch llr, syn;
+    cudaEvent_t done = nullptr;
+    bool valid = false;
+    int64_t seq = 0;
+  };
+  Staged staged[2];
+  int64_t stage_seq = 0;
+  cudaStream_t copy_stream = nullptr;
   int grid_check = 0, grid_var = 0, grid_syn = 0, sms_ = 148;
   int turn_item_blocks = 0, turn_check_blocks = 0;
 };
@@ -1919,6 +1934,8 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   CUDA_OK(cudaMemset(a.syn_target, 0, static_cast<size_t>(G) * M * sizeof(uint32_t)));
 
   CUDA_OK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  for (auto& sg : staged) CUDA_OK(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
   CUDA_OK(cudaHostAlloc(&h_counters, kRing * 4 * sizeof(int32_t), cudaHostAllocDefault));
   for (auto& e : ring_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
@@ -1966,6 +1983,9 @@ GpuDecoder::~GpuDecoder() {
     if (e) cudaEventDestroy(e);
   for (auto& e : prof_ev) cudaEventDestroy(e);
   if (h_counters) cudaFreeHost(h_counters);
+  for (auto& sg : staged)
+    if (sg.done) cudaEventDestroy(sg.done);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 
@@ -2055,16 +2075,29 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   a.q_mode = p.q_mode;
   a.clamp = p.msg_clamp;
 
-  // inputs
-  if (is_device_ptr(b.llr)) {
+  // inputs (a host batch staged earlier by stage_inputs is used in place:
+  // its copy already ran on copy_stream)
+  Staged* sg = nullptr;
+  if (!is_device_ptr(b.llr)) {
+    for (auto& c : staged)
+      if (c.valid && c.llr_host == b.llr && c.syn_host == b.syndrome && c.batch == b.batch &&
+          (sg == nullptr || c.seq < sg->seq))
+        sg = &c;
+  }
+  if (sg != nullptr) {
+    CUDA_OK(cudaStreamWaitEvent(st, sg->done, 0));
+    a.in_llr = static_cast<const float*>(sg->llr.ptr);
+    a.in_syn = b.syndrome ? static_cast<const uint32_t*>(sg->syn.ptr) : nullptr;
+    sg->valid = false;  // consumed; its buffers are free once this (synchronous) decode returns
+  } else if (is_device_ptr(b.llr)) {
     a.in_llr = b.llr;
   } else {
     float* d = static_cast<float*>(s_llr.get(B * a.N * sizeof(float)));
     CUDA_OK(cudaMemcpyAsync(d, b.llr, B * a.N * sizeof(float), cudaMemcpyHostToDevice, st));
     a.in_llr = d;
   }
-  a.in_syn = nullptr;
-  if (b.syndrome) {
+  if (sg == nullptr) a.in_syn = nullptr;
+  if (sg == nullptr && b.syndrome) {
     if (is_device_ptr(b.syndrome)) {
       a.in_syn = b.syndrome;
     } else {
@@ -2158,6 +2191,30 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   CUDA_OK(cudaStreamSynchronize(st));
 }
 
+void GpuDecoder::stage_inputs(int32_t batch, const float* llr_host, const uint32_t* syn_host) {
+  CUDA_OK(cudaSetDevice(device));
+  if (batch <= 0) throw ValidationError("stage_inputs: batch must be positive");
+  if (llr_host == nullptr) throw ValidationError("stage_inputs: null LLR pointer");
+  if (is_device_ptr(llr_host) || (syn_host && is_device_ptr(syn_host)))
+    throw ValidationError("stage_inputs: inputs must be host memory (device inputs need no staging)");
+  // the free slot, else the older staged batch is replaced
+  Staged* sg = !staged[0].valid ? &staged[0] : !staged[1].valid ? &staged[1]
+             : (staged[0].seq < staged[1].seq ? &staged[0] : &staged[1]);
+  const size_t B = static_cast<size_t>(batch);
+  float* dl = static_cast<float*>(sg->llr.get(B * base.N * sizeof(float)));
+  CUDA_OK(cudaMemcpyAsync(dl, llr_host, B * base.N * sizeof(float), cudaMemcpyHostToDevice, copy_stream));
+  if (syn_host) {
+    uint32_t* ds = static_cast<uint32_t*>(sg->syn.get(B * base.MW * sizeof(uint32_t)));
+    CUDA_OK(cudaMemcpyAsync(ds, syn_host, B * base.MW * sizeof(uint32_t), cudaMemcpyHostToDevice, copy_stream));
+  }
+  CUDA_OK(cudaEventRecord(sg->done, copy_stream));
+  sg->llr_host = llr_host;
+  sg->syn_host = syn_host;
+  sg->batch = batch;
+  sg->valid = true;
+  sg->seq = ++stage_seq;
+}
+
 void GpuDecoder::sample_device(double snr, double beta_lo, double beta_hi, double rate, uint64_t seed,
                                int64_t first_frame, int32_t n_frames, bool all_zero,
                                float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t st_in) {
@@ -2199,6 +2256,9 @@ void gpu_sample_frames_device(GpuDecoder* dec, double snr, double beta_lo, doubl
                               uint32_t* d_x_packed, void* stream) {
   dec->sample_device(snr, beta_lo, beta_hi, rate, seed, first_frame, n_frames, all_zero, d_llr, d_syndrome, d_x_packed,
                      static_cast<cudaStream_t>(stream));
+}
+void gpu_stage_inputs(GpuDecoder* dec, int32_t batch, const float* llr_host, const uint32_t* syn_host) {
+  dec->stage_inputs(batch, llr_host, syn_host);
 }
 void gpu_set_profiling(GpuDecoder* dec, bool enable) { dec->profiling = enable; }
 void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches, double* frame_iterations) {

@@ -38,6 +38,9 @@ void gpu_decode_batch(GpuDecoder* dec, const DecodeParams& p, const DecodeBuffer
 void gpu_sample_frames_device(GpuDecoder* dec, double snr, double beta_lo, double beta_hi, double rate,
                               uint64_t seed, int64_t first_frame, int32_t n_frames, bool all_zero, float* d_llr,
                               uint32_t* d_syndrome, uint32_t* d_x_packed, void* stream);
+// Asynchronous H2D of a host batch into one of two staging slots; a later
+// decode with the same host pointers and batch uses the staged copy.
+void gpu_stage_inputs(GpuDecoder* dec, int32_t batch, const float* llr_host, const uint32_t* syn_host);
 void gpu_set_profiling(GpuDecoder* dec, bool enable);
 void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches,
                  double* frame_iterations);

@@ -368,6 +368,18 @@ class BatchDecoder:
         return BatchResult(out["iterations"], out["reasons"], out.get("bits"), out.get("posteriors"),
                            out.get("q_trace"))
 
+    def stage_inputs(self, llr, syndrome=None):
+        """Starts the H2D copy of a host batch (pinned torch tensors for full
+        overlap) on the decoder's copy stream; a later decode_batch with the
+        same host buffers decodes from the staged copy
+        (bpdec_decoder_stage_inputs)."""
+        for arr, dt in ((llr, np.float32), (syndrome, np.uint32)):
+            if isinstance(arr, np.ndarray) and (arr.dtype != dt or not arr.flags["C_CONTIGUOUS"]):
+                raise ValidationError(f"stage_inputs: numpy inputs must be C-contiguous {np.dtype(dt).name} "
+                                      "(decode_batch would otherwise copy them)")
+        batch = int(llr.shape[0]) if llr.ndim > 1 else 1
+        _check(self._lib.bpdec_decoder_stage_inputs(self._h, batch, _ptr(llr), _ptr(syndrome)))
+
     def sample_frames_device(self, snr: float, seed: int, first_frame: int, n_frames: int, llr_dev,
                              syndrome_dev=None, x_packed_dev=None, all_zero: bool = False, stream: int = 0,
                              beta_range=None):

@@ -237,6 +237,39 @@ def test_packed_bits_and_device_buffers(P, cfg1_code):
             assert P.syndrome_check(cfg1_code, a.bits[f], s[f])
 
 
+def test_staged_host_inputs(P, cfg1_code):
+    """bpdec_decoder_stage_inputs: a staged host batch decodes exactly like an
+    unstaged one; staging overlaps the next batch's upload; a replaced stage
+    falls back to the normal copy; device inputs are rejected."""
+    import torch
+    dec = P.BatchDecoder(cfg1_code, max_slots=32)
+    snr = P.snr_for_beta(0.95, cfg1_code.rate())
+    cfg = P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    batches = []
+    for k in range(4):
+        llr, x, s = P.sample_frames(cfg1_code, snr, 41, 40 * k, 40)
+        hl = torch.from_numpy(llr).pin_memory()
+        hs = torch.from_numpy(s.view(np.int32)).pin_memory()
+        batches.append((hl, hs, dec.decode_batch(llr, cfg, syndrome=s, want_posteriors=True)))
+    # pipelined: stage k+1 before decoding k
+    dec.stage_inputs(batches[0][0], batches[0][1])
+    for k in range(4):
+        if k + 1 < 4:
+            dec.stage_inputs(batches[k + 1][0], batches[k + 1][1])
+        hl, hs, want = batches[k]
+        g = dec.decode_batch(hl, cfg, syndrome=hs, want_posteriors=True)
+        assert np.array_equal(g.bits, want.bits) and np.array_equal(g.iterations, want.iterations)
+        assert np.array_equal(g.posteriors, want.posteriors)
+    # three stages: the oldest is replaced, its decode copies again
+    for k in range(3):
+        dec.stage_inputs(batches[k][0], batches[k][1])
+    for k in range(3):
+        g = dec.decode_batch(batches[k][0], cfg, syndrome=batches[k][1])
+        assert np.array_equal(g.bits, batches[k][2].bits)
+    with pytest.raises(P.ValidationError):
+        dec.stage_inputs(batches[0][0].cuda(), None)
+
+
 def test_nonfinite_llr_rejected(P, cfg1_code):
     dec = P.BatchDecoder(cfg1_code, max_slots=32)
     llr = np.zeros((2, cfg1_code.n_vars), dtype=np.float32)
