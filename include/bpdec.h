@@ -213,7 +213,7 @@ typedef struct {
  * *count and *effective_rate returned. */
 int bpdec_code_apply_puncture(const bpdec_code* code, double target_rate, uint64_t seed,
                               int32_t* punctured_out, int32_t* count, double* effective_rate);
-/* ≙ wilson_interval (channel.hpp:63, channel.cpp:63-72) */
+/* ≙ wilson_interval (channel.hpp:64, channel.cpp:63-72) */
 int bpdec_wilson_interval(int64_t k, int64_t n, double* lo, double* hi);
 /* ≙ run_trials (channel.hpp:72-74, channel.cpp:74-156) on the GPU: trials
  * 0,1,2,... of the all-zero codeword at `snr` (sample_block draws, rounded to
