@@ -79,6 +79,7 @@ struct Args {
                             //  first hi edge, first degree-1 row, hi edge end}
   const int2* vtile;        // [n_tiles] {tile degree D (typed path) or -1 (generic), first slot in vedge_t}
   const int32_t* vedge_t;   // tile-padded CSC: per typed tile 64 x D edge ids, -1 = padding
+  int32_t ve_stride;        // k_var edge-id buffer size (32 x largest typed tile degree)
   const int32_t* vsched;    // [n_tiles] k_var hand-out order: generic tiles first, then by degree
   const int32_t* csched;    // [ceil(M/32)] k_check hand-out order: generic chunks first
   // state
@@ -694,62 +695,116 @@ __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
 // chunk0 + chunk1, each summed in variable order — an order fixed by the code
 // (not by slots, batch size or GPU count).
 constexpr int kVarRingRows = 40;   // per-warp ring of the variable kernel (rows of 128 B)
-constexpr int kVarStageRows = 12;  // rows per batch of the variable kernel
+constexpr int kVarStageRows = 13;  // target rows per batch of the variable kernel (degree 12 unsplit)
+constexpr int kVarMaxTyped = 32;   // largest tile degree on the typed (streamed) path
 
+// Batch shape of degree-D tiles.  D + 1 <= kVarStageRows: K whole variables
+// per batch (R = K(D+1) rows: K llr rows, then K*D c2v rows).  Larger D: one
+// variable spans SB batches of R rows (its llr row, then its c2v rows in
+// ascending check order); the posterior sum is carried across them in
+// order.
 template <int D>
 struct VarShape {
-  static constexpr int RPV = D + 1;
-  static constexpr int K =
-      kVarStageRows / RPV >= 8 ? 8 : (kVarStageRows / RPV >= 4 ? 4 : (kVarStageRows / RPV >= 2 ? 2 : 1));
-  static constexpr int ROWS = K * RPV;  // rows per batch
-  static constexpr int NS = kVarRingRows / ROWS >= 6 ? 6 : kVarRingRows / ROWS;  // ring stages
-  static_assert(NS >= 2, "variable degree too large for the ring");
-  static_assert(D <= 16, "chunk edge ids must fit the stage buffer");
+  static constexpr int RV = D + 1;  // rows per variable
+  static constexpr bool kSplit = RV > kVarStageRows;
+  static constexpr int K = kSplit ? 1
+                           : (kVarStageRows / RV >= 8 ? 8 : (kVarStageRows / RV >= 4 ? 4 : (kVarStageRows / RV >= 2 ? 2 : 1)));
+  static constexpr int SB = kSplit ? (RV + kVarStageRows - 1) / kVarStageRows : 1;  // batches per variable
+  static constexpr int ROWS = kSplit ? (RV + SB - 1) / SB : K * RV;                 // rows per batch
+  static constexpr int NS = kVarRingRows / ROWS >= 6 ? 6 : kVarRingRows / ROWS;     // ring stages
+  static constexpr int NB = 32 / K * SB;                                            // batches per chunk
+  static_assert(NS >= 2, "variable batch too large for the ring");
+  static_assert(D <= kVarMaxTyped, "typed variable path limited to degree 32");
 };
 
-// Batch b of a chunk: K variables; stage layout [K llr rows][K*D c2v rows].
-// Edge id -1 pads a variable of lower degree to the tile degree D, and
-// variables at or beyond `nval` pad the last tile: their copies are
-// predicated off, which zero-fills the stage rows (+0.0 leaves the ordered
-// sum unchanged).
+// Batch b of a chunk (variables i0 .. of the chunk).  Edge id -1 pads a
+// variable of lower degree to the tile degree D, and variables at or beyond
+// `nval` pad the last tile: their copies are predicated off, which
+// zero-fills the stage rows (+0.0 leaves the ordered sum unchanged).
 template <int D>
 __device__ __forceinline__ void var_batch_issue(float* stage, const float* llr0, const float* c2vg, const int32_t* ve,
-                                                int i0, int nval, int lrow, int lcol, bool qact, uint64_t pol) {
-  constexpr int K = VarShape<D>::K;
+                                                int b, int nval, int lrow, int lcol, bool qact, uint64_t pol) {
+  using S = VarShape<D>;
+  constexpr int K = S::K;
+  if constexpr (!S::kSplit) {
+    const int i0 = b * K;
 #pragma unroll
-  for (int r0 = 0; r0 < K; r0 += 4) {
-    const int r = r0 + lrow;
-    if (r < K)
-      cp_async16_ef(stage + r * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol,
-                    qact && i0 + r < nval, pol);
-  }
+    for (int r0 = 0; r0 < K; r0 += 4) {
+      const int r = r0 + lrow;
+      if (r < K)
+        cp_async16_ef(stage + r * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol,
+                      qact && i0 + r < nval, pol);
+    }
 #pragma unroll
-  for (int r0 = 0; r0 < K * D; r0 += 4) {
-    const int r = r0 + lrow;
-    if (r < K * D) {
-      const int e = ve[i0 * D + r];
-      cp_async16_ef(stage + (K + r) * kLanes + lcol,
-                    c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0)) * kLanes) + lcol, qact && e >= 0, pol);
+    for (int r0 = 0; r0 < K * D; r0 += 4) {
+      const int r = r0 + lrow;
+      if (r < K * D) {
+        const int e = ve[i0 * D + r];
+        cp_async16_ef(stage + (K + r) * kLanes + lcol,
+                      c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0)) * kLanes) + lcol, qact && e >= 0,
+                      pol);
+      }
+    }
+  } else {
+    const int i = b / S::SB;
+    const int g0 = (b - i * S::SB) * S::ROWS;  // first variable row of this batch
+#pragma unroll
+    for (int r0 = 0; r0 < S::ROWS; r0 += 4) {
+      const int r = r0 + lrow;
+      const int gr = g0 + r;
+      if (r < S::ROWS && gr < S::RV) {
+        const int e = gr > 0 ? ve[i * D + gr - 1] : 0;
+        const float* src = gr == 0 ? llr0 + static_cast<size_t>(i) * kLanes
+                                   : c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0)) * kLanes);
+        cp_async16_ef(stage + r * kLanes + lcol, src + lcol, qact && (gr == 0 ? i < nval : e >= 0), pol);
+      }
     }
   }
 }
 
 template <int D, int QMODE>
+__device__ __forceinline__ void var_finish(float p, float* postg, uint32_t* ebg, const int32_t* ve, int i, int nval,
+                                           int lane, bool act, double& acc, uint32_t& hw) {
+  const bool on = act && i < nval;
+  st_pred(postg + static_cast<size_t>(i) * kLanes, p, on);
+  if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+  const uint32_t word = __ballot_sync(0xffffffffu, on && p < 0.0f);
+  if (lane == (i & 31)) hw = word;
+#pragma unroll
+  for (int j0 = 0; j0 < D; j0 += 32) {
+    const int j = j0 + lane;
+    const int e = ve[i * D + (j < D ? j : 0)];
+    st_pred_u32(ebg + static_cast<uint32_t>(max(e, 0)), word, j < D && e >= 0);
+  }
+}
+
+template <int D, int QMODE>
 __device__ __forceinline__ void var_batch_compute(const float* stage, float* postg, uint32_t* ebg, const int32_t* ve,
-                                                  int i0, int nval, int lane, bool act, double& acc, uint32_t& hw) {
-  constexpr int K = VarShape<D>::K;
+                                                  int b, int nval, int lane, bool act, double& acc, uint32_t& hw,
+                                                  float& carry) {
+  using S = VarShape<D>;
+  constexpr int K = S::K;
+  if constexpr (!S::kSplit) {
+    const int i0 = b * K;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const bool on = act && i0 + k < nval;
-    float p = stage[k * kLanes];
+    for (int k = 0; k < K; ++k) {
+      float p = stage[k * kLanes];
 #pragma unroll
-    for (int j = 0; j < D; ++j) p += stage[(K + k * D + j) * kLanes];  // ascending check order (decoder.cpp:101)
-    st_pred(postg + static_cast<size_t>(i0 + k) * kLanes, p, on);
-    if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
-    const uint32_t word = __ballot_sync(0xffffffffu, on && p < 0.0f);
-    if (lane == ((i0 + k) & 31)) hw = word;
-    const int e = ve[(i0 + k) * D + (lane < D ? lane : 0)];
-    st_pred_u32(ebg + static_cast<uint32_t>(max(e, 0)), word, lane < D && e >= 0);
+      for (int j = 0; j < D; ++j) p += stage[(K + k * D + j) * kLanes];  // ascending check order (decoder.cpp:101)
+      var_finish<D, QMODE>(p, postg, ebg, ve, i0 + k, nval, lane, act, acc, hw);
+    }
+  } else {
+    const int i = b / S::SB;
+    const int sub = b - i * S::SB;
+    const int n = min(S::ROWS, S::RV - sub * S::ROWS);  // rows of this batch
+    float p = sub == 0 ? stage[0] : carry + stage[0];
+#pragma unroll
+    for (int j = 1; j < S::ROWS; ++j)
+      if (j < n) p += stage[j * kLanes];  // ascending check order (decoder.cpp:101)
+    if (sub == S::SB - 1)
+      var_finish<D, QMODE>(p, postg, ebg, ve, i, nval, lane, act, acc, hw);
+    else
+      carry = p;
   }
 }
 
@@ -820,12 +875,13 @@ __device__ __forceinline__ VarChunk var_chunk(const Args& a, const VarTile& t, i
 // Runs this warp's degree-D tiles (starting with grabbed tile w) as one
 // pipeline over their chunks; returns the next grabbed tile it did not take.
 template <int D, int QMODE>
-__device__ long long var_stream(const Args& a, long long w, long long total, int32_t (*sve)[32 * 16], float* ring,
-                                int lane) {
-  constexpr int K = VarShape<D>::K;
+__device__ long long var_stream(const Args& a, long long w, long long total, int32_t* sve0, int32_t* sve1,
+                                float* ring, int lane) {
   constexpr int NS = VarShape<D>::NS;
-  constexpr int NB = 32 / K;  // batches per chunk
+  constexpr int NB = VarShape<D>::NB;  // batches per chunk
   constexpr int RS = VarShape<D>::ROWS * kLanes;  // stage stride
+  int32_t* ve_c = sve0;  // edge ids of cur
+  int32_t* ve_n = sve1;  // edge ids of nxt
   static_assert(NB >= 2 * NS - 1, "the next chunk's edge ids must land before its first batch is issued");
   const int lrow = lane >> 3;
   const int lcol = (lane & 7) * 4;
@@ -837,8 +893,7 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
   long long w_after = total;  // the tile grabbed after the current one
   int2 desc_after = make_int2(-1, 0);
   int kpend = var_grab_issue(a, lane);  // grabbed one chunk ahead of its use
-  int wb = 0;  // edge-id buffer of cur
-  var_stage_ve<D>(sve[wb], a.vedge_t, cur.kb, lane);
+  var_stage_ve<D>(ve_c, a.vedge_t, cur.kb, lane);
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
@@ -857,7 +912,7 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
     const bool in_cur = pos < NB;
     if (in_cur || has_nxt) {
       var_batch_issue<D>(ring + slot_issue * RS, in_cur ? llr_c : llr_n, in_cur ? c2v_c : c2v_n,
-                         in_cur ? sve[wb] : sve[wb ^ 1], (in_cur ? pos : pos - NB) * K, in_cur ? nval_c : nval_n, lrow,
+                         in_cur ? ve_c : ve_n, in_cur ? pos : pos - NB, in_cur ? nval_c : nval_n, lrow,
                          lcol, in_cur ? qact_c : qact_n, pol);
     }
     cp_async_commit();
@@ -884,7 +939,7 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
       }
     }
     if (has_nxt) {
-      var_stage_ve<D>(sve[wb ^ 1], a.vedge_t, nxt.kb, lane);  // travels with this step's group
+      var_stage_ve<D>(ve_n, a.vedge_t, nxt.kb, lane);  // travels with this step's group
       llr_n = nxt.llr0;
       c2v_n = nxt.c2v0;
       nval_n = nxt.nval;
@@ -896,13 +951,14 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
     uint32_t* ebg = a.ebits + static_cast<size_t>(cur.g) * a.EH;
     double acc = 0.0;
     uint32_t hw = 0u;
+    float carry = 0.0f;  // posterior partial of a variable split over batches
 #pragma unroll 1
     for (int b = 0; b < NB; ++b) {
       issue_at(b + NS - 1);
       cp_async_wait<NS - 1>();
       __syncwarp();  // rows (and the next chunk's edge ids) were copied by other lanes
-      var_batch_compute<D, QMODE>(ring + lane + slot_comp * RS, postg, ebg, sve[wb], b * K, cur.nval, lane, act,
-                                  acc, hw);
+      var_batch_compute<D, QMODE>(ring + lane + slot_comp * RS, postg, ebg, ve_c, b, cur.nval, lane, act, acc, hw,
+                                  carry);
       if (++slot_comp == NS) slot_comp = 0;
       __syncwarp();  // stage is refilled in the next round
     }
@@ -918,7 +974,9 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
     c2v_c = c2v_n;
     nval_c = nval_n;
     qact_c = qact_n;
-    wb ^= 1;
+    int32_t* t = ve_c;
+    ve_c = ve_n;
+    ve_n = t;
   }
   cp_async_wait<0>();
   __syncwarp();
@@ -983,22 +1041,32 @@ __device__ void var_tile_generic(const Args& a, long long w, int32_t* sptr, int 
   a.q_part[(static_cast<size_t>(t.g) * a.n_tiles + t.tile) * kLanes + lane] = acc0 + acc;
 }
 
+// Dynamic shared memory per warp: ring (kVarRingRows rows), two edge-id
+// buffers of a.ve_stride ints (32 x the largest typed tile degree), vptr
+// staging for generic tiles.
+__host__ __device__ constexpr size_t var_smem_per_warp(int ve_stride) {
+  return static_cast<size_t>(kVarRingRows) * kLanes * 4 + 2 * static_cast<size_t>(ve_stride) * 4 + 36 * 4;
+}
+
 template <int QMODE>
-__global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
-  __shared__ int32_t s_ve[kVarWarps][2][32 * 16];
-  __shared__ int32_t s_ptr[kVarWarps][33];
-  __shared__ __align__(16) float s_ring[kVarWarps][kVarRingRows * kLanes];
+__global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {  // 5 blocks/SM: measured best
+  extern __shared__ __align__(16) unsigned char var_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  unsigned char* base = var_smem + var_smem_per_warp(a.ve_stride) * warp;
+  float* ring = reinterpret_cast<float*>(base);
+  int32_t* sve0 = reinterpret_cast<int32_t*>(base + kVarRingRows * kLanes * 4);
+  int32_t* sve1 = sve0 + a.ve_stride;
+  int32_t* sptr = sve1 + a.ve_stride;
   const long long total = static_cast<long long>(a.G) * a.n_tiles;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[7] = 0;  // k_check chunk scheduler (next step)
   long long w = var_grab(a, lane);
   while (w < total) {
     const int d = __ldg(&a.vtile[static_cast<int>(w % a.n_tiles)]).x;
     switch (d) {
-#define BPDEC_VSTREAM(D_)                                                   \
-  case D_:                                                                  \
-    w = var_stream<D_, QMODE>(a, w, total, s_ve[warp], s_ring[warp], lane); \
+#define BPDEC_VSTREAM(D_)                                                     \
+  case D_:                                                                    \
+    w = var_stream<D_, QMODE>(a, w, total, sve0, sve1, ring, lane);           \
     continue;
       BPDEC_VSTREAM(2)
       BPDEC_VSTREAM(3)
@@ -1007,11 +1075,14 @@ __global__ void __launch_bounds__(kVarWarps * 32) k_var(const Args a) {
       BPDEC_VSTREAM(8)
       BPDEC_VSTREAM(12)
       BPDEC_VSTREAM(16)
+      BPDEC_VSTREAM(20)
+      BPDEC_VSTREAM(24)
+      BPDEC_VSTREAM(32)
 #undef BPDEC_VSTREAM
       default:
         break;
     }
-    var_tile_generic<QMODE>(a, w, s_ptr[warp], lane);
+    var_tile_generic<QMODE>(a, w, sptr, lane);
     w = var_grab(a, lane);
   }
 }
@@ -1714,6 +1785,7 @@ class GpuDecoder {
   cudaStream_t copy_stream = nullptr;
   int grid_check = 0, grid_var = 0, grid_syn = 0, sms_ = 148;
   int turn_item_blocks = 0, turn_check_blocks = 0;
+  size_t var_smem = 0;
 };
 
 GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
@@ -1842,7 +1914,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
     int32_t dmax = 0;
     for (int32_t h = h0; h < h1; ++h) dmax = std::max(dmax, vptr[h + 1] - vptr[h]);
     int32_t D = -1;
-    for (int32_t d : {2, 3, 4, 6, 8, 12, 16})
+    for (int32_t d : {2, 3, 4, 6, 8, 12, 16, 20, 24, 32})
       if (D < 0 && dmax <= d) D = d;
     vtile[t] = make_int2(D, D < 0 ? vptr[std::min(h0, NV)] : static_cast<int32_t>(vedge_t.size()));
     if (D < 0) continue;
@@ -1854,6 +1926,8 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
       for (; k < D; ++k) vedge_t.push_back(-1);
     }
   }
+  int32_t dmax_typed = 2;
+  for (int32_t t = 0; t < n_tiles; ++t) dmax_typed = std::max(dmax_typed, vtile[t].x);
   // keep 16-byte alignment of every tile slice (cp.async 16)
   for (int32_t t = 0; t < n_tiles; ++t)
     if (vtile[t].x >= 0 && (vtile[t].y & 3) != 0) throw CudaError("decoder: internal layout error (vedge_t alignment)");
@@ -1895,6 +1969,8 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.vtile = up(vtile, static_cast<int2*>(nullptr));
   a.vsched = up(vsched, static_cast<int32_t*>(nullptr));
   a.vedge_t = up(vedge_t, static_cast<int32_t*>(nullptr));
+  a.ve_stride = 32 * dmax_typed;
+  var_smem = kVarWarps * var_smem_per_warp(a.ve_stride);
   d_check_ptr = up(code.check_ptr, static_cast<int32_t*>(nullptr));
   d_check_vars = up(code.check_vars, static_cast<int32_t*>(nullptr));
 
@@ -1966,7 +2042,9 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   {
     // k_var warps run persistent, dynamically scheduled tile streams: one wave
     int per_sm = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_var<1>, kVarWarps * 32, 0));
+    CUDA_OK(cudaFuncSetAttribute(k_var<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(var_smem)));
+    CUDA_OK(cudaFuncSetAttribute(k_var<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(var_smem)));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_var<1>, kVarWarps * 32, var_smem));
     grid_var = sms * std::max(1, per_sm);
   }
   grid_syn = sms * 8;
@@ -2039,9 +2117,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
   });
   launch(kVar, st, [&] {
     if (a.q_mode == 0)
-      k_var<0><<<grid_var, kVarWarps * 32, 0, st>>>(a);
+      k_var<0><<<grid_var, kVarWarps * 32, var_smem, st>>>(a);
     else
-      k_var<1><<<grid_var, kVarWarps * 32, 0, st>>>(a);
+      k_var<1><<<grid_var, kVarWarps * 32, var_smem, st>>>(a);
   });
   if (a.use_pce)
     launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 2 * G * sizeof(uint32_t), st>>>(a); });
