@@ -200,6 +200,32 @@ def test_irregular_edge_cases(P, ref):
         compare(g, r, tie, label=f"irregular pce={pce} vnr={vnr}")
 
 
+def test_high_degree_variables(P, ref):
+    """Variable degrees 14 / 20 / 27 (typed variable path, each variable split
+    over several batches, tiles padded to degree 16 / 20 / 32), 36 (generic
+    path) and mixed-degree boundary tiles, next to degree-3 and degree-1
+    variables."""
+    rng = np.random.default_rng(11)
+    classes = [(3, 100), (14, 128), (20, 128), (27, 64), (36, 64)]
+    degs = np.concatenate([np.full(n, d) for d, n in classes])
+    n_hi = len(degs)
+    m = 1400
+    lists = [set() for _ in range(m)]
+    for v, d in enumerate(degs):
+        for c in rng.choice(m, size=int(d), replace=False):
+            lists[int(c)].add(v)
+    # one degree-1 variable per check (identity block, as in the BASELINE codes)
+    lists = [sorted(c) + [n_hi + j] for j, c in enumerate(lists)]
+    code = P.ParityCheckMatrix.from_check_lists(n_hi + m, lists)
+    dec = P.BatchDecoder(code, max_slots=32)
+    llr = rng.normal(0.9, 1.4, size=(24, code.n_vars)).astype(np.float32)
+    rc = _refcode(ref, code)
+    for pce, vnr in ET_MODES.values():
+        r, tie = ref_ties(rc, llr, d_max=40, use_pce=pce, use_vnr=vnr, threads=8)
+        g = dec.decode_batch(llr, P.DecodeConfig(d_max=40, use_pce=pce, use_vnr=vnr), want_posteriors=True)
+        compare(g, r, tie, label=f"high-degree pce={pce} vnr={vnr}")
+
+
 def test_dmax_one_and_batch_shapes(P, ref, cfg1_code):
     """d_max = 1, B = 1, B not a multiple of 32, B > slots (frames stream
     through recycled slots)."""
