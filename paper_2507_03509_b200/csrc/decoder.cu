@@ -175,6 +175,16 @@ __device__ __forceinline__ void st_pred_u32(uint32_t* p, uint32_t v, bool pred) 
                : "memory");
 }
 
+// Programmatic dependent launch: the step kernels are launched with
+// programmatic stream serialisation, so a kernel's blocks can be scheduled
+// while its predecessor drains; every kernel waits for the predecessor's
+// completion (and memory) before its first global access, then lets its own
+// successor launch.  No-ops when launched without the attribute.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // Advances a grid-stride cursor past the remainder of an inactive group.
 __device__ __forceinline__ long long skip_group(long long w, long long per_group, long long stride) {
   const long long next = (w / per_group + 1) * per_group;
@@ -581,6 +591,7 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
 
 template <int MAXD, bool WANT_POST>
 __global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
+  pdl_begin();
   constexpr bool kStage = MAXD <= 16;
   constexpr int kHH = kStage ? 32 * MAXD : 1;
   __shared__ int4 s_desc[kCheckThreads / 32][32];
@@ -1049,7 +1060,8 @@ __host__ __device__ constexpr size_t var_smem_per_warp(int ve_stride) {
 }
 
 template <int QMODE>
-__global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {  // 5 blocks/SM: measured best
+__global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {
+  pdl_begin();  // 5 blocks/SM: measured best
   extern __shared__ __align__(16) unsigned char var_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -1107,6 +1119,7 @@ __device__ __forceinline__ uint32_t ldu32_pred(const uint32_t* p, bool pred) {
 constexpr int kSynChunks = 4;  // chunks per warp pass (their loads are in flight together)
 
 __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
+  pdl_begin();
   // group state cached per block: active masks (constant during the pass)
   // and the failing frames known so far (global at block start | this block)
   extern __shared__ uint32_t s_grp[];  // [2][G]: active, fail
@@ -1189,6 +1202,7 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
 // then VNR (k >= 2, strict), then d_max (decoder.cpp:114-123).  It rewrites
 // stopped[g] / load_mask[g] for k_turnover (no separate clear).
 __global__ void __launch_bounds__(kTermThreads) k_terminate(const Args a) {
+  pdl_begin();
   constexpr int kW = kTermThreads / 32;
   __shared__ double red[kW][kLanes];
   __shared__ int s_last;
@@ -1360,6 +1374,7 @@ __device__ __forceinline__ void extract_chunk(const Args& a, int ch, int lane) {
 
 template <bool WANT_POST>
 __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_blocks, int check_blocks) {
+  pdl_begin();
   __shared__ float tile[kTurnChunks][32][33];
   uint32_t any_stop = 0u, any_load = 0u;
   for (int g = 0; g < a.G; ++g) {
@@ -1555,6 +1570,7 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
 // read and write — and the last block to finish commits the slot state
 // (counters[5] counts finished blocks).
 __global__ void __launch_bounds__(kThreads) k_compact(const Args a) {
+  pdl_begin();
   __shared__ CompactPlan pl;
   __shared__ int cnt[kMaxCompactGroups];
   __shared__ int s_last;
@@ -1707,6 +1723,26 @@ bool is_device_ptr(const void* p) {
     return false;
   }
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// Kernel launch with programmatic stream serialisation (see pdl_begin).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+#ifdef BPDEC_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#endif
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 // Device scratch that grows on demand.
@@ -2091,9 +2127,9 @@ void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
 void GpuDecoder::launch_turnover(const Args& a, cudaStream_t st, bool want_post) {
   const int grid = turn_item_blocks + turn_check_blocks + 1;
   if (want_post)
-    k_turnover<true><<<grid, kThreads, 0, st>>>(a, turn_item_blocks, turn_check_blocks);
+    launch_pdl(k_turnover<true>, grid, kThreads, 0, st, a, turn_item_blocks, turn_check_blocks);
   else
-    k_turnover<false><<<grid, kThreads, 0, st>>>(a, turn_item_blocks, turn_check_blocks);
+    launch_pdl(k_turnover<false>, grid, kThreads, 0, st, a, turn_item_blocks, turn_check_blocks);
 }
 
 void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
@@ -2102,9 +2138,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
 #define BPDEC_CHECK_CASE(D)                                                                 \
   if (md <= D) {                                                                            \
     if (want_post)                                                                          \
-      k_check<D, true><<<grid_check, kCheckThreads, 0, st>>>(a);                                 \
+      launch_pdl(k_check<D, true>, grid_check, kCheckThreads, 0, st, a);                         \
     else                                                                                    \
-      k_check<D, false><<<grid_check, kCheckThreads, 0, st>>>(a);                                \
+      launch_pdl(k_check<D, false>, grid_check, kCheckThreads, 0, st, a);                        \
     return;                                                                                 \
   }
     BPDEC_CHECK_CASE(3)
@@ -2117,17 +2153,17 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
   });
   launch(kVar, st, [&] {
     if (a.q_mode == 0)
-      k_var<0><<<grid_var, kVarWarps * 32, var_smem, st>>>(a);
+      launch_pdl(k_var<0>, grid_var, kVarWarps * 32, var_smem, st, a);
     else
-      k_var<1><<<grid_var, kVarWarps * 32, var_smem, st>>>(a);
+      launch_pdl(k_var<1>, grid_var, kVarWarps * 32, var_smem, st, a);
   });
   if (a.use_pce)
-    launch(kSyn, st, [&] { k_syndrome<<<grid_syn, kThreads, 2 * G * sizeof(uint32_t), st>>>(a); });
-  launch(kTerm, st, [&] { k_terminate<<<G * kTermBlocks, kTermThreads, 0, st>>>(a); });
+    launch(kSyn, st, [&] { launch_pdl(k_syndrome, grid_syn, kThreads, 2 * G * sizeof(uint32_t), st, a); });
+  launch(kTerm, st, [&] { launch_pdl(k_terminate, G * kTermBlocks, kTermThreads, 0, st, a); });
   launch(kTurnover, st, [&] { launch_turnover(a, st, want_post); });
   // tail compaction (no-op unless the queue is drained and live frames fit
   // in fewer groups; decided on the device, no host round trip)
-  if (G > 1 && G <= kMaxCompactGroups) launch(kCompact, st, [&] { k_compact<<<sms_ * 4, kThreads, 0, st>>>(a); });
+  if (G > 1 && G <= kMaxCompactGroups) launch(kCompact, st, [&] { launch_pdl(k_compact, sms_ * 4, kThreads, 0, st, a); });
 }
 
 void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t st_in) {
