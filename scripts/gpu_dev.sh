@@ -1,5 +1,6 @@
 #!/bin/bash
-# tests (non full-size) + probe + cfg2/cfg3 bench lines + launch list
+# Development pass on the GPU box: GPU tests (without the full-size ones),
+# config-2 perf probe, config-2 and config-3 bench lines, launch list.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 bash scripts/gpu_quick.sh
