@@ -61,14 +61,16 @@ def main():
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu.json"), "w") as f:
         json.dump(res, f, indent=1)
     lines = [f"# ncu summary `{tag}`", "", f"source report: `{os.path.basename(rep)}` (ncu --set full --clock-control none)", ""]
-    lines.append("| kernel | time | DRAM R+W | DRAM % peak | issue active % | L2 hit % | regs | top stalls |")
+    lines.append("| kernel | time | DRAM R+W | DRAM GB/s (R+W / time) | issue active % | L2 hit % | regs | top stalls |")
     lines.append("|---|---|---|---|---|---|---|---|")
     for d in res:
         k = d["kernel"].split("(")[0].replace("void bpdec::<unnamed>::", "")
         t = d.get("gpu__time_duration.sum", {})
         rb = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
+        tv = float(t.get("value", "nan"))
+        ts = tv * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "second": 1.0}.get(t.get("unit", ""), float("nan"))
         lines.append(f"| `{k}` | {t.get('value')} {t.get('unit')} | {rb / 1e6:.1f} MB | "
-                     f"{d.get('dram__throughput.avg.pct_of_peak_sustained_elapsed', {}).get('value')} | "
+                     f"{rb / ts / 1e9:.0f} | "
                      f"{d.get('smsp__issue_active.avg.pct_of_peak_sustained_active', {}).get('value')} | "
                      f"{d.get('lts__t_sector_hit_rate.pct', {}).get('value')} | "
                      f"{d.get('launch__registers_per_thread', {}).get('value')} | "
