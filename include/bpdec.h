@@ -227,8 +227,9 @@ int bpdec_run_trials(bpdec_decoder* dec, double snr, const int32_t* punctured, i
 
 /* Per-kernel timing of the most recent bpdec_decode_batch calls (CUDA events
  * on the launching stream).  Enable before decoding; kernel ids:
- * 0 check-node, 1 variable-node, 2 syndrome, 3 termination, 4 turnover (outputs of
- * stopped frames + loading of queued frames), 5 tail compaction. */
+ * 0 check-node, 1 variable-node, 2 decide (syndrome + q^(k) + stop decision),
+ * 3 unused (termination is part of 2), 4 turnover (outputs of stopped frames +
+ * loading of queued frames), 5 tail compaction. */
 int bpdec_decoder_set_profiling(bpdec_decoder* dec, int32_t enable);
 int bpdec_decoder_profile(const bpdec_decoder* dec, int32_t kernel, double* total_ms,
                           int64_t* launches, double* frame_iterations);

@@ -20,9 +20,9 @@
 //               hard bits and the degree-1 part of the syndrome
 //   k_var       variable-node update (decoder.cpp:99-105) for degree>=2
 //               variables, hard bits, per-tile q partial sums (:32-36, :107)
-//   k_syndrome  bit-sliced parity of every check vs the target syndrome
-//               (decoder.cpp:19-30), 32 frames per 32-bit word
-//   k_terminate PCE -> VNR -> d_max decision per frame (decoder.cpp:114-123)
+//   k_decide    bit-sliced parity of every check vs the target syndrome
+//               (decoder.cpp:19-30), the fixed-order q^(k) reduction, and
+//               the PCE -> VNR -> d_max decision per frame (:114-123)
 //   k_turnover  outputs of frames that stopped this step (:126-128) and
 //               the next queued frames streamed into the freed slots
 //   k_compact   tail compaction of the live frames into fewer groups
@@ -61,8 +61,8 @@ constexpr int kQTile = 64;     // variables per k_var tile and q partial sum (co
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
 enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompact = 5, kNumKernels = 6 };
-constexpr int kTermBlocks = 16;   // k_terminate blocks per group (q partial tree: fixed by the code)
-constexpr int kTermThreads = 256;
+// (kSyn = k_decide; kTerm is kept for the profiling ABI and stays 0)
+constexpr int kTermBlocks = 16;   // k_decide q-reduction blocks per group (q partial tree: fixed by the code)
 
 // ------------------------------------------------------------ arguments --
 struct Args {
@@ -96,7 +96,6 @@ struct Args {
   uint32_t* syn_target;     // [G][M]
   double* q_part;           // [G][n_tiles][32]
   double* q_mid;            // [G][kTermBlocks][32]
-  int32_t* term_cnt;        // [G] k_terminate blocks done (last block decides)
   int32_t* stop_frame;      // [S] frame that stopped in the slot this step (read by k_turnover)
   double* qprev;            // [S]
   int32_t* slot_iter;       // [S] iteration the slot runs next (1-based)
@@ -108,7 +107,8 @@ struct Args {
   uint32_t* load_mask;      // [G]
   int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots,
                             // [4] active slots at the last compaction, [5] k_compact blocks done,
-                            // [6] k_var tiles handed out, [7] k_check chunks handed out
+                            // [6] k_var tiles handed out, [7] k_check chunks handed out,
+                            // [8] k_decide blocks done
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {
   }
 }
 
-// ---------------------------------------------------------- k_syndrome --
+// ------------------------------------------------- k_decide: syndrome part --
 // Warp = 32 consecutive (device-order) checks, lane = check, all groups.
 // Parity of a check = target syndrome ^ degree-1 part (synp, from k_check)
 // ^ the hard-decision words of its degree>=2 edges, which k_var stored per
@@ -1118,11 +1118,10 @@ __device__ __forceinline__ uint32_t ldu32_pred(const uint32_t* p, bool pred) {
 
 constexpr int kSynChunks = 4;  // chunks per warp pass (their loads are in flight together)
 
-__global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
-  pdl_begin();
+// Syndrome part of k_decide: block `b` of `nb` syndrome blocks.
+__device__ __forceinline__ void syndrome_block(const Args& a, int b, int nb, uint32_t* s_grp) {
   // group state cached per block: active masks (constant during the pass)
   // and the failing frames known so far (global at block start | this block)
-  extern __shared__ uint32_t s_grp[];  // [2][G]: active, fail
   uint32_t* s_act = s_grp;
   uint32_t* s_fail = s_grp + a.G;
   for (int t = threadIdx.x; t < a.G; t += blockDim.x) {
@@ -1133,16 +1132,15 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
   const int lane = threadIdx.x & 31;
   const int chunks = (a.M + 31) / 32;
   const int passes = (chunks + kSynChunks - 1) / kSynChunks;
-  const int nwarps = static_cast<int>((static_cast<long long>(gridDim.x) * blockDim.x) >> 5);
-  for (int q = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); q < passes;
-       q += nwarps) {
+  const int nwarps = nb * static_cast<int>(blockDim.x >> 5);
+  for (int q = b * static_cast<int>(blockDim.x >> 5) + static_cast<int>(threadIdx.x >> 5); q < passes; q += nwarps) {
     bool live = false;  // any group with an active frame not yet known to fail (lanes scan groups)
     for (int g0 = 0; g0 < a.G && !live; g0 += 32) {
       const int g = g0 + lane;
       live = __any_sync(0xffffffffu, g < a.G && s_act[g] != 0u && (s_fail[g] & s_act[g]) != s_act[g]);
     }
     if (!live) continue;  // warp-uniform
-    int e0[kSynChunks], nh[kSynChunks], fixed[kSynChunks];
+    int e0[kSynChunks], nh[kSynChunks];
     bool valid[kSynChunks];
 #pragma unroll
     for (int u = 0; u < kSynChunks; ++u) {
@@ -1153,12 +1151,10 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
       if (cdk.x >= 0) {  // homogeneous chunk: NH hi edges per check, contiguous
         nh[u] = cdk.x >> 3;
         e0[u] = cdk.y + lane * nh[u];
-        fixed[u] = 1;
       } else {
         const int4 d = valid[u] ? __ldg(&a.cdesc[c]) : make_int4(0, 0, 0, 0);
         e0[u] = d.x;
         nh[u] = d.y - d.x;
-        fixed[u] = 0;
       }
       if (!valid[u]) nh[u] = 0;
     }
@@ -1180,7 +1176,6 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
 #pragma unroll
       for (int u = 0; u < kSynChunks; ++u) {
         for (int j = 4; j < nh[u]; ++j) word[u] ^= eb[e0[u] + j];  // checks with more than 4 such edges
-        (void)fixed[u];
         any |= word[u];
       }
       any = __reduce_or_sync(0xffffffffu, any & amask);
@@ -1194,30 +1189,13 @@ __global__ void __launch_bounds__(kThreads) k_syndrome(const Args a) {
   }
 }
 
-// --------------------------------------------------------- k_terminate --
-// kTermBlocks blocks per group.  q^(k) = fixed-order double sum of the k_var
-// tile partials: block p sums its tile range (warps interleaved, then the 8
-// warp sums in order), the last block of the group to finish adds the block
-// sums in order and takes the decision for every slot of the group: PCE,
-// then VNR (k >= 2, strict), then d_max (decoder.cpp:114-123).  It rewrites
-// stopped[g] / load_mask[g] for k_turnover (no separate clear).
-__global__ void __launch_bounds__(kTermThreads) k_terminate(const Args a) {
-  pdl_begin();
-  constexpr int kW = kTermThreads / 32;
-  __shared__ double red[kW][kLanes];
-  __shared__ int s_last;
-  const int g = blockIdx.x / kTermBlocks;
-  const int p = blockIdx.x - g * kTermBlocks;
+// q part of k_decide: block p of group g sums its range of the k_var tile
+// partials (warps interleaved, then the warp sums in order) into q_mid.
+__device__ __forceinline__ void q_block(const Args& a, int g, int p, double (*red)[kLanes]) {
+  constexpr int kW = kThreads / 32;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const uint32_t amask = a.group_active[g];
-  if (amask == 0u) {
-    if (p == 0 && threadIdx.x == 0) {
-      a.stopped[g] = 0u;
-      a.load_mask[g] = 0u;
-    }
-    return;
-  }
+  if (a.group_active[g] == 0u) return;  // block-uniform
   const int t_lo = static_cast<int>(static_cast<long long>(a.n_tiles) * p / kTermBlocks);
   const int t_hi = static_cast<int>(static_cast<long long>(a.n_tiles) * (p + 1) / kTermBlocks);
   const double* qp = a.q_part + static_cast<size_t>(g) * a.n_tiles * kLanes + lane;
@@ -1241,25 +1219,29 @@ __global__ void __launch_bounds__(kTermThreads) k_terminate(const Args a) {
 #pragma unroll
     for (int k = 1; k < kW; ++k) q += red[k][lane];
     a.q_mid[(static_cast<size_t>(g) * kTermBlocks + p) * kLanes + lane] = q;
-    __threadfence();
-    int last = 0;
-    if (lane == 0) last = atomicAdd(&a.term_cnt[g], 1) == kTermBlocks - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    s_last = last;
   }
-  __syncthreads();
-  if (!s_last || warp != 0) return;
-  __threadfence();
+}
+
+// Decision for every slot of group g (one warp): q^(k) = the block sums in
+// order; PCE, then VNR (k >= 2, strict), then d_max (decoder.cpp:114-123);
+// stopping slots take the next queued frames.  Rewrites stopped[g] /
+// load_mask[g] for k_turnover.
+__device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
+  const uint32_t amask = a.group_active[g];
+  if (amask == 0u) {
+    if (lane == 0) {
+      a.stopped[g] = 0u;
+      a.load_mask[g] = 0u;
+    }
+    return;
+  }
   double v[kTermBlocks];
 #pragma unroll
   for (int k = 0; k < kTermBlocks; ++k) v[k] = __ldcg(&a.q_mid[(static_cast<size_t>(g) * kTermBlocks + k) * kLanes + lane]);
-  q = v[0];
+  double q = v[0];
 #pragma unroll
   for (int k = 1; k < kTermBlocks; ++k) q += v[k];
-  if (lane == 0) {
-    a.term_cnt[g] = 0;
-    atomicAdd(a.frame_iters, static_cast<unsigned long long>(__popc(amask)));
-  }
+  if (lane == 0) atomicAdd(a.frame_iters, static_cast<unsigned long long>(__popc(amask)));
   const uint32_t bit = 1u << lane;
   const bool act = (amask & bit) != 0u;
   const int s = g * kLanes + lane;
@@ -1268,7 +1250,7 @@ __global__ void __launch_bounds__(kTermThreads) k_terminate(const Args a) {
     it = a.slot_iter[s];
     f = a.slot_frame[s];
     if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (it - 1)] = q;
-    if (a.use_pce && !(a.fail[g] & bit)) {
+    if (a.use_pce && !(__ldcg(&a.fail[g]) & bit)) {
       reason = 0;
     } else if (a.use_vnr && it >= 2 && q < a.qprev[s]) {
       reason = 1;
@@ -1303,6 +1285,39 @@ __global__ void __launch_bounds__(kTermThreads) k_terminate(const Args a) {
     a.stopped[g] = stop;
     a.load_mask[g] = load;
   }
+}
+
+// ------------------------------------------------------------ k_decide --
+// Syndrome, q^(k) and the stop decision of a step in one launch.  Blocks
+// [0, syn_blocks): bit-sliced parity of every check vs its target
+// (decoder.cpp:19-30), streaming synp and the check's contiguous ebits,
+// OR-reduced fail masks; a group is skipped once every active frame in it is
+// known to fail.  Blocks [syn_blocks, syn_blocks + G*kTermBlocks): the fixed
+// -order q partial tree.  The last block to finish (counters[8]) takes the
+// decisions for all groups, one warp per group.
+__global__ void __launch_bounds__(kThreads) k_decide(const Args a, int syn_blocks) {
+  pdl_begin();
+  extern __shared__ uint32_t s_grp[];  // [2][G] (syndrome blocks)
+  __shared__ double red[kThreads / 32][kLanes];
+  __shared__ int s_last;
+  const int b = blockIdx.x;
+  if (b < syn_blocks) {
+    syndrome_block(a, b, syn_blocks, s_grp);
+  } else {
+    const int qb = b - syn_blocks;
+    q_block(a, qb / kTermBlocks, qb - (qb / kTermBlocks) * kTermBlocks, red);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.counters[8], 1) == static_cast<int>(gridDim.x) - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31;
+  for (int g = static_cast<int>(threadIdx.x >> 5); g < a.G; g += kThreads / 32) decide_group(a, g, lane);
+  if (threadIdx.x == 0) a.counters[8] = 0;
 }
 
 // ---------------------------------------------------------- k_turnover --
@@ -2027,9 +2042,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.syn_target = own(dalloc<uint32_t>(static_cast<size_t>(G) * M, &dev_bytes));
   a.q_part = own(dalloc<double>(static_cast<size_t>(G) * a.n_tiles * L, &dev_bytes));
   a.q_mid = own(dalloc<double>(static_cast<size_t>(G) * kTermBlocks * L, &dev_bytes));
-  a.term_cnt = own(dalloc<int32_t>(G, &dev_bytes));
   a.stop_frame = own(dalloc<int32_t>(S, &dev_bytes));
-  CUDA_OK(cudaMemset(a.term_cnt, 0, G * sizeof(int32_t)));
   a.qprev = own(dalloc<double>(S, &dev_bytes));
   a.slot_iter = own(dalloc<int32_t>(S, &dev_bytes));
   a.slot_frame = own(dalloc<int32_t>(S, &dev_bytes));
@@ -2038,7 +2051,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   a.fail = own(dalloc<uint32_t>(G, &dev_bytes));
   a.stopped = own(dalloc<uint32_t>(G, &dev_bytes));
   a.load_mask = own(dalloc<uint32_t>(G, &dev_bytes));
-  a.counters = own(dalloc<int32_t>(8, &dev_bytes));
+  a.counters = own(dalloc<int32_t>(16, &dev_bytes));
   a.frame_iters = own(dalloc<unsigned long long>(1, &dev_bytes));
   CUDA_OK(cudaMemset(a.group_active, 0, G * sizeof(uint32_t)));
   CUDA_OK(cudaMemset(a.stopped, 0, G * sizeof(uint32_t)));
@@ -2157,9 +2170,12 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
     else
       launch_pdl(k_var<1>, grid_var, kVarWarps * 32, var_smem, st, a);
   });
-  if (a.use_pce)
-    launch(kSyn, st, [&] { launch_pdl(k_syndrome, grid_syn, kThreads, 2 * G * sizeof(uint32_t), st, a); });
-  launch(kTerm, st, [&] { launch_pdl(k_terminate, G * kTermBlocks, kTermThreads, 0, st, a); });
+  {
+    const int syn_blocks = a.use_pce ? grid_syn : 0;
+    launch(kSyn, st, [&] {
+      launch_pdl(k_decide, syn_blocks + G * kTermBlocks, kThreads, 2 * G * sizeof(uint32_t), st, a, syn_blocks);
+    });
+  }
   launch(kTurnover, st, [&] { launch_turnover(a, st, want_post); });
   // tail compaction (no-op unless the queue is drained and live frames fit
   // in fewer groups; decided on the device, no host round trip)
@@ -2248,7 +2264,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       pend[s] = s;
       lm[s >> 5] |= 1u << (s & 31);
     }
-    int32_t ctr[8] = {first, 0, 0, 0, G * kLanes + 32, 0, 0, 0};  // active slots counted by k_turnover
+    int32_t ctr[16] = {first, 0, 0, 0, G * kLanes + 32};  // active slots counted by k_turnover
     CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));

@@ -396,7 +396,8 @@ class BatchDecoder:
             _ptr(x_packed_dev), st))
 
     # profiling (CUDA events on the launching stream)
-    KERNELS = ("check", "variable", "syndrome", "terminate", "turnover", "compact")
+    KERNELS = ("check", "variable", "decide", "turnover", "compact")
+    _KERNEL_IDS = {"check": 0, "variable": 1, "decide": 2, "turnover": 4, "compact": 5}
 
     def set_profiling(self, enable: bool):
         _check(self._lib.bpdec_decoder_set_profiling(self._h, int(enable)))
@@ -406,9 +407,10 @@ class BatchDecoder:
 
     def profile(self) -> dict:
         res = {}
-        for k, name in enumerate(self.KERNELS):
+        for name in self.KERNELS:
             ms, n, fi = C.c_double(), C.c_int64(), C.c_double()
-            _check(self._lib.bpdec_decoder_profile(self._h, k, C.byref(ms), C.byref(n), C.byref(fi)))
+            _check(self._lib.bpdec_decoder_profile(self._h, self._KERNEL_IDS[name], C.byref(ms), C.byref(n),
+                                                   C.byref(fi)))
             res[name] = {"ms": ms.value, "launches": n.value}
             res["frame_iterations"] = fi.value
         return res
