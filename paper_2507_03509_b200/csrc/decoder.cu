@@ -1325,64 +1325,136 @@ __global__ void __launch_bounds__(kThreads) k_decide(const Args a, int syn_block
 //  * extract — outputs (hard bits, posteriors) of the frames that stopped
 //    (decoder.cpp:126-128), in the original variable order;
 //  * load — the next queued frames into the freed slots.
-// Item block b owns the chunk quads q = b, b + item_blocks, ... (4 x 32
-// original variables).  Phase A: its warps extract the stopped lanes of
-// those chunks (warp = chunk, lane = variable; the variable map and the
-// bit-sliced hard-decision word serve every stopped lane; packed words come
-// from one ballot).  Barrier.  Phase B: the same rows are overwritten with
-// the new frames' LLRs — 32 frames x 128 variables read row-coalesced,
-// transposed in shared memory, written as one 128-byte [item][32 lanes] row
-// per variable at its device position (vmap); a slot is recycled in the
-// step it frees.  Check blocks: the target syndrome, one 32-check input word
-// per warp bit-transposed with 32 ballots into the device-order words (cdev).
-// One block: slot state.
+// Work items are (group with turnover, quad of 4 x 32 original variables),
+// so groups are handled in parallel.  Per item: its warps extract the
+// group's stopped lanes of the 4 chunks (warp = chunk, lane = variable; the
+// bit-sliced hard-decision word serves every stopped lane; packed words come
+// from one ballot); barrier; the same rows are overwritten with the new
+// frames' LLRs — up to 32 frames x 128 variables read row-coalesced,
+// transposed in shared memory, written as one [item][32 lanes] row per
+// variable at its device position (vmap); a slot is recycled in the step it
+// frees.  Check blocks: the target syndrome, one 32-check input word per warp
+// bit-transposed with 32 ballots into the device-order words (cdev).  One
+// block: slot state.
 constexpr int kTurnChunks = 4;
+constexpr int kMaxGroups = 1024;  // worklist capacity (slots <= 32768)
+constexpr int kSparseLoad = 8;    // at most this many entering frames per group: direct scatter path
 
 template <bool WANT_POST>
-__device__ __forceinline__ void extract_chunk(const Args& a, int ch, int lane) {
+__device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm, int ch, int lane) {
   const int i = ch * 32 + lane;
   const bool valid = i < a.N;
   const int vm = valid ? __ldg(&a.vmap[i]) : 0;
-  for (int g = 0; g < a.G; ++g) {
-    uint32_t sm = a.stopped[g];
-    if (sm == 0u) continue;
-    uint32_t word = 0u;
-    const float* prow = nullptr;  // row of 32 lanes holding this variable's posterior
-    const bool deg0 = valid && vm >= a.NV;
+  uint32_t word = 0u;
+  const float* prow = nullptr;  // row of 32 lanes holding this variable's posterior
+  const bool deg0 = valid && vm >= a.NV;
+  if (valid) {
+    if (vm >= 0) {
+      if (vm < a.NV) {
+        word = a.hbits[static_cast<size_t>(g) * a.NV + vm];
+        prow = a.post + (static_cast<size_t>(g) * a.NV + vm) * kLanes;
+      } else {  // degree-0 variable: posterior = channel LLR
+        prow = a.llr_h + (static_cast<size_t>(g) * a.NH + vm) * kLanes;
+      }
+    } else {
+      const int dd = -1 - vm;
+      word = a.d1bits[static_cast<size_t>(g) * a.N1 + dd];
+      if (WANT_POST) prow = a.d1post + (static_cast<size_t>(g) * a.N1 + dd) * kLanes;
+    }
+  }
+  while (sm) {
+    const int l = __ffs(sm) - 1;
+    sm &= sm - 1;
+    const int f = a.stop_frame[g * kLanes + l];
+    uint32_t bit = (word >> l) & 1u;
+    float pv = 0.0f;
+    if (deg0) {
+      pv = prow[l];
+      bit = pv < 0.0f ? 1u : 0u;
+    } else if (WANT_POST && valid) {
+      pv = prow[l];
+    }
     if (valid) {
-      if (vm >= 0) {
-        if (vm < a.NV) {
-          word = a.hbits[static_cast<size_t>(g) * a.NV + vm];
-          prow = a.post + (static_cast<size_t>(g) * a.NV + vm) * kLanes;
-        } else {  // degree-0 variable: posterior = channel LLR
-          prow = a.llr_h + (static_cast<size_t>(g) * a.NH + vm) * kLanes;
-        }
+      if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
+      if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
+    }
+    if (a.out_bits_pk) {
+      const uint32_t pw = __ballot_sync(0xffffffffu, bit);
+      if (lane == 0) a.out_bits_pk[static_cast<size_t>(f) * a.NW + ch] = pw;
+    }
+  }
+}
+
+// Dense refill of one quad (4 x 32 original variables) of group g: up to 32
+// entering frames read row-coalesced, transposed in shared memory, written as
+// one [item][32 lanes] row per variable at its device position (vmap).
+// Block-level (two barriers).
+__device__ __forceinline__ void load_quad_tile(const Args& a, int g, uint32_t lm, int ch0,
+                                               float (*tile)[32][33], int lane, int warp) {
+  constexpr int kW = kThreads / 32;
+  // read: warp = slot lanes r = warp + 8m, lanes = consecutive original
+  // variables; all 4 x 4 loads in flight before any use
+  constexpr int kRpw = 32 / kW;
+  float v[kTurnChunks][kRpw];
+#pragma unroll
+  for (int m = 0; m < kRpw; ++m) {
+    const int r = warp + kW * m;
+    const bool on = (lm >> r) & 1u;
+    const int f = on ? a.pending_frame[g * kLanes + r] : 0;
+    const float* src = a.in_llr + static_cast<size_t>(f) * a.N;
+#pragma unroll
+    for (int c = 0; c < kTurnChunks; ++c) {
+      const int i = (ch0 + c) * 32 + lane;
+      v[c][m] = (on && i < a.N) ? src[i] : 0.0f;
+    }
+  }
+  bool bad = false;
+#pragma unroll
+  for (int m = 0; m < kRpw; ++m) {
+#pragma unroll
+    for (int c = 0; c < kTurnChunks; ++c) {
+      bad |= !isfinite(v[c][m]);
+      tile[c][warp + kW * m][lane] = v[c][m];
+    }
+  }
+  if (bad) atomicOr(&a.counters[2], 1);
+  __syncthreads();
+  // write: warp = variable j, lanes = slots (one row)
+  for (int jj = warp; jj < 32 * kTurnChunks; jj += kW) {
+    const int i = ch0 * 32 + jj;
+    if (i < a.N && ((lm >> lane) & 1u)) {
+      const float x = tile[jj >> 5][lane][jj & 31];
+      const int vj = __ldg(&a.vmap[i]);
+      if (vj >= 0) {
+        a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + lane] = x;
+        // posterior state starts at the channel LLR (v2c of iteration 1)
+        if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + lane] = x;
       } else {
-        const int dd = -1 - vm;
-        word = a.d1bits[static_cast<size_t>(g) * a.N1 + dd];
-        if (WANT_POST) prow = a.d1post + (static_cast<size_t>(g) * a.N1 + dd) * kLanes;
+        a.llr_d[(static_cast<size_t>(g) * a.N1 + (-1 - vj)) * kLanes + lane] = x;
       }
     }
-    while (sm) {
-      const int l = __ffs(sm) - 1;
-      sm &= sm - 1;
-      const int f = a.stop_frame[g * kLanes + l];
-      uint32_t bit = (word >> l) & 1u;
-      float pv = 0.0f;
-      if (deg0) {
-        pv = prow[l];
-        bit = pv < 0.0f ? 1u : 0u;
-      } else if (WANT_POST && valid) {
-        pv = prow[l];
-      }
-      if (valid) {
-        if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
-        if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
-      }
-      if (a.out_bits_pk) {
-        const uint32_t pw = __ballot_sync(0xffffffffu, bit);
-        if (lane == 0) a.out_bits_pk[static_cast<size_t>(f) * a.NW + ch] = pw;
-      }
+  }
+  __syncthreads();  // the tile is reused
+}
+
+// Sparse refill of one chunk (32 original variables) of group g: few frames
+// enter, so lane = variable, one coalesced LLR read per entering frame and a
+// direct write into its slot lane (no transpose, no barrier).  Warp-level.
+__device__ __forceinline__ void load_chunk_sparse(const Args& a, int g, uint32_t lm, int ch, int lane) {
+  const int i = ch * 32 + lane;
+  if (i >= a.N) return;
+  const int vj = __ldg(&a.vmap[i]);
+  while (lm) {
+    const int r = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const int f = a.pending_frame[g * kLanes + r];
+    const float v = a.in_llr[static_cast<size_t>(f) * a.N + i];
+    if (!isfinite(v)) atomicOr(&a.counters[2], 1);
+    if (vj >= 0) {
+      a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + r] = v;
+      if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + r] = v;
+    } else {
+      a.llr_d[(static_cast<size_t>(g) * a.N1 + (-1 - vj)) * kLanes + r] = v;
     }
   }
 }
@@ -1391,88 +1463,96 @@ template <bool WANT_POST>
 __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_blocks, int check_blocks) {
   pdl_begin();
   __shared__ float tile[kTurnChunks][32][33];
-  uint32_t any_stop = 0u, any_load = 0u;
-  for (int g = 0; g < a.G; ++g) {
-    any_stop |= a.stopped[g];
-    any_load |= a.load_mask[g];
-  }
-  if ((any_stop | any_load) == 0u) return;  // nothing to hand over this step
+  __shared__ int16_t s_wg[kMaxGroups];  // groups with turnover (stops or loads), ascending
+  __shared__ int16_t s_lg[kMaxGroups];  // groups with loads
+  __shared__ int16_t s_sg[kMaxGroups];  // groups with stops
+  __shared__ int16_t s_dg[kMaxGroups];  // groups with more than kSparseLoad entering frames
+  __shared__ int16_t s_pg[kMaxGroups];  // groups with 1..kSparseLoad entering frames
+  __shared__ int s_n[5];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int kW = kThreads / 32;
-  const int b = blockIdx.x;
-  if (b < item_blocks) {
-    const int quads = (a.NW + kTurnChunks - 1) / kTurnChunks;
-    if (any_stop) {
-      // phase A: (quad, chunk) pairs of this block dealt over its warps
-      const int per_block = (quads - b + item_blocks - 1) / item_blocks * kTurnChunks;
-      for (int k = warp; k < per_block; k += kW) {
-        const int ch = (b + (k / kTurnChunks) * item_blocks) * kTurnChunks + (k % kTurnChunks);
-        if (ch < a.NW) extract_chunk<WANT_POST>(a, ch, lane);
+  // worklists (every block builds the same ones; warp 0, in group order)
+  if (warp == 0) {
+    int n[5] = {0, 0, 0, 0, 0};
+    for (int g0 = 0; g0 < a.G; g0 += 32) {
+      const int g = g0 + lane;
+      const uint32_t st = g < a.G ? a.stopped[g] : 0u;
+      const uint32_t lm = g < a.G ? a.load_mask[g] : 0u;
+      const bool c[5] = {(st | lm) != 0u, lm != 0u, st != 0u, __popc(lm) > kSparseLoad,
+                         lm != 0u && __popc(lm) <= kSparseLoad};
+      int16_t* lists[5] = {s_wg, s_lg, s_sg, s_dg, s_pg};
+      const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const uint32_t bw = __ballot_sync(0xffffffffu, c[k]);
+        if (c[k]) lists[k][n[k] + __popc(bw & below)] = static_cast<int16_t>(g);
+        n[k] += __popc(bw);
       }
-      if (!any_load) return;
-      __syncthreads();  // outputs read before the rows are refilled
     }
-    for (int qd = b; qd < quads; qd += item_blocks) {
+    if (lane == 0)
+      for (int k = 0; k < 5; ++k) s_n[k] = n[k];
+  }
+  __syncthreads();
+  const int nw = s_n[0], nl = s_n[1];
+  if (nw == 0) return;  // nothing to hand over this step
+  const int b = blockIdx.x;
+  const int quads = (a.NW + kTurnChunks - 1) / kTurnChunks;
+  if (b < item_blocks && (WANT_POST || a.NH != a.NV)) {
+    // outputs read rows a refill overwrites (posteriors, degree-0 LLRs):
+    // items (group, quad), extraction before the refill of the same rows
+    const long long items = static_cast<long long>(nw) * quads;
+    for (long long it = b; it < items; it += item_blocks) {
+      const int wi = static_cast<int>(it / quads);
+      const int qd = static_cast<int>(it - static_cast<long long>(wi) * quads);
+      const int g = s_wg[wi];
+      const uint32_t sm = a.stopped[g];
+      const uint32_t lm = a.load_mask[g];
       const int ch0 = qd * kTurnChunks;
-      for (int g = 0; g < a.G; ++g) {
-        const uint32_t lm = a.load_mask[g];
-        if (lm == 0u) continue;  // block-uniform
-        // read: warp = slot lanes r = warp + 8m, lanes = consecutive original
-        // variables; all 4 x 4 loads in flight before any use
-        constexpr int kRpw = 32 / kW;
-        float v[kTurnChunks][kRpw];
-#pragma unroll
-        for (int m = 0; m < kRpw; ++m) {
-          const int r = warp + kW * m;
-          const bool on = (lm >> r) & 1u;
-          const int f = on ? a.pending_frame[g * kLanes + r] : 0;
-          const float* src = a.in_llr + static_cast<size_t>(f) * a.N;
-#pragma unroll
-          for (int c = 0; c < kTurnChunks; ++c) {
-            const int i = (ch0 + c) * 32 + lane;
-            v[c][m] = (on && i < a.N) ? src[i] : 0.0f;
-          }
-        }
-        bool bad = false;
-#pragma unroll
-        for (int m = 0; m < kRpw; ++m) {
-#pragma unroll
-          for (int c = 0; c < kTurnChunks; ++c) {
-            bad |= !isfinite(v[c][m]);
-            tile[c][warp + kW * m][lane] = v[c][m];
-          }
-        }
-        if (bad) atomicOr(&a.counters[2], 1);
-        __syncthreads();
-        // write: warp = variable j, lanes = slots (one 128-byte row)
-        for (int jj = warp; jj < 32 * kTurnChunks; jj += kW) {
-          const int i = ch0 * 32 + jj;
-          if (i < a.N && ((lm >> lane) & 1u)) {
-            const float v = tile[jj >> 5][lane][jj & 31];
-            const int vj = __ldg(&a.vmap[i]);
-            if (vj >= 0) {
-              a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + lane] = v;
-              // posterior state starts at the channel LLR (v2c of iteration 1)
-              if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + lane] = v;
-            } else {
-              a.llr_d[(static_cast<size_t>(g) * a.N1 + (-1 - vj)) * kLanes + lane] = v;
-            }
-          }
-        }
-        __syncthreads();
+      if (sm) {
+        if (warp < kTurnChunks && ch0 + warp < a.NW) extract_chunk<WANT_POST>(a, g, sm, ch0 + warp, lane);
+        __syncthreads();  // outputs read before the rows are refilled
+      }
+      if (lm) load_quad_tile(a, g, lm, ch0, tile, lane, warp);
+    }
+  } else if (b < item_blocks) {
+    // packed/u8 bits only and no degree-0 variables: extraction reads only the
+    // hard-decision words, which a refill does not touch, so the phases are
+    // independent.  Dense refills: block-level (group, quad) items.
+    const int nd = s_n[3], ns = s_n[2], np = s_n[4];
+    const long long dense = static_cast<long long>(nd) * quads;
+    for (long long it = b; it < dense; it += item_blocks) {
+      const int di = static_cast<int>(it / quads);
+      const int qd = static_cast<int>(it - static_cast<long long>(di) * quads);
+      const int g = s_dg[di];
+      load_quad_tile(a, g, a.load_mask[g], qd * kTurnChunks, tile, lane, warp);
+    }
+    // extraction and sparse refills: warp-level (group, chunk) items
+    const long long ext = static_cast<long long>(ns) * a.NW;
+    const long long total = ext + static_cast<long long>(np) * a.NW;
+    const long long nwarps = static_cast<long long>(item_blocks) * kW;
+    for (long long e = static_cast<long long>(b) * kW + warp; e < total; e += nwarps) {
+      if (e < ext) {
+        const int si = static_cast<int>(e / a.NW);
+        const int g = s_sg[si];
+        extract_chunk<WANT_POST>(a, g, a.stopped[g], static_cast<int>(e - static_cast<long long>(si) * a.NW), lane);
+      } else {
+        const long long e2 = e - ext;
+        const int pi = static_cast<int>(e2 / a.NW);
+        const int g = s_pg[pi];
+        load_chunk_sparse(a, g, a.load_mask[g], static_cast<int>(e2 - static_cast<long long>(pi) * a.NW), lane);
       }
     }
   } else if (b < item_blocks + check_blocks) {
-    if (any_load == 0u) return;
+    if (nl == 0) return;
     if (a.in_syn) {
-      const int nw = check_blocks * kW;
-      for (long long w = static_cast<long long>(b - item_blocks) * kW + warp; w < static_cast<long long>(a.G) * a.MW;
-           w += nw) {
-        const int g = static_cast<int>(w / a.MW);
-        const int wi = static_cast<int>(w - static_cast<long long>(g) * a.MW);
+      const int nwarp = check_blocks * kW;
+      const long long items = static_cast<long long>(nl) * a.MW;
+      for (long long w = static_cast<long long>(b - item_blocks) * kW + warp; w < items; w += nwarp) {
+        const int li = static_cast<int>(w / a.MW);
+        const int wi = static_cast<int>(w - static_cast<long long>(li) * a.MW);
+        const int g = s_lg[li];
         const uint32_t lm = a.load_mask[g];
-        if (lm == 0u) continue;
         uint32_t mine = 0u;  // lane r: input word wi of the frame entering slot r
         if ((lm >> lane) & 1u) {
           const int f = a.pending_frame[g * kLanes + lane];
@@ -1491,15 +1571,16 @@ __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_bl
         }
       }
     } else {
-      const long long total = static_cast<long long>(a.G) * a.M;
+      const long long items = static_cast<long long>(nl) * a.M;
       const long long stride = static_cast<long long>(check_blocks) * blockDim.x;
-      for (long long w = static_cast<long long>(b - item_blocks) * blockDim.x + threadIdx.x; w < total; w += stride) {
-        const uint32_t lm = a.load_mask[static_cast<int>(w / a.M)];
-        if (lm != 0u) a.syn_target[w] &= ~lm;
+      for (long long w = static_cast<long long>(b - item_blocks) * blockDim.x + threadIdx.x; w < items; w += stride) {
+        const int li = static_cast<int>(w / a.M);
+        const int g = s_lg[li];
+        a.syn_target[static_cast<size_t>(g) * a.M + (w - static_cast<long long>(li) * a.M)] &= ~a.load_mask[g];
       }
     }
   } else {
-    if (any_load == 0u) return;
+    if (nl == 0) return;
     for (int s = threadIdx.x; s < a.G * kLanes; s += blockDim.x) {
       const int g = s >> 5;
       const uint32_t bit = 1u << (s & 31);
@@ -1853,6 +1934,7 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
     throw CudaError(std::string("device ") + prop.name + " is not sm_100-class; this build targets sm_100a only");
   }
   if (max_slots < 1) throw ValidationError("decoder: max_slots must be positive");
+  if (max_slots > 32 * kMaxGroups) throw ValidationError("decoder: max_slots above 32768 is not supported");
   S = (max_slots + 31) / 32 * 32;
   G = S / 32;
 

@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Short, deterministic decode used as the ncu capture target: config-2 code,
 64 device-generated frames, PCE-ET, D_max=6 (every frame runs 6 iterations).
-Third argument "vnr": the bench decode instead (VNR+PCE, the workload's D_max)."""
+Third argument "vnr": the bench decode instead (VNR+PCE, the workload's D_max);
+"stream": VNR+PCE with the frames streaming through a quarter of the slots."""
 import os
 import sys
 
@@ -24,7 +25,9 @@ out = {"iterations": torch.zeros(frames, dtype=torch.int32, device="cuda"),
        "reasons": torch.zeros(frames, dtype=torch.uint8, device="cuda"),
        "bits": torch.zeros((frames, (N + 31) // 32), dtype=torch.int32, device="cuda")}
 mode = sys.argv[3] if len(sys.argv) > 3 else "pce6"
-cfg = (P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS) if mode == "vnr"
+if mode == "stream":  # frames stream through a quarter of the slots
+    dec = P.BatchDecoder(code, max_slots=max(32, frames // 4))
+cfg = (P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS) if mode in ("vnr", "stream")
        else P.DecodeConfig(d_max=6, use_pce=True, use_vnr=False, q_mode=Q_ABS))
 r = dec.decode_batch(d_llr, cfg, syndrome=d_syn,
                      packed=True, out=out)

@@ -330,6 +330,25 @@ def test_determinism_and_slot_invariance(P, cfg1_code):
     assert np.array_equal(np.concatenate([p.iterations for p in parts]), ref.iterations)
 
 
+def test_streaming_turnover_paths(P, cfg1_code):
+    """Frames streaming through few slots (refills of 1..32 lanes per group,
+    sparse and dense refill paths, independent extraction) give the same
+    per-frame results as one frame per slot, with and without posteriors."""
+    snr = P.snr_for_beta(0.95, cfg1_code.rate())
+    llr, x, s = P.sample_frames(cfg1_code, snr, 51, 0, 200)
+    cfg = P.DecodeConfig(d_max=120, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    ref = P.BatchDecoder(cfg1_code, max_slots=224).decode_batch(llr, cfg, syndrome=s, want_posteriors=True)
+    for slots in (32, 96):
+        d = P.BatchDecoder(cfg1_code, max_slots=slots)
+        for packed in (False, True):
+            g = d.decode_batch(llr, cfg, syndrome=s, packed=packed)
+            bits = P.unpack_bits(g.bits, cfg1_code.n_vars) if packed else g.bits
+            assert np.array_equal(bits, ref.bits), (slots, packed)
+            assert np.array_equal(g.iterations, ref.iterations) and np.array_equal(g.reasons, ref.reasons)
+        g = d.decode_batch(llr, cfg, syndrome=s, want_posteriors=True)
+        assert np.array_equal(g.posteriors, ref.posteriors)
+
+
 def test_device_generator_matches_host(P, cfg1_code):
     import torch
     dec = P.BatchDecoder(cfg1_code, max_slots=32)
