@@ -19,7 +19,7 @@ sys.path.insert(0, ROOT)
 import paper_2507_03509_b200 as P  # noqa: E402
 from paper_2507_03509_b200.decoder import Q_ABS  # noqa: E402
 
-BETAS = [0.50, 0.70, 0.80, 0.90, 0.92, 0.94, 0.96, 0.98, 0.99]
+BETAS = [0.10, 0.20, 0.30, 0.40, 0.50, 0.70, 0.80, 0.90, 0.92, 0.94, 0.96, 0.98, 0.99]
 FRAMES = 64
 
 
