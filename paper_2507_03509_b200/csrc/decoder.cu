@@ -1746,6 +1746,21 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Args a) {
   }
 }
 
+// Start of a decode: frames 0..first-1 go to slots 0..first-1, per-decode
+// counters and masks are reset (counters[4] = compaction hysteresis start).
+__global__ void k_decode_init(const Args a, int first) {
+  for (int s = threadIdx.x; s < a.G * kLanes; s += blockDim.x) a.pending_frame[s] = s < first ? s : 0;
+  for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
+    const int lo = g * kLanes;
+    const int n = min(max(first - lo, 0), kLanes);
+    a.load_mask[g] = n == kLanes ? 0xffffffffu : ((1u << n) - 1u);
+    a.group_active[g] = 0u;
+    a.stopped[g] = 0u;
+  }
+  if (threadIdx.x < 16) a.counters[threadIdx.x] = threadIdx.x == 0 ? first : (threadIdx.x == 4 ? a.G * kLanes + 32 : 0);
+  if (threadIdx.x == 0) *a.frame_iters = 0ull;
+}
+
 // ---------------------------------------------------------- generators --
 // Syndrome-mode frames on device; same draws as bpdec_sample_frames
 // (channel.cpp:44-61 with the message bit x and s = Hx on top).
@@ -2337,25 +2352,11 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   a.out_qtrace = static_cast<double*>(dev_out(b.q_trace, B * p.d_max * sizeof(double), s_qtrace, &st_q));
   if (a.out_qtrace) CUDA_OK(cudaMemsetAsync(a.out_qtrace, 0xff, B * p.d_max * sizeof(double), st));  // NaN
 
-  // initial slot assignment: frames 0..min(B,S)-1 -> slots 0..
+  // initial slot assignment (frames 0..min(B,S)-1 -> slots 0..) and state
+  // reset on the device: no host copies, no host synchronisation
   const int first = static_cast<int>(std::min<size_t>(B, S));
-  {
-    std::vector<int32_t> pend(S, 0);
-    std::vector<uint32_t> lm(G, 0u);
-    for (int s = 0; s < first; ++s) {
-      pend[s] = s;
-      lm[s >> 5] |= 1u << (s & 31);
-    }
-    int32_t ctr[16] = {first, 0, 0, 0, G * kLanes + 32};  // active slots counted by k_turnover
-    CUDA_OK(cudaMemcpyAsync(a.pending_frame, pend.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    CUDA_OK(cudaMemcpyAsync(a.load_mask, lm.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    CUDA_OK(cudaMemcpyAsync(a.counters, ctr, sizeof(ctr), cudaMemcpyHostToDevice, st));
-    CUDA_OK(cudaMemsetAsync(a.group_active, 0, G * sizeof(uint32_t), st));
-    CUDA_OK(cudaMemsetAsync(a.stopped, 0, G * sizeof(uint32_t), st));
-    CUDA_OK(cudaMemsetAsync(a.frame_iters, 0, sizeof(unsigned long long), st));
-    // the host vectors die at scope end: make the copies complete first
-    CUDA_OK(cudaStreamSynchronize(st));
-  }
+  k_decode_init<<<1, 1024, 0, st>>>(a, first);
+  CUDA_OK(cudaGetLastError());
   launch(kTurnover, st, [&] { launch_turnover(a, st, false); });
   CUDA_OK(cudaMemsetAsync(a.load_mask, 0, G * sizeof(uint32_t), st));
 
