@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 echo "ncu_launches=$?" >> gpurun_out/status.txt
 cat gpurun_out/status.txt
 python scripts/ncu_target.py cfg2 64 vnr > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_check|k_var|k_syndrome|k_terminate|k_turnover" -s 10 -c 5 \
+ncu --set full --clock-control none --import-source on -k regex:"k_check|k_var|k_decide|k_turnover" -s 8 -c 4 \
     -o gpurun_out/prof_full python scripts/ncu_target.py cfg2 64 vnr > gpurun_out/ncu_full.log 2>&1
 echo "ncu_full=$?" >> gpurun_out/status.txt
 cat gpurun_out/status.txt
