@@ -590,7 +590,7 @@ __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, 
 }
 
 template <int MAXD, bool WANT_POST>
-__global__ void __launch_bounds__(kCheckThreads, 6) k_check(const Args a) {
+__global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 5 blocks/SM, 96 regs: measured best
   pdl_begin();
   constexpr bool kStage = MAXD <= 16;
   constexpr int kHH = kStage ? 32 * MAXD : 1;

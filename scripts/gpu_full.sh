@@ -16,6 +16,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-pce-compare > gpurun_out/ncu_launch.log 2>&1
 echo "ncu_launches=$?" >> gpurun_out/status.txt
 cat gpurun_out/status.txt
+timeout 900 python scripts/vnr_pce_sweep.py gpurun_out/et_sweep_cfg2.json > gpurun_out/sweep2.log 2>&1; echo "sweep2=$?" >> gpurun_out/status.txt
+timeout 900 python scripts/vnr_pce_sweep.py gpurun_out/et_sweep_cfg5.json --workload cfg5 > gpurun_out/sweep5.log 2>&1; echo "sweep5=$?" >> gpurun_out/status.txt
 python scripts/ncu_target.py cfg2 64 vnr > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_check|k_var|k_decide|k_turnover" -s 8 -c 4 \
     -o gpurun_out/prof_full python scripts/ncu_target.py cfg2 64 vnr > gpurun_out/ncu_full.log 2>&1
