@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
 // check-major copy the syndrome kernel streams).  The tile's q partial is
 // chunk0 + chunk1, each summed in variable order — an order fixed by the code
 // (not by slots, batch size or GPU count).
-constexpr int kVarRingRows = 40;   // per-warp ring of the variable kernel (rows of 128 B)
+constexpr int kVarRingRows = 40;   // per-warp ring of the variable kernel (rows of 128 B; 48/56 measured slower)
 constexpr int kVarStageRows = 13;  // target rows per batch of the variable kernel (degree 12 unsplit)
 constexpr int kVarMaxTyped = 32;   // largest tile degree on the typed (streamed) path
 
