@@ -1903,6 +1903,8 @@ class GpuDecoder {
   void launch(int kid, cudaStream_t st, F&& f);
   void run_step(const Args& a, cudaStream_t st, bool want_post);
   void launch_turnover(const Args& a, cudaStream_t st, bool want_post);
+  void init(const Code& code, int max_slots);
+  void release() noexcept;
 
   Args base{};
   int32_t max_check_deg = 0;
@@ -1936,6 +1938,17 @@ class GpuDecoder {
 };
 
 GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
+  // a failed construction (bad device, out of memory) releases what it got
+  try {
+    init(code, max_slots);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+void GpuDecoder::init(const Code& code, int max_slots) {
+  const int dev = device;
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
     (void)cudaGetLastError();
@@ -2199,18 +2212,26 @@ GpuDecoder::GpuDecoder(const Code& code, int dev, int max_slots) : device(dev) {
   turn_check_blocks = sms * 2;
 }
 
-GpuDecoder::~GpuDecoder() {
+GpuDecoder::~GpuDecoder() { release(); }
+
+void GpuDecoder::release() noexcept {
   cudaSetDevice(device);
   for (void* p : owned) cudaFree(p);
   if (base.d1post) cudaFree(base.d1post);
   for (auto& e : ring_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : prof_ev) cudaEventDestroy(e);
+  prof_ev.clear();
+  for (auto& e : ring_ev) e = nullptr;
   if (h_counters) cudaFreeHost(h_counters);
   for (auto& sg : staged)
     if (sg.done) cudaEventDestroy(sg.done);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
+  owned.clear();
+  base.d1post = nullptr;
+  h_counters = nullptr;
+  copy_stream = own_stream = nullptr;
 }
 
 template <typename F>

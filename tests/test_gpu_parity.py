@@ -296,6 +296,22 @@ def test_staged_host_inputs(P, cfg1_code):
         dec.stage_inputs(batches[0][0].cuda(), None)
 
 
+def test_failed_construction_is_clean(P, cfg1_code):
+    """A bad device index or an impossible slot count fails with the right
+    error class and releases what it allocated; decoders still work after."""
+    with pytest.raises(P.ConfigError):
+        P.BatchDecoder(cfg1_code, device=99, max_slots=32)
+    with pytest.raises(P.ValidationError):
+        P.BatchDecoder(cfg1_code, max_slots=0)
+    big = P.generate_met(1 << 20, 943718, 0.75, (3, 6, 12), (0.5, 0.3, 0.2), 7)
+    for _ in range(3):  # ~15 GB per attempt would exhaust the GPU if leaked
+        with pytest.raises((P.decoder.BpdecOomError, P.ValidationError)):
+            P.BatchDecoder(big, max_slots=32768)
+    dec = P.BatchDecoder(cfg1_code, max_slots=32)
+    llr, _, _ = P.sample_frames(cfg1_code, P.snr_for_beta(0.9, cfg1_code.rate()), 3, 0, 4, all_zero=True)
+    assert dec.decode_batch(llr, P.DecodeConfig(d_max=10)).iterations.shape == (4,)
+
+
 def test_nonfinite_llr_rejected(P, cfg1_code):
     dec = P.BatchDecoder(cfg1_code, max_slots=32)
     llr = np.zeros((2, cfg1_code.n_vars), dtype=np.float32)
