@@ -108,7 +108,7 @@ struct Args {
   int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots,
                             // [4] active slots at the last compaction, [5] k_compact blocks done,
                             // [6] k_var tiles handed out, [7] k_check chunks handed out,
-                            // [8] k_decide blocks done
+                            // [8] k_decide blocks done, [9] frames available (uploaded)
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -1226,12 +1226,38 @@ __device__ __forceinline__ void q_block(const Args& a, int g, int p, double (*re
 // order; PCE, then VNR (k >= 2, strict), then d_max (decoder.cpp:114-123);
 // stopping slots take the next queued frames.  Rewrites stopped[g] /
 // load_mask[g] for k_turnover.
+// Hands the free lanes of group g (lane order) the next available frames:
+// at most counters[9] (frames uploaded) and batch; returns the load mask.
+__device__ __forceinline__ uint32_t refill_lanes(const Args& a, int g, uint32_t free, int lane) {
+  int take = 0, base = 0;
+  if (lane == 0 && free != 0u) {
+    const int want = __popc(free);
+    const int limit = min(a.batch, *reinterpret_cast<volatile int32_t*>(&a.counters[9]));
+    int old = *reinterpret_cast<volatile int32_t*>(&a.counters[0]);
+    for (;;) {  // bounded grab: frames beyond the limit stay queued
+      take = max(0, min(want, limit - old));
+      if (take == 0) break;
+      const int prev = atomicCAS(&a.counters[0], old, old + take);
+      if (prev == old) break;
+      old = prev;
+    }
+    base = old;
+  }
+  take = __shfl_sync(0xffffffffu, take, 0);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const int rank = __popc(free & ((1u << lane) - 1u));
+  const bool refill = ((free >> lane) & 1u) && rank < take;
+  if (refill) a.pending_frame[g * kLanes + lane] = base + rank;
+  return __ballot_sync(0xffffffffu, refill);
+}
+
 __device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
   const uint32_t amask = a.group_active[g];
-  if (amask == 0u) {
+  if (amask == 0u) {  // idle group: frames may have become available since
+    const uint32_t load = refill_lanes(a, g, 0xffffffffu, lane);
     if (lane == 0) {
       a.stopped[g] = 0u;
-      a.load_mask[g] = 0u;
+      a.load_mask[g] = load;
     }
     return;
   }
@@ -1268,19 +1294,14 @@ __device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
   }
   const uint32_t stop = __ballot_sync(0xffffffffu, reason >= 0);
   const int nstop = __popc(stop);
-  int base = 0;
   if (lane == 0 && nstop > 0) {
     a.group_active[g] = amask & ~stop;
     atomicAdd(&a.counters[1], nstop);
     atomicSub(&a.counters[3], nstop);
-    base = atomicAdd(&a.counters[0], nstop);
   }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  // refill: the stopping slots take the next queued frames, in lane order
-  const int nf = base + __popc(stop & ((1u << lane) - 1u));
-  const bool refill = reason >= 0 && nf < a.batch;
-  if (refill) a.pending_frame[s] = nf;
-  const uint32_t load = __ballot_sync(0xffffffffu, refill);
+  // refill: every lane that is not active (this step's stops and lanes left
+  // free earlier) takes the next available queued frame, in lane order
+  const uint32_t load = refill_lanes(a, g, ~(amask & ~stop), lane);
   if (lane == 0) {
     a.stopped[g] = stop;
     a.load_mask[g] = load;
@@ -1748,7 +1769,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Args a) {
 
 // Start of a decode: frames 0..first-1 go to slots 0..first-1, per-decode
 // counters and masks are reset (counters[4] = compaction hysteresis start).
-__global__ void k_decode_init(const Args a, int first) {
+__global__ void k_decode_init(const Args a, int first, int avail) {
   for (int s = threadIdx.x; s < a.G * kLanes; s += blockDim.x) a.pending_frame[s] = s < first ? s : 0;
   for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
     const int lo = g * kLanes;
@@ -1757,7 +1778,11 @@ __global__ void k_decode_init(const Args a, int first) {
     a.group_active[g] = 0u;
     a.stopped[g] = 0u;
   }
-  if (threadIdx.x < 16) a.counters[threadIdx.x] = threadIdx.x == 0 ? first : (threadIdx.x == 4 ? a.G * kLanes + 32 : 0);
+  if (threadIdx.x < 16)
+    a.counters[threadIdx.x] = threadIdx.x == 0 ? first
+                              : threadIdx.x == 4 ? a.G * kLanes + 32
+                              : threadIdx.x == 9 ? avail
+                                                 : 0;
   if (threadIdx.x == 0) *a.frame_iters = 0ull;
 }
 
@@ -1932,6 +1957,10 @@ class GpuDecoder {
   Staged staged[2];
   int64_t stage_seq = 0;
   cudaStream_t copy_stream = nullptr;
+  // chunked upload of unstaged host inputs (frames available -> counters[9])
+  int32_t* h_avail = nullptr;
+  size_t h_avail_n = 0;
+  cudaEvent_t up_start = nullptr, up_first = nullptr, up_done = nullptr;
   int grid_check = 0, grid_var = 0, grid_syn = 0, sms_ = 148;
   int turn_item_blocks = 0, turn_check_blocks = 0;
   size_t var_smem = 0;
@@ -2171,6 +2200,7 @@ void GpuDecoder::init(const Code& code, int max_slots) {
   CUDA_OK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
   for (auto& sg : staged) CUDA_OK(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&up_start, &up_first, &up_done}) CUDA_OK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CUDA_OK(cudaHostAlloc(&h_counters, kRing * 4 * sizeof(int32_t), cudaHostAllocDefault));
   for (auto& e : ring_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
@@ -2226,6 +2256,10 @@ void GpuDecoder::release() noexcept {
   if (h_counters) cudaFreeHost(h_counters);
   for (auto& sg : staged)
     if (sg.done) cudaEventDestroy(sg.done);
+  for (cudaEvent_t e : {up_start, up_first, up_done})
+    if (e) cudaEventDestroy(e);
+  if (h_avail) cudaFreeHost(h_avail);
+  h_avail = nullptr;
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
   owned.clear();
@@ -2340,20 +2374,21 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   } else if (is_device_ptr(b.llr)) {
     a.in_llr = b.llr;
   } else {
-    float* d = static_cast<float*>(s_llr.get(B * a.N * sizeof(float)));
-    CUDA_OK(cudaMemcpyAsync(d, b.llr, B * a.N * sizeof(float), cudaMemcpyHostToDevice, st));
-    a.in_llr = d;
+    a.in_llr = static_cast<float*>(s_llr.get(B * a.N * sizeof(float)));
   }
   if (sg == nullptr) a.in_syn = nullptr;
   if (sg == nullptr && b.syndrome) {
-    if (is_device_ptr(b.syndrome)) {
-      a.in_syn = b.syndrome;
-    } else {
-      uint32_t* d = static_cast<uint32_t*>(s_syn.get(B * a.MW * sizeof(uint32_t)));
-      CUDA_OK(cudaMemcpyAsync(d, b.syndrome, B * a.MW * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-      a.in_syn = d;
-    }
+    a.in_syn = is_device_ptr(b.syndrome) ? b.syndrome
+                                         : static_cast<uint32_t*>(s_syn.get(B * a.MW * sizeof(uint32_t)));
   }
+  // Host inputs not staged: uploaded chunk by chunk (S frames) on the copy
+  // stream; after each chunk, counters[9] (frames available) is advanced by
+  // a 4-byte copy on the same stream, and refills only take available frames
+  // (k_decide), so the upload of later frames overlaps the decode of earlier
+  // ones.  The decode waits for the first chunk only.
+  const bool up_llr = sg == nullptr && !is_device_ptr(b.llr);
+  const bool up_syn = sg == nullptr && b.syndrome != nullptr && !is_device_ptr(b.syndrome);
+  const size_t nchunks = (B + S - 1) / S;
   // outputs (device targets; staged when the caller passed host memory)
   auto dev_out = [&](void* user, size_t bytes, Scratch& s, bool* staged) -> void* {
     *staged = false;
@@ -2376,18 +2411,61 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   // initial slot assignment (frames 0..min(B,S)-1 -> slots 0..) and state
   // reset on the device: no host copies, no host synchronisation
   const int first = static_cast<int>(std::min<size_t>(B, S));
-  k_decode_init<<<1, 1024, 0, st>>>(a, first);
+  k_decode_init<<<1, 1024, 0, st>>>(a, first, (up_llr || up_syn) ? first : static_cast<int>(B));
   CUDA_OK(cudaGetLastError());
+  // (the uploads start after the init kernel, so its reset of counters[9]
+  // cannot overwrite a later availability update)
+  if (up_llr || up_syn) {
+    if (h_avail_n < nchunks) {
+      if (h_avail) cudaFreeHost(h_avail);
+      h_avail = nullptr;
+      h_avail_n = 0;
+      CUDA_OK(cudaHostAlloc(&h_avail, nchunks * sizeof(int32_t), cudaHostAllocDefault));
+      h_avail_n = nchunks;
+    }
+    CUDA_OK(cudaEventRecord(up_start, st));  // uploads begin after earlier work on st
+    CUDA_OK(cudaStreamWaitEvent(copy_stream, up_start, 0));
+    for (size_t c = 0; c < nchunks; ++c) {
+      const size_t f0 = c * S, nf = std::min<size_t>(S, B - f0);
+      if (up_llr)
+        CUDA_OK(cudaMemcpyAsync(const_cast<float*>(a.in_llr) + f0 * a.N, b.llr + f0 * a.N, nf * a.N * sizeof(float),
+                                cudaMemcpyHostToDevice, copy_stream));
+      if (up_syn)
+        CUDA_OK(cudaMemcpyAsync(const_cast<uint32_t*>(a.in_syn) + f0 * a.MW, b.syndrome + f0 * a.MW,
+                                nf * a.MW * sizeof(uint32_t), cudaMemcpyHostToDevice, copy_stream));
+      h_avail[c] = static_cast<int32_t>(f0 + nf);
+      if (c == 0) CUDA_OK(cudaEventRecord(up_first, copy_stream));
+      if (c > 0)  // chunk 0 is available by construction (the decode waits for it)
+        CUDA_OK(cudaMemcpyAsync(a.counters + 9, h_avail + c, sizeof(int32_t), cudaMemcpyHostToDevice, copy_stream));
+    }
+    CUDA_OK(cudaEventRecord(up_done, copy_stream));
+  }
+  if (up_llr || up_syn) CUDA_OK(cudaStreamWaitEvent(st, up_first, 0));
   launch(kTurnover, st, [&] { launch_turnover(a, st, false); });
   CUDA_OK(cudaMemsetAsync(a.load_mask, 0, G * sizeof(uint32_t), st));
 
   // step loop: poll the frames-done counter with a lag so the GPU never idles
   const int64_t waves = (static_cast<int64_t>(B) + S - 1) / S;
-  const int64_t max_steps = static_cast<int64_t>(p.d_max) * waves + 2;
+  int64_t max_steps = static_cast<int64_t>(p.d_max) * waves + 2;
   constexpr int kLag = 4;
   int64_t step = 0;
   bool done = false;
-  for (; step < max_steps + kLag && !done; ++step) {
+  bool uploading = up_llr || up_syn;
+  // safety bound on the step count (frames must terminate within d_max
+  // steps per wave); while chunks are still uploading, steps spent waiting
+  // for frames do not count
+  for (; (uploading || step < max_steps + kLag) && !done; ++step) {
+    if (uploading) {
+      const cudaError_t q = cudaEventQuery(up_done);
+      if (q == cudaSuccess) {
+        uploading = false;
+        max_steps = std::max(max_steps, step + static_cast<int64_t>(p.d_max) * waves + 2);
+      } else if (q == cudaErrorNotReady) {
+        (void)cudaGetLastError();  // not an error: keep it out of the launch checks
+      } else {
+        CUDA_OK(q);
+      }
+    }
     run_step(a, st, want_post);
     const int slot = static_cast<int>(step % kRing);
     CUDA_OK(cudaMemcpyAsync(h_counters + 4 * slot, a.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -2400,6 +2478,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
     }
   }
   CUDA_OK(cudaStreamSynchronize(st));
+  if (up_llr || up_syn) CUDA_OK(cudaEventSynchronize(up_done));  // host buffers no longer read
   int32_t ctr[4];
   CUDA_OK(cudaMemcpy(ctr, a.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
   if (ctr[2] != 0) throw ValidationError("decode: non-finite input LLR");
