@@ -1440,12 +1440,22 @@ __device__ __forceinline__ void load_quad_tile(const Args& a, int g, uint32_t lm
   }
   if (bad) atomicOr(&a.counters[2], 1);
   __syncthreads();
-  // write: warp = variable j, lanes = slots (one row)
-  for (int jj = warp; jj < 32 * kTurnChunks; jj += kW) {
+  // write: warp = variable j, lanes = slots (one row); the device rows of
+  // all this warp's variables are looked up first (loads in flight together)
+  constexpr int kJ = 32 * kTurnChunks / kW;
+  int vjs[kJ];
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) {
+    const int i = ch0 * 32 + warp + kW * m;
+    vjs[m] = __ldg(&a.vmap[i < a.N ? i : 0]);
+  }
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) {
+    const int jj = warp + kW * m;
     const int i = ch0 * 32 + jj;
     if (i < a.N && ((lm >> lane) & 1u)) {
       const float x = tile[jj >> 5][lane][jj & 31];
-      const int vj = __ldg(&a.vmap[i]);
+      const int vj = vjs[m];
       if (vj >= 0) {
         a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + lane] = x;
         // posterior state starts at the channel LLR (v2c of iteration 1)
@@ -1463,21 +1473,35 @@ __device__ __forceinline__ void load_quad_tile(const Args& a, int g, uint32_t lm
 // direct write into its slot lane (no transpose, no barrier).  Warp-level.
 __device__ __forceinline__ void load_chunk_sparse(const Args& a, int g, uint32_t lm, int ch, int lane) {
   const int i = ch * 32 + lane;
-  if (i >= a.N) return;
-  const int vj = __ldg(&a.vmap[i]);
-  while (lm) {
-    const int r = __ffs(lm) - 1;
+  const bool in = i < a.N;
+  const int vj = in ? __ldg(&a.vmap[i]) : 0;
+  // all entering frames' values in flight at once (lm has <= kSparseLoad bits)
+  int r[kSparseLoad];
+  float v[kSparseLoad];
+#pragma unroll
+  for (int k = 0; k < kSparseLoad; ++k) {
+    r[k] = lm ? __ffs(lm) - 1 : -1;
     lm &= lm - 1;
-    const int f = a.pending_frame[g * kLanes + r];
-    const float v = a.in_llr[static_cast<size_t>(f) * a.N + i];
-    if (!isfinite(v)) atomicOr(&a.counters[2], 1);
+  }
+  int f[kSparseLoad];
+#pragma unroll
+  for (int k = 0; k < kSparseLoad; ++k) f[k] = a.pending_frame[g * kLanes + max(r[k], 0)];  // safe index
+#pragma unroll
+  for (int k = 0; k < kSparseLoad; ++k)  // predicated loads: no branch per load
+    v[k] = ld_pred(a.in_llr + static_cast<size_t>(f[k]) * a.N + (in ? i : 0), r[k] >= 0 && in);
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < kSparseLoad; ++k) {
+    if (r[k] < 0 || !in) continue;
+    bad |= !isfinite(v[k]);
     if (vj >= 0) {
-      a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + r] = v;
-      if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + r] = v;
+      a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + r[k]] = v[k];
+      if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + r[k]] = v[k];
     } else {
-      a.llr_d[(static_cast<size_t>(g) * a.N1 + (-1 - vj)) * kLanes + r] = v;
+      a.llr_d[(static_cast<size_t>(g) * a.N1 + (-1 - vj)) * kLanes + r[k]] = v[k];
     }
   }
+  if (bad) atomicOr(&a.counters[2], 1);
 }
 
 template <bool WANT_POST>
