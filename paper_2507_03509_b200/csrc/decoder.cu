@@ -577,11 +577,14 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   }
 }
 
-template <int NH, int ND, bool WANT_POST>
+// SPLIT_FM: a separate steady-state copy (no first-iteration lanes) of the
+// chunk loop.  Kernels for codes with heavy check types (MAXD >= 6) keep the
+// general copy only: twice the typed code would thrash the instruction cache.
+template <int NH, int ND, bool WANT_POST, bool SPLIT_FM>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                   const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                   uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
-  if (fmask)
+  if (!SPLIT_FM || fmask)
     check_chunk_loop<NH, ND, WANT_POST, true>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
                                               d1w);
   else
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
 #define BPDEC_TYPED(NH_, ND_)                                                                       \
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
-      check_chunk_typed<NH_, ND_, WANT_POST>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
+      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= 4)>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
                                              first, amask, fmask, &synw, &d1w);                     \
     else                                                                                            \
       typed = false;                                                                                \
@@ -658,6 +661,10 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
       BPDEC_TYPED(2, 1)
       BPDEC_TYPED(3, 0)
       BPDEC_TYPED(3, 1)
+      BPDEC_TYPED(4, 0)
+      BPDEC_TYPED(4, 1)
+      BPDEC_TYPED(5, 0)
+      BPDEC_TYPED(5, 1)
       BPDEC_TYPED(6, 0)
 #undef BPDEC_TYPED
       default:
@@ -2093,7 +2100,8 @@ void GpuDecoder::init(const Code& code, int max_slots) {
       const int32_t t0 = cnh[corig[c0]] * 8 + cnd[corig[c0]];
       bool same = true;
       for (int32_t i = 1; i < 32 && same; ++i) same = cnh[corig[c0 + i]] * 8 + cnd[corig[c0 + i]] == t0;
-      const bool shape_ok = t0 == 1 || t0 == 8 || t0 == 9 || t0 == 16 || t0 == 17 || t0 == 24 || t0 == 25 || t0 == 48;
+      const bool shape_ok = t0 == 1 || t0 == 8 || t0 == 9 || t0 == 16 || t0 == 17 || t0 == 24 || t0 == 25 ||
+                            t0 == 32 || t0 == 33 || t0 == 40 || t0 == 41 || t0 == 48;
       if (same && shape_ok) t.x = t0;
     }
     ctype[k] = t;
