@@ -407,6 +407,11 @@ struct CheckShape {
   static constexpr int RPC = 2 * NH + ND;  // rows per check
   static constexpr int K = RPC == 0 ? 8 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
   static_assert(K * RPC <= kStageRows, "stage too small");
+  // the per-warp ring (kRingRows) is cut into as many stages of this shape's
+  // batch size as fit (light shapes keep more batches in flight)
+  static constexpr int ROWS = RPC == 0 ? 1 : K * RPC;
+  static constexpr int NS = kRingRows / ROWS >= 6 ? 6 : kRingRows / ROWS;
+  static_assert(NS >= kStages, "at least the default ring depth");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -548,13 +553,14 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   const bool qact = qbits != 0u;
   const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
   const uint64_t pol = policy_evict_first();
-  constexpr int NS = kStages;
+  constexpr int NS = CheckShape<NH, ND>::NS;
+  constexpr int RS = CheckShape<NH, ND>::ROWS * kLanes;  // stage stride
   // one commit group per step (empty past the last batch), so the wait
   // count is a constant
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p) {
     if (p < NB)
-      check_batch_issue<NH, ND>(ring + p * kStageRows * kLanes, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v,
+      check_batch_issue<NH, ND>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v,
                                 pol);
     else
       cp_async_commit();
@@ -563,14 +569,14 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
     if (b + NS - 1 < NB)
-      check_batch_issue<NH, ND>(ring + slot_i * kStageRows * kLanes, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow,
+      check_batch_issue<NH, ND>(ring + slot_i * RS, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow,
                                 lcol, qact, qc2v, pol);
     else
       cp_async_commit();
     if (++slot_i == NS) slot_i = 0;
     cp_async_wait<NS - 1>();
     __syncwarp();  // rows were copied by other lanes
-    check_batch_compute<NH, ND, WANT_POST, FM>(ring + lane + slot_c * kStageRows * kLanes, c2vg, d1p, ssyn, b * K,
+    check_batch_compute<NH, ND, WANT_POST, FM>(ring + lane + slot_c * RS, c2vg, d1p, ssyn, b * K,
                                                lane, act, first, cl, clamp, synw, d1w);
     if (++slot_c == NS) slot_c = 0;
     __syncwarp();  // stage is refilled in the next round
