@@ -402,7 +402,7 @@ __device__ __forceinline__ void cp_async_wait_upto(int pending) {
   }
 }
 
-template <int NH, int ND>
+template <int NH, int ND, int RING = kRingRows>
 struct CheckShape {
   static constexpr int RPC = 2 * NH + ND;  // rows per check
   static constexpr int K = RPC == 0 ? 8 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
@@ -410,7 +410,7 @@ struct CheckShape {
   // the per-warp ring (kRingRows) is cut into as many stages of this shape's
   // batch size as fit (light shapes keep more batches in flight)
   static constexpr int ROWS = RPC == 0 ? 1 : K * RPC;
-  static constexpr int NS = kRingRows / ROWS >= 6 ? 6 : kRingRows / ROWS;
+  static constexpr int NS = RING / ROWS >= 6 ? 6 : RING / ROWS;
   static_assert(NS >= kStages, "at least the default ring depth");
 };
 
@@ -533,7 +533,7 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   }
 }
 
-template <int NH, int ND, bool WANT_POST, bool FM>
+template <int NH, int ND, bool WANT_POST, bool FM, int RING>
 __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
@@ -553,8 +553,8 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   const bool qact = qbits != 0u;
   const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
   const uint64_t pol = policy_evict_first();
-  constexpr int NS = CheckShape<NH, ND>::NS;
-  constexpr int RS = CheckShape<NH, ND>::ROWS * kLanes;  // stage stride
+  constexpr int NS = CheckShape<NH, ND, RING>::NS;
+  constexpr int RS = CheckShape<NH, ND, RING>::ROWS * kLanes;  // stage stride
   // one commit group per step (empty past the last batch), so the wait
   // count is a constant
 #pragma unroll
@@ -586,15 +586,15 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 // SPLIT_FM: a separate steady-state copy (no first-iteration lanes) of the
 // chunk loop.  Kernels for codes with heavy check types (MAXD >= 6) keep the
 // general copy only: twice the typed code would thrash the instruction cache.
-template <int NH, int ND, bool WANT_POST, bool SPLIT_FM>
+template <int NH, int ND, bool WANT_POST, bool SPLIT_FM, int RING>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                   const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                   uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   if (!SPLIT_FM || fmask)
-    check_chunk_loop<NH, ND, WANT_POST, true>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
+    check_chunk_loop<NH, ND, WANT_POST, true, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
                                               d1w);
   else
-    check_chunk_loop<NH, ND, WANT_POST, false>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
+    check_chunk_loop<NH, ND, WANT_POST, false, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
                                                d1w);
 }
 
@@ -606,7 +606,10 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
   __shared__ int4 s_desc[kCheckThreads / 32][32];
   __shared__ uint32_t s_syn[kCheckThreads / 32][32];
   __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
-  __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRingRows * kLanes];
+  // ring rows per warp: 80 (four stages of the heaviest typed batch) where
+  // the static shared memory allows it, else 60
+  constexpr int kRing = MAXD <= 4 ? 80 : kRingRows;
+  __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRing * kLanes];
   if (blockIdx.x == 0) {
     for (int t = threadIdx.x; t < a.G; t += blockDim.x) a.fail[t] = 0u;
     if (threadIdx.x == 0) a.counters[6] = 0;  // k_var tile scheduler (this step)
@@ -655,7 +658,7 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
 #define BPDEC_TYPED(NH_, ND_)                                                                       \
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
-      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= 4)>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
+      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= 4), kRing>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
                                              first, amask, fmask, &synw, &d1w);                     \
     else                                                                                            \
       typed = false;                                                                                \
