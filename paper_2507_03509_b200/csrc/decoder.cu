@@ -185,13 +185,6 @@ __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-// Advances a grid-stride cursor past the remainder of an inactive group.
-__device__ __forceinline__ long long skip_group(long long w, long long per_group, long long stride) {
-  const long long next = (w / per_group + 1) * per_group;
-  const long long k = (next - w + stride - 1) / stride;
-  return w + k * stride;
-}
-
 // ------------------------------------------------------- work schedulers --
 // k_check and k_var hand out work dynamically: a warp grabs the next index k
 // from counters[ctr] (k_check resets k_var's counter and vice versa) and k
@@ -375,32 +368,14 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
 // Typed chunk: 32 checks, each with NH edges to degree>=2 variables (c2v rows
 // hb + 32-check-local i*NH + j) and ND <= 1 degree-1 edge (row db + i).
 // K checks form a batch of R = K*(2*NH+ND) message rows.  Batches are
-// copied asynchronously (cp.async, one 4-byte element per lane per row, so a
-// warp moves whole 128-byte rows) into a two-stage per-warp shared-memory
-// ring: the rows of batch b+1 are in flight while batch b is computed from
-// shared memory, and no registers are held for data in flight.  Each lane
-// only reads back the elements it copied itself, so cp.async.wait_group is
-// the only synchronisation needed.
+// copied asynchronously (16-byte cp.async: a warp instruction moves four
+// 128-byte rows) into a per-warp shared-memory ring of NS stages: NS-1
+// batches are in flight while one is computed from shared memory, and no
+// registers are held for data in flight.  Lanes read rows other lanes
+// copied, so a __syncwarp follows each cp.async.wait_group.
 constexpr int kStageRows = 20;  // rows per batch stage (check shapes)
-constexpr int kStages = 3;      // ring depth: two batches in flight while one is computed
+constexpr int kStages = 3;      // minimum ring depth (stages of kStageRows rows)
 constexpr int kRingRows = kStages * kStageRows;
-
-// Waits until at most `pending` (0..5) committed cp.async groups are in flight.
-__device__ __forceinline__ void cp_async_wait_upto(int pending) {
-  if (pending >= 5) {
-    asm volatile("cp.async.wait_group 5;\n" ::: "memory");
-  } else if (pending == 4) {
-    asm volatile("cp.async.wait_group 4;\n" ::: "memory");
-  } else if (pending == 3) {
-    asm volatile("cp.async.wait_group 3;\n" ::: "memory");
-  } else if (pending == 2) {
-    asm volatile("cp.async.wait_group 2;\n" ::: "memory");
-  } else if (pending == 1) {
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  } else {
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  }
-}
 
 template <int NH, int ND, int RING = kRingRows>
 struct CheckShape {
@@ -416,16 +391,6 @@ struct CheckShape {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool pred) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
-               "r"(pred ? 4 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async4_ef(float* sdst, const float* gsrc, bool pred, uint64_t pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n" ::"r"(smem_u32(sdst)),
-               "l"(gsrc), "r"(pred ? 4 : 0), "l"(pol)
-               : "memory");
 }
 // 16-byte copy: lane l moves floats [4(l%8), 4(l%8)+4) of row (l/8) of a
 // 4-row group, so one warp instruction moves four 128-byte rows.
