@@ -26,6 +26,8 @@
 #include <cstdint>
 #include <functional>
 #include <limits>
+#include <algorithm>
+#include <map>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -167,10 +169,67 @@ inline double vnr_statistic(std::span<const double> posteriors, const ActiveVarS
 }
 inline bool vnr_should_stop(double q_k, double q_km1) { return q_k < q_km1; }
 
-inline double snr_for_beta(double beta, double rate) {
+// ≙ etdec::ChannelPoint / snr_for_beta (channel.hpp:14-23)
+struct ChannelPoint {
+  double beta = 0.0;
+  double rate = 0.0;
   double snr = 0.0;
-  check_status(bpdec_snr_for_beta(beta, rate, &snr));
-  return snr;
+  double sigma2 = 0.0;
+};
+inline ChannelPoint snr_for_beta(double beta, double rate) {
+  ChannelPoint p;
+  check_status(bpdec_snr_for_beta(beta, rate, &p.snr));
+  p.beta = beta;
+  p.rate = rate;
+  p.sigma2 = 1.0 / p.snr;
+  return p;
+}
+
+// ≙ etdec::PunctureMask / no_puncture / apply_puncture (puncture.hpp:12-26)
+struct PunctureMask {
+  std::vector<int> punctured;  // ascending variable indices
+  double effective_rate = 0.0;
+  bool empty() const { return punctured.empty(); }
+};
+inline PunctureMask no_puncture(const ParityCheckMatrix& code) {
+  PunctureMask m;
+  m.effective_rate = code.rate();
+  return m;
+}
+inline PunctureMask apply_puncture(const ParityCheckMatrix& code, double target_rate, std::uint64_t seed) {
+  PunctureMask m;
+  m.punctured.resize(static_cast<size_t>(code.n_vars()));
+  int32_t count = 0;
+  check_status(bpdec_code_apply_puncture(code.handle(), target_rate, seed, m.punctured.data(), &count,
+                                         &m.effective_rate));
+  m.punctured.resize(static_cast<size_t>(count));
+  return m;
+}
+
+// ≙ etdec::StopRule / TrialStats / wilson_interval (channel.hpp:42-64)
+struct StopRule {
+  long min_frame_errors = 100;
+  long max_frames = 10000;
+};
+struct TrialStats {
+  long frames = 0;
+  long frame_errors = 0;
+  long undetected_errors = 0;
+  double fer = 0.0;
+  double fer_ci_low = 0.0;
+  double fer_ci_high = 0.0;
+  double d_bar = 0.0;
+  long long iteration_sum = 0;
+  std::map<int, long> iteration_histogram;
+  long stops_syndrome = 0;
+  long stops_vnr = 0;
+  long stops_max_iter = 0;
+  bool hit_max_frames = false;
+};
+inline std::pair<double, double> wilson_interval(long k, long n) {
+  double lo = 0.0, hi = 0.0;
+  check_status(bpdec_wilson_interval(k, n, &lo, &hi));
+  return {lo, hi};
 }
 
 // GPU decoder for one code on one device.  Not thread-safe (like the
@@ -240,6 +299,42 @@ class BpDecoder {
   ParityCheckMatrix code_;
   std::unique_ptr<bpdec_decoder, Del> dec_;
 };
+
+// ≙ etdec::run_trials (channel.hpp:72-74) on the GPU: trials are decoded in
+// device-resident blocks instead of by `workers` threads; the stop rule is
+// applied to the exact trial-index prefix, so the statistics equal the
+// reference's for any block size.  `workers` only scales the block
+// (64 frames per worker, at least 64).
+inline TrialStats run_trials(const ParityCheckMatrix& code, const PunctureMask& mask, const ChannelPoint& point,
+                             const DecodeConfig& cfg, const StopRule& stop, std::uint64_t master_seed,
+                             int workers = 1, int device = 0) {
+  const int block = std::max(64, 64 * std::max(1, workers));
+  bpdec_decoder* d = nullptr;
+  check_status(bpdec_decoder_create(code.handle(), device, block, &d));
+  std::unique_ptr<bpdec_decoder, void (*)(bpdec_decoder*)> hold(d, bpdec_decoder_destroy);
+  bpdec_config c{cfg.d_max, cfg.use_pce ? 1 : 0, cfg.use_vnr ? 1 : 0, cfg.q_mode, cfg.msg_clamp};
+  bpdec_stop_rule r{stop.min_frame_errors, stop.max_frames};
+  bpdec_trial_stats st{};
+  std::vector<int64_t> hist(static_cast<size_t>(cfg.d_max) + 1, 0);
+  check_status(bpdec_run_trials(d, point.snr, mask.punctured.data(), static_cast<int32_t>(mask.punctured.size()), &c,
+                                &r, master_seed, block, &st, hist.data()));
+  TrialStats t;
+  t.frames = st.frames;
+  t.frame_errors = st.frame_errors;
+  t.undetected_errors = st.undetected_errors;
+  t.fer = st.fer;
+  t.fer_ci_low = st.fer_ci_low;
+  t.fer_ci_high = st.fer_ci_high;
+  t.d_bar = st.d_bar;
+  t.iteration_sum = st.iteration_sum;
+  for (size_t k = 0; k < hist.size(); ++k)
+    if (hist[k] > 0) t.iteration_histogram[static_cast<int>(k)] = static_cast<long>(hist[k]);
+  t.stops_syndrome = st.stops_syndrome;
+  t.stops_vnr = st.stops_vnr;
+  t.stops_max_iter = st.stops_max_iter;
+  t.hit_max_frames = st.hit_max_frames != 0;
+  return t;
+}
 
 // ≙ etdec::decode (decoder.hpp:78-79): throwaway decoder.
 inline DecodeOutcome decode(const ParityCheckMatrix& code, std::span<const double> llr_in, const ActiveVarSet& active,

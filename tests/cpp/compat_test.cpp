@@ -33,11 +33,19 @@ int main(int argc, char** argv) {
   CHECK(threw);
   const std::vector<std::uint8_t> ok_word = {1, 1, 0};
   CHECK(ed::syndrome_check(h, ok_word));
-  CHECK(std::fabs(ed::snr_for_beta(0.95, 0.1) - 0.15711023728271978) < 1e-15);
+  const ed::ChannelPoint pt = ed::snr_for_beta(0.95, 0.1);  // channel.hpp:14-23
+  CHECK(std::fabs(pt.snr - 0.15711023728271978) < 1e-15 && pt.beta == 0.95 && pt.rate == 0.1);
+  CHECK(std::fabs(pt.sigma2 * pt.snr - 1.0) < 1e-15);
+  const auto wi = ed::wilson_interval(0, 10);  // channel.cpp:63-72
+  CHECK(wi.first == 0.0 && wi.second > 0.27 && wi.second < 0.28);
   const auto lift = ed::lift_protograph({{3, 3}}, 1024, 1);
   CHECK(lift.n_vars() == 2048 && lift.n_checks() == 1024 && lift.n_edges() == 6144);
   CHECK(ed::active_var_set(lift).members.size() == 2048);
   CHECK(std::strcmp(ed::to_string(ed::StopReason::kVnrDrop), "vnr_drop") == 0);
+  // puncturing (puncture.cpp:16-48): round(N - (N-M)/target) degree>=2 positions
+  const auto pm = ed::apply_puncture(lift, 0.6, 3);
+  CHECK(pm.punctured.size() == static_cast<size_t>(std::lround(2048 - 1024 / 0.6)));
+  CHECK(ed::no_puncture(lift).empty() && std::fabs(ed::no_puncture(lift).effective_rate - 0.5) < 1e-15);
 
   if (!gpu) {
     bool dev_err = false;
@@ -71,6 +79,20 @@ int main(int argc, char** argv) {
     threw = true;
   }
   CHECK(threw);
+  // Monte-Carlo harness (channel.cpp:74-156): statistics independent of the
+  // block size, histogram consistent with the frame count
+  ed::DecodeConfig tc;
+  tc.d_max = 60;
+  tc.use_vnr = true;
+  const ed::StopRule rule{20, 200};
+  const auto t1 = ed::run_trials(lift, pm, ed::snr_for_beta(0.6, pm.effective_rate), tc, rule, 9, 1);
+  const auto t4 = ed::run_trials(lift, pm, ed::snr_for_beta(0.6, pm.effective_rate), tc, rule, 9, 4);
+  CHECK(t1.frames > 0 && t1.frames == t4.frames && t1.frame_errors == t4.frame_errors);
+  CHECK(t1.iteration_sum == t4.iteration_sum && t1.iteration_histogram == t4.iteration_histogram);
+  long hsum = 0;
+  for (const auto& kv : t1.iteration_histogram) hsum += kv.second;
+  CHECK(hsum == t1.frames && t1.stops_syndrome + t1.stops_vnr + t1.stops_max_iter == t1.frames);
+  CHECK(t1.fer >= 0.0 && t1.fer <= 1.0 && t1.fer_ci_low <= t1.fer && t1.fer <= t1.fer_ci_high);
   std::printf("compat_test (gpu) OK\n");
   return 0;
 }
