@@ -2453,7 +2453,10 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   // step loop: poll the frames-done counter with a lag so the GPU never idles
   const int64_t waves = (static_cast<int64_t>(B) + S - 1) / S;
   int64_t max_steps = static_cast<int64_t>(p.d_max) * waves + 2;
-  constexpr int kLag = 4;
+  // lag 2: the GPU always has the next step queued, and at most two empty
+  // steps run after the last frame stops (lag 1/2/4 measured: 2 keeps slack
+  // for a busy host at no cost)
+  constexpr int kLag = 2;
   int64_t step = 0;
   bool done = false;
   bool uploading = up_llr || up_syn;
