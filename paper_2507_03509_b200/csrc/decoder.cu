@@ -108,7 +108,8 @@ struct Args {
   int32_t* counters;        // [0] next frame, [1] frames done, [2] error flags, [3] active slots,
                             // [4] active slots at the last compaction, [5] k_compact blocks done,
                             // [6] k_var tiles handed out, [7] k_check chunks handed out,
-                            // [8] k_decide blocks done, [9] frames available (uploaded)
+                            // [8] k_decide blocks done, [9] frames available (uploaded),
+                            // [10] k_decide syndrome passes handed out
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
@@ -1052,7 +1053,10 @@ __global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {
   int32_t* sve1 = sve0 + a.ve_stride;
   int32_t* sptr = sve1 + a.ve_stride;
   const long long total = static_cast<long long>(a.G) * a.n_tiles;
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[7] = 0;  // k_check chunk scheduler (next step)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.counters[7] = 0;   // k_check chunk scheduler (next step)
+    a.counters[10] = 0;  // k_decide syndrome passes (this step)
+  }
   long long w = var_grab(a, lane);
   while (w < total) {
     const int d = __ldg(&a.vtile[static_cast<int>(w % a.n_tiles)]).x;
@@ -1086,9 +1090,8 @@ __global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {
 // ^ the hard-decision words of its degree>=2 edges, which k_var stored per
 // edge in check-major order (ebits): the check's words are contiguous, so
 // the pass streams instead of gathering.  A group is skipped as soon as
-// every active frame in it is known to fail; new failing frames are
-// published at once (block-local copy first, so about one global atomic per
-// block and group).
+// every active frame in it is known to fail (global fail masks, re-read per
+// pass); new failing frames are published at once.
 __device__ __forceinline__ uint32_t ldu32_pred(const uint32_t* p, bool pred) {
   uint32_t v = 0u;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.u32 %0, [%1];\n\t}"
@@ -1099,28 +1102,30 @@ __device__ __forceinline__ uint32_t ldu32_pred(const uint32_t* p, bool pred) {
 
 constexpr int kSynChunks = 4;  // chunks per warp pass (their loads are in flight together)
 
-// Syndrome part of k_decide: block `b` of `nb` syndrome blocks.
-__device__ __forceinline__ void syndrome_block(const Args& a, int b, int nb, uint32_t* s_grp) {
-  // group state cached per block: active masks (constant during the pass)
-  // and the failing frames known so far (global at block start | this block)
-  uint32_t* s_act = s_grp;
-  uint32_t* s_fail = s_grp + a.G;
-  for (int t = threadIdx.x; t < a.G; t += blockDim.x) {
-    s_act[t] = a.group_active[t];
-    s_fail[t] = *reinterpret_cast<volatile uint32_t*>(&a.fail[t]);
-  }
+// Syndrome part of k_decide.  Warps grab passes (kSynChunks chunks) from
+// counters[10] (reset by k_var) and, before each, re-read the published
+// failing frames: once every active frame is known to fail — in the high-FER
+// regime after the first round of passes — the warps stop, so the pass costs
+// about one round of loads instead of a sweep over all checks.
+__device__ __forceinline__ void syndrome_block(const Args& a, uint32_t* s_act) {
+  for (int t = threadIdx.x; t < a.G; t += blockDim.x) s_act[t] = a.group_active[t];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int chunks = (a.M + 31) / 32;
   const int passes = (chunks + kSynChunks - 1) / kSynChunks;
-  const int nwarps = nb * static_cast<int>(blockDim.x >> 5);
-  for (int q = b * static_cast<int>(blockDim.x >> 5) + static_cast<int>(threadIdx.x >> 5); q < passes; q += nwarps) {
-    bool live = false;  // any group with an active frame not yet known to fail (lanes scan groups)
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(&a.counters[10], 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= passes) break;
+    bool live = false;  // any group with an active frame not yet known to fail
     for (int g0 = 0; g0 < a.G && !live; g0 += 32) {
       const int g = g0 + lane;
-      live = __any_sync(0xffffffffu, g < a.G && s_act[g] != 0u && (s_fail[g] & s_act[g]) != s_act[g]);
+      const uint32_t am = g < a.G ? s_act[g] : 0u;
+      const uint32_t fl = g < a.G ? __ldcg(&a.fail[g]) : 0u;
+      live = __any_sync(0xffffffffu, am != 0u && (fl & am) != am);
     }
-    if (!live) continue;  // warp-uniform
+    if (!live) break;  // warp-uniform: nothing left to prove this step
     int e0[kSynChunks], nh[kSynChunks];
     bool valid[kSynChunks];
 #pragma unroll
@@ -1139,33 +1144,36 @@ __device__ __forceinline__ void syndrome_block(const Args& a, int b, int nb, uin
       }
       if (!valid[u]) nh[u] = 0;
     }
-    for (int g = 0; g < a.G; ++g) {
-      const uint32_t amask = s_act[g];
-      const uint32_t fl = s_fail[g];
-      if (amask == 0u || (fl & amask) == amask) continue;  // warp-uniform
-      const uint32_t* eb = a.ebits + static_cast<size_t>(g) * a.EH;
-      const uint32_t* sp = a.synp + static_cast<size_t>(g) * a.M;
-      uint32_t word[kSynChunks];
+    for (int g0 = 0; g0 < a.G; g0 += 32) {
+      const int gl = g0 + lane;
+      const uint32_t aml = gl < a.G ? s_act[gl] : 0u;
+      const uint32_t fll = gl < a.G ? __ldcg(&a.fail[gl]) : 0u;
+      uint32_t need = __ballot_sync(0xffffffffu, aml != 0u && (fll & aml) != aml);
+      while (need) {  // warp-uniform
+        const int k = __ffs(need) - 1;
+        need &= need - 1;
+        const int g = g0 + k;
+        const uint32_t amask = __shfl_sync(0xffffffffu, aml, k);
+        const uint32_t fl = __shfl_sync(0xffffffffu, fll, k);
+        const uint32_t* eb = a.ebits + static_cast<size_t>(g) * a.EH;
+        const uint32_t* sp = a.synp + static_cast<size_t>(g) * a.M;
+        uint32_t word[kSynChunks];
 #pragma unroll
-      for (int u = 0; u < kSynChunks; ++u) {
-        const int c = (q * kSynChunks + u) * 32 + lane;
-        word[u] = ldu32_pred(sp + (valid[u] ? c : 0), valid[u]);
+        for (int u = 0; u < kSynChunks; ++u) {
+          const int c = (q * kSynChunks + u) * 32 + lane;
+          word[u] = ldu32_pred(sp + (valid[u] ? c : 0), valid[u]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) word[u] ^= ldu32_pred(eb + e0[u] + (j < nh[u] ? j : 0), j < nh[u]);
-      }
-      uint32_t any = 0u;
+          for (int j = 0; j < 4; ++j) word[u] ^= ldu32_pred(eb + e0[u] + (j < nh[u] ? j : 0), j < nh[u]);
+        }
+        uint32_t any = 0u;
 #pragma unroll
-      for (int u = 0; u < kSynChunks; ++u) {
-        for (int j = 4; j < nh[u]; ++j) word[u] ^= eb[e0[u] + j];  // checks with more than 4 such edges
-        any |= word[u];
+        for (int u = 0; u < kSynChunks; ++u) {
+          for (int j = 4; j < nh[u]; ++j) word[u] ^= eb[e0[u] + j];  // checks with more than 4 such edges
+          any |= word[u];
+        }
+        any = __reduce_or_sync(0xffffffffu, any & amask);
+        if (lane == 0 && (any & ~fl) != 0u) atomicOr(&a.fail[g], any);  // published at once
       }
-      any = __reduce_or_sync(0xffffffffu, any & amask);
-      // new failing frames: block-local copy first, published at once
-      if (lane == 0 && (any & ~fl) != 0u) {
-        atomicOr(&s_fail[g], any);
-        atomicOr(&a.fail[g], any);
-      }
-      __syncwarp();
     }
   }
 }
@@ -1293,18 +1301,18 @@ __device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
 // Syndrome, q^(k) and the stop decision of a step in one launch.  Blocks
 // [0, syn_blocks): bit-sliced parity of every check vs its target
 // (decoder.cpp:19-30), streaming synp and the check's contiguous ebits,
-// OR-reduced fail masks; a group is skipped once every active frame in it is
-// known to fail.  Blocks [syn_blocks, syn_blocks + G*kTermBlocks): the fixed
+// OR-reduced fail masks, dynamically handed-out passes; the warps stop once
+// every active frame is known to fail.  Blocks [syn_blocks, syn_blocks + G*kTermBlocks): the fixed
 // -order q partial tree.  The last block to finish (counters[8]) takes the
 // decisions for all groups, one warp per group.
 __global__ void __launch_bounds__(kThreads) k_decide(const Args a, int syn_blocks) {
   pdl_begin();
-  extern __shared__ uint32_t s_grp[];  // [2][G] (syndrome blocks)
+  extern __shared__ uint32_t s_grp[];  // [G] active masks (syndrome blocks)
   __shared__ double red[kThreads / 32][kLanes];
   __shared__ int s_last;
   const int b = blockIdx.x;
   if (b < syn_blocks) {
-    syndrome_block(a, b, syn_blocks, s_grp);
+    syndrome_block(a, s_grp);
   } else {
     const int qb = b - syn_blocks;
     q_block(a, qb / kTermBlocks, qb - (qb / kTermBlocks) * kTermBlocks, red);
@@ -2242,7 +2250,7 @@ void GpuDecoder::init(const Code& code, int max_slots) {
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_var<1>, kVarWarps * 32, var_smem));
     grid_var = sms * std::max(1, per_sm);
   }
-  grid_syn = sms * 8;
+  grid_syn = sms * 2;  // syndrome warps grab passes dynamically (k_decide)
   // load / extract are no-ops on most steps: keep their grids small
   turn_item_blocks = sms * 8;
   turn_check_blocks = sms * 2;
@@ -2331,7 +2339,7 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
   {
     const int syn_blocks = a.use_pce ? grid_syn : 0;
     launch(kSyn, st, [&] {
-      launch_pdl(k_decide, syn_blocks + G * kTermBlocks, kThreads, 2 * G * sizeof(uint32_t), st, a, syn_blocks);
+      launch_pdl(k_decide, syn_blocks + G * kTermBlocks, kThreads, G * sizeof(uint32_t), st, a, syn_blocks);
     });
   }
   launch(kTurnover, st, [&] { launch_turnover(a, st, want_post); });
