@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -109,11 +110,14 @@ struct Args {
                             // [4] active slots at the last compaction, [5] k_compact blocks done,
                             // [6] k_var tiles handed out, [7] k_check chunks handed out,
                             // [8] k_decide blocks done, [9] frames available (uploaded),
-                            // [10] k_decide syndrome passes handed out
+                            // [10] k_decide syndrome passes handed out, [11] lane width of
+                            // the live groups' layout (32, or 16 / 8 for a narrow tail group),
+                            // [12] slots were moved (k_compact) since the last k_check
   unsigned long long* frame_iters;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
   float clamp;
+  int32_t narrow_ok;          // the tail group may be re-laid out narrow (check degree <= 4, G >= 2)
   // inputs / outputs (device)
   const float* in_llr;        // [batch][N]
   const uint32_t* in_syn;     // [batch][MW] or null
@@ -130,6 +134,15 @@ __device__ __forceinline__ float clampf(float x, float c) { return fminf(fmaxf(x
 __device__ __forceinline__ uint32_t signbit_u(float x) { return __float_as_uint(x) >> 31; }
 __device__ __forceinline__ float with_sign(float mag, uint32_t s) {
   return __uint_as_float(__float_as_uint(mag) | (s << 31));
+}
+
+// Per-slot arrays are [group][row][32 lanes].  A group that is the only
+// live one in the decoder's tail can be re-laid out "narrow": its <= lw
+// (16 or 8) live frames in lanes 0..lw-1 and rows of lw floats
+// ([group][row][lw] inside the group's block), so a row is one or two
+// sectors instead of a 128-byte line (see k_compact).  `lw` is 32 otherwise.
+__device__ __forceinline__ size_t rix(int g, int64_t rows, int64_t row, int lw) {
+  return static_cast<size_t>(g) * static_cast<size_t>(rows) * kLanes + static_cast<size_t>(row) * lw;
 }
 
 // Streaming loads/stores for the once-per-iteration message traffic; the
@@ -245,7 +258,7 @@ struct CheckState {
 
 template <int MAXD>
 __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, int g, const int4 d, uint32_t sword,
-                                           const int32_t* hh, int lane, bool act, bool first) {
+                                           const int32_t* hh, int lane, bool act, bool first, int lw) {
   constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
   s.d = d;
   s.nh = d.y - d.x;
@@ -260,15 +273,15 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
       if (j < s.nh) {
         const int h = hh[j];
         if (act) {
-          const float p = a.post[(static_cast<size_t>(g) * a.NV + h) * kLanes + lane];
-          const float co = first ? 0.0f : ld_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + d.x + j) * kLanes + lane]);
+          const float p = a.post[rix(g, a.NV, h, lw) + lane];
+          const float co = first ? 0.0f : ld_stream(&a.c2v[rix(g, a.EH, d.x + j, lw) + lane]);
           v = first ? p : clampf(p - co, a.clamp);
         }
         s.l1[j] = 0.0f;
       } else {
         const int dd = d.z + (j - s.nh);
         float l = 0.0f;
-        if (act) l = ld_stream(&a.llr_d[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane]);
+        if (act) l = ld_stream(&a.llr_d[rix(g, a.N1, dd, lw) + lane]);
         s.l1[j] = l;
         v = first ? l : clampf(l, a.clamp);
       }
@@ -310,7 +323,7 @@ __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&ou
 }
 
 template <int MAXD, bool WANT_POST>
-__device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>& s, int g, int lane, bool act) {
+__device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>& s, int g, int lane, bool act, int lw) {
   constexpr int kUnroll = MAXD <= 16 ? MAXD : 1;
   const int deg = s.deg;
   const int lim = MAXD <= 16 ? MAXD : deg;
@@ -351,7 +364,7 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
     if (j < deg) {
       const float o = with_sign(out[j], par ^ signbit_u(s.m[j]));
       if (j < s.nh) {
-        if (act) st_stream(&a.c2v[(static_cast<size_t>(g) * a.EH + s.d.x + j) * kLanes + lane], o);
+        if (act) st_stream(&a.c2v[rix(g, a.EH, s.d.x + j, lw) + lane], o);
       } else {
         const int dd = s.d.z + (j - s.nh);
         const float pd = s.l1[j] + o;  // posterior of the degree-1 variable
@@ -359,7 +372,7 @@ __device__ __forceinline__ uint32_t check_finish(const Args& a, CheckState<MAXD>
         dpar ^= bit;
         const uint32_t word = __ballot_sync(0xffffffffu, bit);
         if (lane == 0) a.d1bits[static_cast<size_t>(g) * a.N1 + dd] = word;
-        if (WANT_POST && act) a.d1post[(static_cast<size_t>(g) * a.N1 + dd) * kLanes + lane] = pd;
+        if (WANT_POST && act) a.d1post[rix(g, a.N1, dd, lw) + lane] = pd;
       }
     }
   }
@@ -417,64 +430,83 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 
 // Stage layout for a batch of K checks: [K*NH posterior rows][K*NH c2v rows]
-// [K*ND llr rows].  `q4` = this lane's 16-byte quarter within a row group:
-// row offset (lane/8), float offset 4*(lane%8); `qact` = any of the 4 frames
-// covered by that quarter is active.
-template <int NH, int ND>
+// [K*ND llr rows], rows of LW floats.  `lrow`/`lcol` = this lane's 16-byte
+// piece: a warp instruction moves 128/LW rows (LW = 32: four 128-byte
+// rows); `qact` = any of the 4 frames covered by that piece is active.
+template <int NH, int ND, int LW>
 __device__ __forceinline__ void check_batch_issue(float* stage, const float* post0, const float* c2v0,
                                                   const float* llr0, const int32_t* hh, int i0, int lrow, int lcol,
                                                   bool qact, bool qc2v, uint64_t pol) {
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NPH = K * NH;  // posterior / c2v rows
   constexpr int NPD = K * ND;  // degree-1 rows
+  constexpr int RPI = 128 / LW;  // rows per warp instruction
 #pragma unroll
-  for (int r0 = 0; r0 < NPH; r0 += 4) {
+  for (int r0 = 0; r0 < NPH; r0 += RPI) {
     const int r = r0 + lrow;
     if (r < NPH) {
       const int h = hh[i0 * NH + r];
-      cp_async16(stage + r * kLanes + lcol, post0 + static_cast<size_t>(h) * kLanes + lcol, qact);
-      cp_async16_ef(stage + (NPH + r) * kLanes + lcol, c2v0 + static_cast<size_t>(i0 * NH + r) * kLanes + lcol, qc2v,
-                    pol);
+      cp_async16(stage + r * LW + lcol, post0 + static_cast<size_t>(h) * LW + lcol, qact);
+      cp_async16_ef(stage + (NPH + r) * LW + lcol, c2v0 + static_cast<size_t>(i0 * NH + r) * LW + lcol, qc2v, pol);
     }
   }
 #pragma unroll
-  for (int r0 = 0; r0 < NPD; r0 += 4) {
+  for (int r0 = 0; r0 < NPD; r0 += RPI) {
     const int r = r0 + lrow;
     if (r < NPD)
-      cp_async16_ef(stage + (2 * NPH + r) * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol, qact,
-                    pol);
+      cp_async16_ef(stage + (2 * NPH + r) * LW + lcol, llr0 + static_cast<size_t>(i0 + r) * LW + lcol, qact, pol);
   }
   cp_async_commit();
 }
 
 // FM: some lane of the warp is in its first iteration (v2c = channel LLR,
 // unclamped, no previous c2v).  The steady state runs the FM = false copy.
-template <int NH, int ND, bool WANT_POST, bool FM>
+//
+// LW < 32 (narrow group, steady state only): the warp is folded — lane
+// (q = lane / LW, f = lane % LW) computes check kb + q of each sub-batch of
+// FE = min(32/LW, K) checks for the frame in lane f — so a narrow group
+// costs ~LW/32 of the instructions as well as of the bytes.  The arithmetic
+// of every (check, frame) is that of LW = 32; the 32-bit words (degree-1
+// hard bits, syndrome part) of check kb + qq are bits qq*LW .. of one ballot.
+template <int NH, int ND, bool WANT_POST, bool FM, int LW>
 __device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p,
                                                     const uint32_t* ssyn, int i0, int lane, bool act, bool first,
                                                     float cl, float clamp, uint32_t* synw, uint32_t* d1w) {
   constexpr int D = NH + ND;
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NPH = K * NH;
+  constexpr int F = 32 / LW;
+  constexpr int FE = F < K ? F : K;  // checks per folded step
   constexpr uint32_t kSign = 0x80000000u;
+  const int q = LW == 32 ? 0 : lane / LW;
+  const int f = LW == 32 ? lane : lane % LW;
+  const bool qok = q < FE;
+  const bool on = act && qok;
+  // this lane's rows: check kb + q of sub-batch kb
+  const float* sp = stage + f + q * NH * LW;          // posterior rows
+  const float* sc = stage + f + (NPH + q * NH) * LW;  // previous c2v rows
+  const float* sl = stage + f + (2 * NPH + q) * LW;   // degree-1 llr rows
+  float* cq = c2vg + q * NH * LW;
+  float* dq = WANT_POST ? d1p + q * LW : nullptr;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
+  for (int kb = 0; kb < K; kb += FE) {
     float m[D > 0 ? D : 1];      // |v2c|, clamped (cl = inf in the first iteration)
     uint32_t sm[D > 0 ? D : 1];  // sign masks of v2c (the clamp keeps the sign)
     float l = 0.0f;
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const float c = stage[(NPH + k * NH + j) * kLanes];
-      const float v = stage[(k * NH + j) * kLanes] - (FM && first ? 0.0f : c);
+      const float c = sc[(kb * NH + j) * LW];
+      const float v = sp[(kb * NH + j) * LW] - (FM && first ? 0.0f : c);
       m[j] = fminf(fabsf(v), FM ? cl : clamp);
       sm[j] = __float_as_uint(v) & kSign;
     }
     if (ND) {
-      l = stage[(2 * NPH + k) * kLanes];
+      l = sl[kb * LW];
       m[NH] = fminf(fabsf(l), FM ? cl : clamp);
       sm[NH] = __float_as_uint(l) & kSign;
     }
-    const uint32_t sbit = (ssyn[i0 + k] >> lane) & 1u;
+    const int ci = i0 + kb + (qok ? q : 0);  // this lane's check (chunk-local)
+    const uint32_t sbit = (ssyn[ci] >> f) & 1u;
     uint32_t par = sbit << 31;  // sign of the product times (1 - 2 s_c)
 #pragma unroll
     for (int j = 0; j < D; ++j) par ^= sm[j];
@@ -483,38 +515,56 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const float o = __uint_as_float(__float_as_uint(out[j]) | (par ^ sm[j]));
-      stcs_pred(c2vg + static_cast<size_t>((i0 + k) * NH + j) * kLanes, o, act);
+      stcs_pred(cq + static_cast<size_t>((i0 + kb) * NH + j) * LW, o, on);
     }
     uint32_t dbit = 0u;
     if (ND) {
       const float o = __uint_as_float(__float_as_uint(out[NH]) | (par ^ sm[NH]));
       const float pd = l + o;  // posterior of the degree-1 variable
-      dbit = (act && pd < 0.0f) ? 1u : 0u;
-      if (WANT_POST) st_pred(d1p + static_cast<size_t>(i0 + k) * kLanes, pd, act);
-      const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
-      if (lane == i0 + k) *d1w = dw;
+      dbit = (on && pd < 0.0f) ? 1u : 0u;
+      if (WANT_POST) st_pred(dq + static_cast<size_t>(i0 + kb) * LW, pd, on);
     }
-    const uint32_t sw = __ballot_sync(0xffffffffu, sbit ^ dbit);
-    if (lane == i0 + k) *synw = sw;
+    if constexpr (LW == 32) {
+      if (ND) {
+        const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
+        if (lane == ci) *d1w = dw;
+      }
+      const uint32_t sw = __ballot_sync(0xffffffffu, sbit ^ dbit);
+      if (lane == ci) *synw = sw;
+    } else {
+      constexpr uint32_t kMask = (1u << LW) - 1u;
+      const uint32_t bd = ND ? __ballot_sync(0xffffffffu, dbit) : 0u;
+      const uint32_t bs = __ballot_sync(0xffffffffu, qok && ((sbit ^ dbit) & 1u));
+#pragma unroll
+      for (int qq = 0; qq < FE; ++qq) {
+        if (lane == i0 + kb + qq) {
+          if (ND) *d1w = (bd >> (qq * LW)) & kMask;
+          *synw = (bs >> (qq * LW)) & kMask;
+        }
+      }
+    }
   }
 }
 
-template <int NH, int ND, bool WANT_POST, bool FM, int RING>
+template <int NH, int ND, bool WANT_POST, bool FM, int RING, int LW = 32>
 __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   constexpr int K = CheckShape<NH, ND>::K;
   constexpr int NB = 32 / K;
-  const float* post0 = a.post + static_cast<size_t>(g) * a.NV * kLanes;
-  const float* c2v0 = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes;
-  const float* llr0 = a.llr_d + (static_cast<size_t>(g) * a.N1 + db) * kLanes;
-  float* c2vg = a.c2v + (static_cast<size_t>(g) * a.EH + hb) * kLanes + lane;
-  float* d1p = WANT_POST ? a.d1post + (static_cast<size_t>(g) * a.N1 + db) * kLanes + lane : nullptr;
+  const int f = LW == 32 ? lane : lane % LW;  // this lane's frame (slot lane)
+  if (LW < 32) act = (amask >> f) & 1u;
+  const float* post0 = a.post + rix(g, a.NV, 0, LW);
+  const float* c2v0 = a.c2v + rix(g, a.EH, hb, LW);
+  const float* llr0 = a.llr_d + rix(g, a.N1, db, LW);
+  float* c2vg = a.c2v + rix(g, a.EH, hb, LW) + f;
+  float* d1p = WANT_POST ? a.d1post + rix(g, a.N1, db, LW) + f : nullptr;
   const float clamp = a.clamp;
   const float cl = first ? __int_as_float(0x7f800000) : clamp;
-  // this lane's 16-byte quarter: frames 4*(lane%8) .. +3 of row group member lane/8
-  const int lrow = lane >> 3;
-  const int lcol = (lane & 7) * 4;
+  // this lane's 16-byte piece: frames lcol .. lcol+3 of row lrow of a row group
+  constexpr int QPR = LW / 4;  // 16-byte pieces per row
+  const int lrow = lane / QPR;
+  const int lcol = (lane % QPR) * 4;
   const uint32_t qbits = (amask >> lcol) & 0xFu;
   const bool qact = qbits != 0u;
   const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
@@ -526,8 +576,7 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p) {
     if (p < NB)
-      check_batch_issue<NH, ND>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v,
-                                pol);
+      check_batch_issue<NH, ND, LW>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v, pol);
     else
       cp_async_commit();
   }
@@ -535,15 +584,15 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
     if (b + NS - 1 < NB)
-      check_batch_issue<NH, ND>(ring + slot_i * RS, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow,
-                                lcol, qact, qc2v, pol);
+      check_batch_issue<NH, ND, LW>(ring + slot_i * RS, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow, lcol, qact,
+                                    qc2v, pol);
     else
       cp_async_commit();
     if (++slot_i == NS) slot_i = 0;
     cp_async_wait<NS - 1>();
     __syncwarp();  // rows were copied by other lanes
-    check_batch_compute<NH, ND, WANT_POST, FM>(ring + lane + slot_c * RS, c2vg, d1p, ssyn, b * K,
-                                               lane, act, first, cl, clamp, synw, d1w);
+    check_batch_compute<NH, ND, WANT_POST, FM, LW>(ring + slot_c * RS, c2vg, d1p, ssyn, b * K, lane, act, first, cl,
+                                                   clamp, synw, d1w);
     if (++slot_c == NS) slot_c = 0;
     __syncwarp();  // stage is refilled in the next round
   }
@@ -552,36 +601,48 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 // SPLIT_FM: a separate steady-state copy (no first-iteration lanes) of the
 // chunk loop.  Kernels for codes with heavy check types (MAXD >= 6) keep the
 // general copy only: twice the typed code would thrash the instruction cache.
-template <int NH, int ND, bool WANT_POST, bool SPLIT_FM, int RING>
+// Narrow groups (LW < 32) never have first-iteration lanes (the frame queue
+// is drained before a group is narrowed).
+template <int NH, int ND, bool WANT_POST, bool SPLIT_FM, int RING, int LW>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                   const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                   uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
-  if (!SPLIT_FM || fmask)
+  if constexpr (LW < 32)
+    check_chunk_loop<NH, ND, WANT_POST, false, RING, LW>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, 0u,
+                                                         synw, d1w);
+  else if (!SPLIT_FM || fmask)
     check_chunk_loop<NH, ND, WANT_POST, true, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
-                                              d1w);
+                                                    d1w);
   else
-    check_chunk_loop<NH, ND, WANT_POST, false, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
-                                               d1w);
+    check_chunk_loop<NH, ND, WANT_POST, false, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask,
+                                                     synw, d1w);
 }
 
-template <int MAXD, bool WANT_POST>
-__global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 5 blocks/SM, 96 regs: measured best
-  pdl_begin();
-  constexpr bool kStage = MAXD <= 16;
-  constexpr int kHH = kStage ? 32 * MAXD : 1;
-  __shared__ int4 s_desc[kCheckThreads / 32][32];
-  __shared__ uint32_t s_syn[kCheckThreads / 32][32];
-  __shared__ int32_t s_hh[kCheckThreads / 32][kHH];
+template <int MAXD>
+struct CheckSmem {
+  static constexpr bool kStage = MAXD <= 16;
+  static constexpr int kHH = kStage ? 32 * MAXD : 1;
   // ring rows per warp: 80 (four stages of the heaviest typed batch) where
   // the static shared memory allows it, else 60
-  constexpr int kRing = MAXD <= 4 ? 80 : kRingRows;
-  __shared__ __align__(16) float s_ring[kCheckThreads / 32][kRing * kLanes];
-  if (blockIdx.x == 0) {
-    for (int t = threadIdx.x; t < a.G; t += blockDim.x) a.fail[t] = 0u;
-    if (threadIdx.x == 0) a.counters[6] = 0;  // k_var tile scheduler (this step)
-  }
+  static constexpr int kRing = MAXD <= 4 ? 80 : kRingRows;
+  int4 desc[kCheckThreads / 32][32];
+  uint32_t syn[kCheckThreads / 32][32];
+  int32_t hh[kCheckThreads / 32][kHH];
+  __align__(16) float ring[kCheckThreads / 32][kRing * kLanes];
+};
+
+// The chunk loop of k_check for groups laid out with lane width LW.
+template <int MAXD, bool WANT_POST, int LW>
+__device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
+  constexpr bool kStage = CheckSmem<MAXD>::kStage;
+  constexpr int kRing = CheckSmem<MAXD>::kRing;
+  auto& s_desc = sm.desc;
+  auto& s_syn = sm.syn;
+  auto& s_hh = sm.hh;
+  auto& s_ring = sm.ring;
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
+  const bool moved = __ldcg(&a.counters[12]) != 0;
   const int chunks = (a.M + 31) / 32;
   const long long total = static_cast<long long>(a.G) * chunks;
   // dynamic chunk schedule (counters[7], generic chunks first), one grab ahead
@@ -599,8 +660,9 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
     const uint32_t fmask = __ballot_sync(0xffffffffu, act && first);
     const int4 cdk = __ldg(&a.ctype[ch]);
     const int type = kStage ? cdk.x : -1;
-    // degree-1 checks only change in a frame's first iteration
-    if ((type == 1 || type == 8) && fmask == 0u) {
+    // degree-1 checks only change in a frame's first iteration (and their
+    // bit words must follow frames that k_compact moved)
+    if ((type == 1 || type == 8) && fmask == 0u && !moved) {
       w = sched_resolve(a, kpend, lane, chunks, a.csched);
       continue;
     }
@@ -624,8 +686,8 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
 #define BPDEC_TYPED(NH_, ND_)                                                                       \
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
-      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= 4), kRing>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], lane, act, \
-                                             first, amask, fmask, &synw, &d1w);                     \
+      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= 4), kRing, LW>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], \
+                                             lane, act, first, amask, fmask, &synw, &d1w);          \
     else                                                                                            \
       typed = false;                                                                                \
     break;
@@ -652,17 +714,17 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
         CheckState<MAXD> A, B;
         const int4 dA = s_desc[wi][j];
         check_load<MAXD>(a, A, g, dA, s_syn[wi][j], kStage ? &s_hh[wi][dA.x - hb0] : &a.chk_hi_h[dA.x], lane, act,
-                         first);
+                         first, LW);
         const bool hasB = j + 1 < nc;
         if (hasB) {
           const int4 dB = s_desc[wi][j + 1];
           check_load<MAXD>(a, B, g, dB, s_syn[wi][j + 1], kStage ? &s_hh[wi][dB.x - hb0] : &a.chk_hi_h[dB.x], lane,
-                           act, first);
+                           act, first, LW);
         }
-        const uint32_t wa = check_finish<MAXD, WANT_POST>(a, A, g, lane, act);
+        const uint32_t wa = check_finish<MAXD, WANT_POST>(a, A, g, lane, act, LW);
         if (lane == j) synw = wa;
         if (hasB) {
-          const uint32_t wb = check_finish<MAXD, WANT_POST>(a, B, g, lane, act);
+          const uint32_t wb = check_finish<MAXD, WANT_POST>(a, B, g, lane, act, LW);
           if (lane == j + 1) synw = wb;
         }
       }
@@ -670,6 +732,30 @@ __global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 
     if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = synw;
     w = sched_resolve(a, kpend, lane, chunks, a.csched);
   }
+}
+
+template <int MAXD, bool WANT_POST>
+__global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 5 blocks/SM, 96 regs: measured best
+  pdl_begin();
+  __shared__ CheckSmem<MAXD> sm;
+  if (blockIdx.x == 0) {
+    for (int t = threadIdx.x; t < a.G; t += blockDim.x) a.fail[t] = 0u;
+    if (threadIdx.x == 0) a.counters[6] = 0;  // k_var tile scheduler (this step)
+  }
+  // lane width of the live groups' layout (narrow tail, k_compact); only
+  // codes with check degree <= 4 are ever narrowed
+  const int lw = MAXD <= 4 ? __ldcg(&a.counters[11]) : 32;
+  if constexpr (MAXD <= 4) {
+    if (lw == 8) {
+      check_body<MAXD, WANT_POST, 8>(a, sm);
+      return;
+    }
+    if (lw == 16) {
+      check_body<MAXD, WANT_POST, 16>(a, sm);
+      return;
+    }
+  }
+  check_body<MAXD, WANT_POST, 32>(a, sm);
 }
 
 // --------------------------------------------------------------- k_var --
@@ -696,16 +782,22 @@ constexpr int kVarMaxTyped = 32;   // largest tile degree on the typed (streamed
 // variable spans SB batches of R rows (its llr row, then its c2v rows in
 // ascending check order); the posterior sum is carried across them in
 // order.
-template <int D>
+template <int D, int LW = 32>
 struct VarShape {
+  // narrow groups (LW < 32): rows are LW floats, so the same ring bytes hold
+  // 32/LW times the rows and a batch holds up to 4 variables (the fold)
+  static constexpr int kStage = kVarStageRows * (32 / LW);
+  static constexpr int kRing = kVarRingRows * (32 / LW);
   static constexpr int RV = D + 1;  // rows per variable
-  static constexpr bool kSplit = RV > kVarStageRows;
-  static constexpr int K = kSplit ? 1
-                           : (kVarStageRows / RV >= 8 ? 8 : (kVarStageRows / RV >= 4 ? 4 : (kVarStageRows / RV >= 2 ? 2 : 1)));
-  static constexpr int SB = kSplit ? (RV + kVarStageRows - 1) / kVarStageRows : 1;  // batches per variable
-  static constexpr int ROWS = kSplit ? (RV + SB - 1) / SB : K * RV;                 // rows per batch
-  static constexpr int NS = kVarRingRows / ROWS >= 6 ? 6 : kVarRingRows / ROWS;     // ring stages
-  static constexpr int NB = 32 / K * SB;                                            // batches per chunk
+  static constexpr bool kSplit = RV > kStage;
+  static constexpr int K0 = kSplit ? 1
+                            : (kStage / RV >= 8 ? 8 : (kStage / RV >= 4 ? 4 : (kStage / RV >= 2 ? 2 : 1)));
+  static constexpr int K = LW < 32 && K0 > 4 ? 4 : K0;
+  static constexpr int SB = kSplit ? (RV + kStage - 1) / kStage : 1;  // batches per variable
+  static constexpr int ROWS = kSplit ? (RV + SB - 1) / SB : K * RV;    // rows per batch
+  static constexpr int NB = 32 / K * SB;                              // batches per chunk
+  static constexpr int NS0 = kRing / ROWS >= 6 ? 6 : kRing / ROWS;      // ring stages
+  static constexpr int NS = LW < 32 && NS0 > (NB + 1) / 2 ? (NB + 1) / 2 : NS0;
   static_assert(NS >= 2, "variable batch too large for the ring");
   static_assert(D <= kVarMaxTyped, "typed variable path limited to degree 32");
 };
@@ -713,89 +805,118 @@ struct VarShape {
 // Batch b of a chunk (variables i0 .. of the chunk).  Edge id -1 pads a
 // variable of lower degree to the tile degree D, and variables at or beyond
 // `nval` pad the last tile: their copies are predicated off, which
-// zero-fills the stage rows (+0.0 leaves the ordered sum unchanged).
-template <int D>
+// zero-fills the stage rows (+0.0 leaves the ordered sum unchanged).  Rows
+// of LW floats (narrow groups: LW = 16 / 8, see rix).
+template <int D, int LW>
 __device__ __forceinline__ void var_batch_issue(float* stage, const float* llr0, const float* c2vg, const int32_t* ve,
                                                 int b, int nval, int lrow, int lcol, bool qact, uint64_t pol) {
-  using S = VarShape<D>;
+  using S = VarShape<D, LW>;
   constexpr int K = S::K;
+  constexpr int RPI = 128 / LW;  // rows per warp instruction
   if constexpr (!S::kSplit) {
     const int i0 = b * K;
 #pragma unroll
-    for (int r0 = 0; r0 < K; r0 += 4) {
+    for (int r0 = 0; r0 < K; r0 += RPI) {
       const int r = r0 + lrow;
       if (r < K)
-        cp_async16_ef(stage + r * kLanes + lcol, llr0 + static_cast<size_t>(i0 + r) * kLanes + lcol,
-                      qact && i0 + r < nval, pol);
+        cp_async16_ef(stage + r * LW + lcol, llr0 + static_cast<size_t>(i0 + r) * LW + lcol, qact && i0 + r < nval,
+                      pol);
     }
 #pragma unroll
-    for (int r0 = 0; r0 < K * D; r0 += 4) {
+    for (int r0 = 0; r0 < K * D; r0 += RPI) {
       const int r = r0 + lrow;
       if (r < K * D) {
         const int e = ve[i0 * D + r];
-        cp_async16_ef(stage + (K + r) * kLanes + lcol,
-                      c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0)) * kLanes) + lcol, qact && e >= 0,
-                      pol);
+        cp_async16_ef(stage + (K + r) * LW + lcol,
+                      c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0))) * LW + lcol, qact && e >= 0, pol);
       }
     }
   } else {
     const int i = b / S::SB;
     const int g0 = (b - i * S::SB) * S::ROWS;  // first variable row of this batch
 #pragma unroll
-    for (int r0 = 0; r0 < S::ROWS; r0 += 4) {
+    for (int r0 = 0; r0 < S::ROWS; r0 += RPI) {
       const int r = r0 + lrow;
       const int gr = g0 + r;
       if (r < S::ROWS && gr < S::RV) {
         const int e = gr > 0 ? ve[i * D + gr - 1] : 0;
-        const float* src = gr == 0 ? llr0 + static_cast<size_t>(i) * kLanes
-                                   : c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0)) * kLanes);
-        cp_async16_ef(stage + r * kLanes + lcol, src + lcol, qact && (gr == 0 ? i < nval : e >= 0), pol);
+        const float* src = gr == 0 ? llr0 + static_cast<size_t>(i) * LW
+                                   : c2vg + static_cast<size_t>(static_cast<uint32_t>(max(e, 0))) * LW;
+        cp_async16_ef(stage + r * LW + lcol, src + lcol, qact && (gr == 0 ? i < nval : e >= 0), pol);
       }
     }
   }
 }
 
-template <int D, int QMODE>
-__device__ __forceinline__ void var_finish(float p, float* postg, uint32_t* ebg, const int32_t* ve, int i, int nval,
-                                           int lane, bool act, double& acc, uint32_t& hw) {
-  const bool on = act && i < nval;
-  st_pred(postg + static_cast<size_t>(i) * kLanes, p, on);
-  if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
-  const uint32_t word = __ballot_sync(0xffffffffu, on && p < 0.0f);
-  if (lane == (i & 31)) hw = word;
+// Outputs of variables i0 .. i0+FE-1 (posterior p of this lane's frame f and
+// variable i0 + q; `act` = that frame is live and the lane not idle):
+// posterior row, q partial, hard-decision word (hbits via hw, and every
+// edge's ebits).  Folded (FE > 1): `p` of variable i0 + qq is fetched from
+// lane qq*LW + f, so the q partial is summed in variable order exactly as
+// with LW = 32.
+template <int D, int QMODE, int LW, int FE>
+__device__ __forceinline__ void var_finish(float p, float* postg, uint32_t* ebg, const int32_t* ve, int i0, int nval,
+                                           int lane, int q, int f, bool act, double& acc, uint32_t& hw) {
+  const bool on = act && i0 + q < nval;
+  st_pred(postg + static_cast<size_t>(i0 + q) * LW, p, on);
+  if constexpr (FE == 1) {
+    if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
+  } else {
 #pragma unroll
-  for (int j0 = 0; j0 < D; j0 += 32) {
-    const int j = j0 + lane;
-    const int e = ve[i * D + (j < D ? j : 0)];
-    st_pred_u32(ebg + static_cast<uint32_t>(max(e, 0)), word, j < D && e >= 0);
+    for (int qq = 0; qq < FE; ++qq) {  // this frame's posteriors in variable order
+      const float pv = __shfl_sync(0xffffffffu, p, qq * LW + f);
+      if (act && i0 + qq < nval) acc += QMODE == 0 ? static_cast<double>(pv) : static_cast<double>(fabsf(pv));
+    }
+  }
+  const uint32_t bal = __ballot_sync(0xffffffffu, on && p < 0.0f);
+#pragma unroll
+  for (int qq = 0; qq < FE; ++qq) {
+    const int i = i0 + qq;
+    const uint32_t word = LW == 32 ? bal : (bal >> (qq * LW)) & ((1u << (LW & 31)) - 1u);
+    if (lane == (i & 31)) hw = word;
+#pragma unroll
+    for (int j0 = 0; j0 < D; j0 += 32) {
+      const int j = j0 + lane;
+      const int e = ve[i * D + (j < D ? j : 0)];
+      st_pred_u32(ebg + static_cast<uint32_t>(max(e, 0)), word, j < D && e >= 0);
+    }
   }
 }
 
-template <int D, int QMODE>
+template <int D, int QMODE, int LW>
 __device__ __forceinline__ void var_batch_compute(const float* stage, float* postg, uint32_t* ebg, const int32_t* ve,
                                                   int b, int nval, int lane, bool act, double& acc, uint32_t& hw,
                                                   float& carry) {
-  using S = VarShape<D>;
+  using S = VarShape<D, LW>;
   constexpr int K = S::K;
+  constexpr int F = S::kSplit ? 1 : 32 / LW;
+  constexpr int FE = F < K ? F : K;  // variables per folded step
+  const int qr = LW == 32 ? 0 : lane / LW;  // lanes with qr >= FE idle (q = 0 keeps their reads in range)
+  const int q = qr < FE ? qr : 0;
+  const int f = LW == 32 ? lane : lane % LW;
   if constexpr (!S::kSplit) {
     const int i0 = b * K;
+    const bool on = act && qr < FE;
+    const float* st = stage + f + q * LW;
+    const float* sc = stage + f + (K + q * D) * LW;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      float p = stage[k * kLanes];
+    for (int kb = 0; kb < K; kb += FE) {
+      float p = st[kb * LW];
 #pragma unroll
-      for (int j = 0; j < D; ++j) p += stage[(K + k * D + j) * kLanes];  // ascending check order (decoder.cpp:101)
-      var_finish<D, QMODE>(p, postg, ebg, ve, i0 + k, nval, lane, act, acc, hw);
+      for (int j = 0; j < D; ++j) p += sc[(kb * D + j) * LW];  // ascending check order (decoder.cpp:101)
+      var_finish<D, QMODE, LW, FE>(p, postg, ebg, ve, i0 + kb, nval, lane, q, f, on, acc, hw);
     }
   } else {
     const int i = b / S::SB;
     const int sub = b - i * S::SB;
     const int n = min(S::ROWS, S::RV - sub * S::ROWS);  // rows of this batch
-    float p = sub == 0 ? stage[0] : carry + stage[0];
+    const float* st = stage + f;
+    float p = sub == 0 ? st[0] : carry + st[0];
 #pragma unroll
     for (int j = 1; j < S::ROWS; ++j)
-      if (j < n) p += stage[j * kLanes];  // ascending check order (decoder.cpp:101)
+      if (j < n) p += st[j * LW];  // ascending check order (decoder.cpp:101)
     if (sub == S::SB - 1)
-      var_finish<D, QMODE>(p, postg, ebg, ve, i, nval, lane, act, acc, hw);
+      var_finish<D, QMODE, LW, 1>(p, postg, ebg, ve, i, nval, lane, 0, f, act && lane < LW, acc, hw);
     else
       carry = p;
   }
@@ -851,7 +972,7 @@ struct VarChunk {
   const float* c2v0;  // c2v of the group
 };
 
-template <int D>
+template <int D, int LW>
 __device__ __forceinline__ VarChunk var_chunk(const Args& a, const VarTile& t, int half) {
   VarChunk c;
   c.g = t.g;
@@ -860,28 +981,30 @@ __device__ __forceinline__ VarChunk var_chunk(const Args& a, const VarTile& t, i
   c.kb = t.kb + half * 32 * D;
   c.nval = max(0, min(32, a.NV - (t.h0 + half * 32)));
   c.am = a.group_active[t.g];
-  c.llr0 = a.llr_h + (static_cast<size_t>(t.g) * a.NH + t.h0 + half * 32) * kLanes;
-  c.c2v0 = a.c2v + static_cast<size_t>(t.g) * a.EH * kLanes;
+  c.llr0 = a.llr_h + rix(t.g, a.NH, t.h0 + half * 32, LW);
+  c.c2v0 = a.c2v + rix(t.g, a.EH, 0, LW);
   return c;
 }
 
 // Runs this warp's degree-D tiles (starting with grabbed tile w) as one
 // pipeline over their chunks; returns the next grabbed tile it did not take.
-template <int D, int QMODE>
+template <int D, int QMODE, int LW>
 __device__ long long var_stream(const Args& a, long long w, long long total, int32_t* sve0, int32_t* sve1,
                                 float* ring, int lane) {
-  constexpr int NS = VarShape<D>::NS;
-  constexpr int NB = VarShape<D>::NB;  // batches per chunk
-  constexpr int RS = VarShape<D>::ROWS * kLanes;  // stage stride
+  constexpr int NS = VarShape<D, LW>::NS;
+  constexpr int NB = VarShape<D, LW>::NB;          // batches per chunk
+  constexpr int RS = VarShape<D, LW>::ROWS * LW;   // stage stride (floats)
   int32_t* ve_c = sve0;  // edge ids of cur
   int32_t* ve_n = sve1;  // edge ids of nxt
   static_assert(NB >= 2 * NS - 1, "the next chunk's edge ids must land before its first batch is issued");
-  const int lrow = lane >> 3;
-  const int lcol = (lane & 7) * 4;
+  constexpr int QPR = LW / 4;  // 16-byte pieces per row
+  const int lrow = lane / QPR;
+  const int lcol = (lane % QPR) * 4;
+  const int f = LW == 32 ? lane : lane % LW;  // this lane's frame (slot lane)
   const uint64_t pol = policy_evict_first();
 
   VarTile tile = var_tile(a, w);
-  VarChunk cur = var_chunk<D>(a, tile, 0), nxt = cur;
+  VarChunk cur = var_chunk<D, LW>(a, tile, 0), nxt = cur;
   bool has_nxt = false;
   long long w_after = total;  // the tile grabbed after the current one
   int2 desc_after = make_int2(-1, 0);
@@ -904,7 +1027,7 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
   auto issue_at = [&](int pos) {
     const bool in_cur = pos < NB;
     if (in_cur || has_nxt) {
-      var_batch_issue<D>(ring + slot_issue * RS, in_cur ? llr_c : llr_n, in_cur ? c2v_c : c2v_n,
+      var_batch_issue<D, LW>(ring + slot_issue * RS, in_cur ? llr_c : llr_n, in_cur ? c2v_c : c2v_n,
                          in_cur ? ve_c : ve_n, in_cur ? pos : pos - NB, in_cur ? nval_c : nval_n, lrow,
                          lcol, in_cur ? qact_c : qact_n, pol);
     }
@@ -919,7 +1042,7 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
     // if it has the same degree.  The grab was issued a chunk earlier and its
     // descriptor loaded during the first half, so neither latency is exposed.
     if (cur.half == 0) {
-      nxt = var_chunk<D>(a, tile, 1);
+      nxt = var_chunk<D, LW>(a, tile, 1);
       has_nxt = true;
       w_after = var_grab_resolve(a, kpend, lane);
       if (w_after < total) desc_after = __ldg(&a.vtile[static_cast<int>(w_after % a.n_tiles)]);
@@ -927,7 +1050,7 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
       has_nxt = w_after < total && desc_after.x == D;
       if (has_nxt) {
         tile = var_tile(a, w_after, desc_after.y);
-        nxt = var_chunk<D>(a, tile, 0);
+        nxt = var_chunk<D, LW>(a, tile, 0);
         kpend = var_grab_issue(a, lane);
       }
     }
@@ -938,9 +1061,9 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
       nval_n = nxt.nval;
       qact_n = ((nxt.am >> lcol) & 0xFu) != 0u;
     }
-    const bool act = (cur.am >> lane) & 1u;
+    const bool act = (cur.am >> f) & 1u;
     const size_t hv = static_cast<size_t>(cur.g) * a.NV + static_cast<size_t>(cur.tile) * kQTile + cur.half * 32;
-    float* postg = a.post + hv * kLanes + lane;
+    float* postg = a.post + rix(cur.g, a.NV, static_cast<int64_t>(cur.tile) * kQTile + cur.half * 32, LW) + f;
     uint32_t* ebg = a.ebits + static_cast<size_t>(cur.g) * a.EH;
     double acc = 0.0;
     uint32_t hw = 0u;
@@ -950,8 +1073,8 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
       issue_at(b + NS - 1);
       cp_async_wait<NS - 1>();
       __syncwarp();  // rows (and the next chunk's edge ids) were copied by other lanes
-      var_batch_compute<D, QMODE>(ring + lane + slot_comp * RS, postg, ebg, ve_c, b, cur.nval, lane, act, acc, hw,
-                                  carry);
+      var_batch_compute<D, QMODE, LW>(ring + slot_comp * RS, postg, ebg, ve_c, b, cur.nval, lane, act, acc, hw,
+                                      carry);
       if (++slot_comp == NS) slot_comp = 0;
       __syncwarp();  // stage is refilled in the next round
     }
@@ -977,14 +1100,14 @@ __device__ long long var_stream(const Args& a, long long w, long long total, int
 }
 
 // ve points at the edge ids of CSC slot `kb` (staged copy or global array).
-__device__ __forceinline__ float var_sum(const Args& a, size_t gl, size_t ge, int h, int k0, int k1,
-                                         const int32_t* ve, int kb, int lane) {
-  float p = ld_stream(&a.llr_h[(gl + h) * kLanes + lane]);
+__device__ __forceinline__ float var_sum(const Args& a, int g, int h, int k0, int k1, const int32_t* ve, int kb,
+                                         int lane, int lw) {
+  float p = ld_stream(&a.llr_h[rix(g, a.NH, h, lw) + lane]);
   for (int k = k0; k < k1; k += 8) {
     float v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      v[u] = (k + u < k1) ? ld_stream(&a.c2v[(ge + ve[k + u - kb]) * kLanes + lane]) : 0.0f;
+      v[u] = (k + u < k1) ? ld_stream(&a.c2v[rix(g, a.EH, ve[k + u - kb], lw) + lane]) : 0.0f;
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (k + u < k1) p += v[u];  // ascending check order (decoder.cpp:101)
@@ -995,11 +1118,10 @@ __device__ __forceinline__ float var_sum(const Args& a, size_t gl, size_t ge, in
 // Generic tile (mixed degrees, partial, or degree > 12): per variable,
 // register gathers.
 template <int QMODE>
-__device__ void var_tile_generic(const Args& a, long long w, int32_t* sptr, int lane) {
+__device__ void var_tile_generic(const Args& a, long long w, int32_t* sptr, int lane, int lw) {
   const VarTile t = var_tile(a, w);
   const uint32_t amask = a.group_active[t.g];
-  const bool act = (amask >> lane) & 1u;
-  const size_t gl = static_cast<size_t>(t.g) * a.NH;
+  const bool act = lane < lw && ((amask >> lane) & 1u);
   const size_t gv = static_cast<size_t>(t.g) * a.NV;
   const size_t ge = static_cast<size_t>(t.g) * a.EH;
   double acc = 0.0, acc0 = 0.0;
@@ -1021,8 +1143,8 @@ __device__ void var_tile_generic(const Args& a, long long w, int32_t* sptr, int 
       const int k0 = sptr[i], k1 = sptr[i + 1];
       float p = 0.0f;
       if (act) {
-        p = var_sum(a, gl, ge, h, k0, k1, a.vedge + k0, k0, lane);
-        a.post[(gv + h) * kLanes + lane] = p;
+        p = var_sum(a, t.g, h, k0, k1, a.vedge + k0, k0, lane, lw);
+        a.post[rix(t.g, a.NV, h, lw) + lane] = p;
         acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
       }
       const uint32_t word = __ballot_sync(0xffffffffu, act && p < 0.0f);
@@ -1041,6 +1163,47 @@ __host__ __device__ constexpr size_t var_smem_per_warp(int ve_stride) {
   return static_cast<size_t>(kVarRingRows) * kLanes * 4 + 2 * static_cast<size_t>(ve_stride) * 4 + 36 * 4;
 }
 
+// The tile loop of k_var for groups laid out with lane width LW (narrow
+// groups: typed streams for tile degrees <= 16, the generic path otherwise).
+template <int QMODE, int LW>
+__device__ __forceinline__ void var_body(const Args& a, float* ring, int32_t* sve0, int32_t* sve1, int32_t* sptr,
+                                         int lane) {
+  const long long total = static_cast<long long>(a.G) * a.n_tiles;
+  long long w = var_grab(a, lane);
+  while (w < total) {
+    const int d = __ldg(&a.vtile[static_cast<int>(w % a.n_tiles)]).x;
+    switch (d) {
+#define BPDEC_VSTREAM(D_)                                                     \
+  case D_:                                                                    \
+    w = var_stream<D_, QMODE, LW>(a, w, total, sve0, sve1, ring, lane);       \
+    continue;
+#define BPDEC_VSTREAM_WIDE(D_)                                                \
+  case D_:                                                                    \
+    if constexpr (LW == 32) {                                                 \
+      w = var_stream<D_, QMODE, LW>(a, w, total, sve0, sve1, ring, lane);     \
+      continue;                                                               \
+    }                                                                         \
+    break;
+      BPDEC_VSTREAM(2)
+      BPDEC_VSTREAM(3)
+      BPDEC_VSTREAM(4)
+      BPDEC_VSTREAM(6)
+      BPDEC_VSTREAM(8)
+      BPDEC_VSTREAM(12)
+      BPDEC_VSTREAM(16)
+      BPDEC_VSTREAM_WIDE(20)
+      BPDEC_VSTREAM_WIDE(24)
+      BPDEC_VSTREAM_WIDE(32)
+#undef BPDEC_VSTREAM
+#undef BPDEC_VSTREAM_WIDE
+      default:
+        break;
+    }
+    var_tile_generic<QMODE>(a, w, sptr, lane, LW);
+    w = var_grab(a, lane);
+  }
+}
+
 template <int QMODE>
 __global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {
   pdl_begin();  // 5 blocks/SM: measured best
@@ -1052,36 +1215,18 @@ __global__ void __launch_bounds__(kVarWarps * 32, 5) k_var(const Args a) {
   int32_t* sve0 = reinterpret_cast<int32_t*>(base + kVarRingRows * kLanes * 4);
   int32_t* sve1 = sve0 + a.ve_stride;
   int32_t* sptr = sve1 + a.ve_stride;
-  const long long total = static_cast<long long>(a.G) * a.n_tiles;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.counters[7] = 0;   // k_check chunk scheduler (next step)
     a.counters[10] = 0;  // k_decide syndrome passes (this step)
+    a.counters[12] = 0;  // moved slots: k_check of this step has rewritten their degree-1-check words
   }
-  long long w = var_grab(a, lane);
-  while (w < total) {
-    const int d = __ldg(&a.vtile[static_cast<int>(w % a.n_tiles)]).x;
-    switch (d) {
-#define BPDEC_VSTREAM(D_)                                                     \
-  case D_:                                                                    \
-    w = var_stream<D_, QMODE>(a, w, total, sve0, sve1, ring, lane);           \
-    continue;
-      BPDEC_VSTREAM(2)
-      BPDEC_VSTREAM(3)
-      BPDEC_VSTREAM(4)
-      BPDEC_VSTREAM(6)
-      BPDEC_VSTREAM(8)
-      BPDEC_VSTREAM(12)
-      BPDEC_VSTREAM(16)
-      BPDEC_VSTREAM(20)
-      BPDEC_VSTREAM(24)
-      BPDEC_VSTREAM(32)
-#undef BPDEC_VSTREAM
-      default:
-        break;
-    }
-    var_tile_generic<QMODE>(a, w, sptr, lane);
-    w = var_grab(a, lane);
-  }
+  const int lw = __ldcg(&a.counters[11]);  // lane width of the live groups (narrow tail)
+  if (lw == 8)
+    var_body<QMODE, 8>(a, ring, sve0, sve1, sptr, lane);
+  else if (lw == 16)
+    var_body<QMODE, 16>(a, ring, sve0, sve1, sptr, lane);
+  else
+    var_body<QMODE, 32>(a, ring, sve0, sve1, sptr, lane);
 }
 
 // ------------------------------------------------- k_decide: syndrome part --
@@ -1351,7 +1496,7 @@ constexpr int kMaxGroups = 1024;  // worklist capacity (slots <= 32768)
 constexpr int kSparseLoad = 8;    // at most this many entering frames per group: direct scatter path
 
 template <bool WANT_POST>
-__device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm, int ch, int lane) {
+__device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm, int ch, int lane, int lw) {
   const int i = ch * 32 + lane;
   const bool valid = i < a.N;
   const int vm = valid ? __ldg(&a.vmap[i]) : 0;
@@ -1362,14 +1507,14 @@ __device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm,
     if (vm >= 0) {
       if (vm < a.NV) {
         word = a.hbits[static_cast<size_t>(g) * a.NV + vm];
-        prow = a.post + (static_cast<size_t>(g) * a.NV + vm) * kLanes;
+        prow = a.post + rix(g, a.NV, vm, lw);
       } else {  // degree-0 variable: posterior = channel LLR
-        prow = a.llr_h + (static_cast<size_t>(g) * a.NH + vm) * kLanes;
+        prow = a.llr_h + rix(g, a.NH, vm, lw);
       }
     } else {
       const int dd = -1 - vm;
       word = a.d1bits[static_cast<size_t>(g) * a.N1 + dd];
-      if (WANT_POST) prow = a.d1post + (static_cast<size_t>(g) * a.N1 + dd) * kLanes;
+      if (WANT_POST) prow = a.d1post + rix(g, a.N1, dd, lw);
     }
   }
   while (sm) {
@@ -1530,6 +1675,9 @@ __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_bl
   __syncthreads();
   const int nw = s_n[0], nl = s_n[1];
   if (nw == 0) return;  // nothing to hand over this step
+  // lane width of the live groups (a narrow tail group never refills: the
+  // queue is drained before a group is narrowed)
+  const int lw = __ldcg(&a.counters[11]);
   const int b = blockIdx.x;
   const int quads = (a.NW + kTurnChunks - 1) / kTurnChunks;
   if (b < item_blocks && (WANT_POST || a.NH != a.NV)) {
@@ -1544,7 +1692,7 @@ __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_bl
       const uint32_t lm = a.load_mask[g];
       const int ch0 = qd * kTurnChunks;
       if (sm) {
-        if (warp < kTurnChunks && ch0 + warp < a.NW) extract_chunk<WANT_POST>(a, g, sm, ch0 + warp, lane);
+        if (warp < kTurnChunks && ch0 + warp < a.NW) extract_chunk<WANT_POST>(a, g, sm, ch0 + warp, lane, lw);
         __syncthreads();  // outputs read before the rows are refilled
       }
       if (lm) load_quad_tile(a, g, lm, ch0, tile, lane, warp);
@@ -1569,7 +1717,8 @@ __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_bl
       if (e < ext) {
         const int si = static_cast<int>(e / a.NW);
         const int g = s_sg[si];
-        extract_chunk<WANT_POST>(a, g, a.stopped[g], static_cast<int>(e - static_cast<long long>(si) * a.NW), lane);
+        extract_chunk<WANT_POST>(a, g, a.stopped[g], static_cast<int>(e - static_cast<long long>(si) * a.NW), lane,
+                                 lw);
       } else {
         const long long e2 = e - ext;
         const int pi = static_cast<int>(e2 / a.NW);
@@ -1641,6 +1790,8 @@ constexpr int kMaxMoves = 1024;
 
 struct CompactPlan {
   int n;
+  int narrow;          // 1: re-lay out the only live group narrow (moves = its live lanes, in order)
+  int lw_old, lw_new;  // lane widths before / after (narrow plans)
   int16_t src[kMaxMoves];  // slot indices
   int16_t dst[kMaxMoves];
 };
@@ -1648,6 +1799,7 @@ struct CompactPlan {
 __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   // single thread
   pl.n = 0;
+  pl.narrow = 0;
   const int G = a.G;
   if (G > kMaxCompactGroups || G < 2) return;
   if (a.counters[0] < a.batch) return;  // frames still queued: freed slots get refilled instead
@@ -1658,6 +1810,31 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
     alive += cnt[g] > 0;
   }
   const int need = (total + 31) / 32;
+  if (alive == 1 && a.narrow_ok) {
+    // tail: the only live group holds <= 16 (<= 8) frames -> move them into
+    // another (free) group laid out with 16 (8) lanes per row, so every
+    // later pass moves 64 (32) bytes per row instead of a 128-byte line and
+    // runs lane-folded (k_check / k_var)
+    int gs = 0;
+    while (cnt[gs] == 0) ++gs;
+    const int n = cnt[gs];
+    const int lw_old = a.counters[11];
+    const int lw_new = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+    if (lw_new >= lw_old) return;
+    const int gd = gs == 0 ? 1 : 0;
+    uint32_t m = a.group_active[gs];
+    for (int f = 0; f < n; ++f) {
+      const int ls = __ffs(m) - 1;
+      m &= m - 1;
+      pl.src[f] = static_cast<int16_t>(gs * kLanes + ls);
+      pl.dst[f] = static_cast<int16_t>(gd * kLanes + f);
+    }
+    pl.n = n;
+    pl.narrow = 1;
+    pl.lw_old = lw_old;
+    pl.lw_new = lw_new;
+    return;
+  }
   if (alive <= need) return;
   if (total > a.counters[4] - 32) return;  // hysteresis: re-pack only after 32 more frames finished
   // targets: the `need` fullest groups (ties -> lower index); the rest are sources
@@ -1695,6 +1872,66 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   }
 }
 
+// Narrowing move (plan.narrow): element (row r, lane f) of the target group
+// = (row r, lane src_f) of the source group, every per-slot array, rows of
+// lw_new floats in the target; then the target syndrome words (bit f = bit
+// src_f), and the last block moves the slot state and sets counters[11].
+__device__ void compact_narrow(const Args& a, const CompactPlan& pl, int& s_last) {
+  const int n = pl.n, lwo = pl.lw_old, lwn = pl.lw_new;
+  const int gs = pl.src[0] >> 5, gd = pl.dst[0] >> 5;
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
+  const int f = static_cast<int>(tid % lwn);  // constant per thread (nth is a multiple of lwn)
+  const int ls = f < n ? (pl.src[f] & 31) : 0;
+  float* arrs[5] = {a.c2v, a.post, a.llr_h, a.llr_d, a.d1post};
+  const long long rows[5] = {a.EH, a.NV, a.NH, a.N1, a.d1post != nullptr ? a.N1 : 0};
+  for (int k = 0; k < 5; ++k) {
+    const long long R = rows[k];
+    if (R == 0) continue;
+    const float* src = arrs[k] + rix(gs, R, 0, lwo) + ls;
+    float* dst = arrs[k] + rix(gd, R, 0, lwn) + f;
+    // thread = (row, lane f): 8 rows in flight per thread
+    constexpr int kU = 8;
+    const long long step = nth / lwn;
+    for (long long r0 = tid / lwn; r0 < R; r0 += step * kU) {
+      float v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const long long r = r0 + u * step;
+        v[u] = (f < n && r < R) ? src[r * lwo] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const long long r = r0 + u * step;
+        if (r < R) dst[r * lwn] = v[u];  // lanes f >= n: zero (idle)
+      }
+    }
+  }
+  for (long long c = tid; c < a.M; c += nth) {
+    const uint32_t w = a.syn_target[static_cast<size_t>(gs) * a.M + c];
+    uint32_t nw = 0u;
+    for (int k = 0; k < n; ++k) nw |= ((w >> (pl.src[k] & 31)) & 1u) << k;
+    a.syn_target[static_cast<size_t>(gd) * a.M + c] = nw;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[5], 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  a.counters[5] = 0;
+  for (int k = 0; k < n; ++k) {
+    const int s = pl.src[k], d = pl.dst[k];
+    a.slot_iter[d] = a.slot_iter[s];
+    a.slot_frame[d] = a.slot_frame[s];
+    a.qprev[d] = a.qprev[s];
+  }
+  a.group_active[gs] = 0u;
+  a.group_active[gd] = (1u << n) - 1u;
+  a.counters[11] = lwn;
+  a.counters[12] = 1;
+}
+
 // One launch: every block computes the (identical) plan, moves its share of
 // rows — warp = one row, lane = one move, so a row moves as one 128-byte
 // read and write — and the last block to finish commits the slot state
@@ -1708,6 +1945,10 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Args a) {
   __syncthreads();
   const int n = pl.n;
   if (n == 0) return;  // same decision in every block
+  if (pl.narrow) {
+    compact_narrow(a, pl, s_last);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const long long rows_e = a.EH, rows_v = a.NV, rows_h = a.NH, rows_d = a.N1;
   const bool post_d = a.d1post != nullptr;
@@ -1778,6 +2019,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Args a) {
     a.group_active[s >> 5] &= ~(1u << (s & 31));
     a.group_active[d >> 5] |= 1u << (d & 31);
   }
+  a.counters[12] = 1;  // degree-1-only checks are recomputed for the moved frames
 }
 
 // Start of a decode: frames 0..first-1 go to slots 0..first-1, per-decode
@@ -1795,6 +2037,7 @@ __global__ void k_decode_init(const Args a, int first, int avail) {
     a.counters[threadIdx.x] = threadIdx.x == 0 ? first
                               : threadIdx.x == 4 ? a.G * kLanes + 32
                               : threadIdx.x == 9 ? avail
+                              : threadIdx.x == 11 ? kLanes
                                                  : 0;
   if (threadIdx.x == 0) *a.frame_iters = 0ull;
 }
@@ -1930,6 +2173,7 @@ class GpuDecoder {
   int device = 0;
   int64_t dev_bytes = 0;
   bool profiling = false;
+  bool no_narrow = false;  // BPDEC_NO_NARROW set at construction
   double prof_ms[kNumKernels] = {};
   int64_t prof_launches[kNumKernels] = {};
   double prof_frame_iters = 0.0;
@@ -2003,6 +2247,7 @@ void GpuDecoder::init(const Code& code, int max_slots) {
   if (prop.major < 10) {
     throw CudaError(std::string("device ") + prop.name + " is not sm_100-class; this build targets sm_100a only");
   }
+  if (const char* e = std::getenv("BPDEC_NO_NARROW")) no_narrow = e[0] != '\0' && e[0] != '0';
   if (max_slots < 1) throw ValidationError("decoder: max_slots must be positive");
   if (max_slots > 32 * kMaxGroups) throw ValidationError("decoder: max_slots above 32768 is not supported");
   S = (max_slots + 31) / 32 * 32;
@@ -2370,6 +2615,10 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   a.use_vnr = p.use_vnr;
   a.q_mode = p.q_mode;
   a.clamp = p.msg_clamp;
+  // narrow tail groups: the folded check paths exist for check degree <= 4
+  // (k_check<3|4>); a free group to move into needs G >= 2.
+  // BPDEC_NO_NARROW=1 keeps every group wide (tests compare both).
+  a.narrow_ok = (max_check_deg <= 4 && G >= 2 && !no_narrow) ? 1 : 0;
 
   // inputs (a host batch staged earlier by stage_inputs is used in place:
   // its copy already ran on copy_stream)

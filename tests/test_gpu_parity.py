@@ -401,6 +401,64 @@ def test_tail_compaction_is_transparent(P, cfg1_code):
         assert np.array_equal(o.q_trace[0], r.q_trace[f], equal_nan=True)
 
 
+def _decode_all(dec, llr, s, cfg):
+    return dec.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True)
+
+
+def _assert_same(a, b, idx=None):
+    sel = slice(None) if idx is None else idx
+    assert np.array_equal(a.iterations, b.iterations[sel]) and np.array_equal(a.reasons, b.reasons[sel])
+    assert np.array_equal(a.bits, b.bits[sel])
+    assert np.array_equal(a.posteriors, b.posteriors[sel])
+    assert np.array_equal(a.q_trace, b.q_trace[sel], equal_nan=True)
+
+
+def _with_degree1_checks(P, code, n01=48, n10=24):
+    """The config-1 code plus n01 checks holding one new degree-1 variable
+    each (type (0,1)) and n10 single-edge checks on existing degree>=2
+    variables (type (1,0)) — check types k_check skips after a frame's first
+    iteration."""
+    ptr, var = code.csr()
+    lists = [list(var[ptr[c]:ptr[c + 1]]) for c in range(code.n_checks)]
+    n = code.n_vars
+    lists += [[n + i] for i in range(n01)]
+    hi = np.nonzero(code.var_degrees() >= 2)[0]
+    lists += [[int(v)] for v in hi[:: max(1, len(hi) // n10)][:n10]]
+    return P.ParityCheckMatrix.from_check_lists(n + n01, lists)
+
+
+@pytest.mark.parametrize("kind", ["cfg1", "deg1checks"])
+def test_narrow_tail_bit_exact(P, cfg1_code, kind):
+    """Narrow tail groups (the only live group re-laid out with 16 / 8 lanes
+    per row, lane-folded check and variable passes) and group compaction
+    move frames mid-decode.  Every per-frame output — bits, iterations,
+    reasons, posteriors and the q trace — must equal (a) the all-wide decode
+    (BPDEC_NO_NARROW=1) and (b) decoding the frame alone in a one-group
+    decoder (no moves).  "deg1checks" adds degree-1-only checks, whose
+    words k_check recomputes only in a frame's first iteration or after
+    frames moved."""
+    if kind == "cfg1":
+        code = cfg1_code
+    else:
+        code = _with_degree1_checks(P, cfg1_code)
+        assert (code.check_degrees() == 1).sum() == 48 + 24
+    # VNR: stop times spread at any beta; PCE alone: in the converging regime
+    for pce, vnr, blo, bhi in ((True, True, 0.2, 1.0), (True, False, 0.05, 0.35)):
+        llr, x, s, _ = P.sample_frames_beta(code, blo, bhi, 808, 0, 96)
+        cfg = P.DecodeConfig(d_max=150, use_pce=pce, use_vnr=vnr, q_mode=P.decoder.Q_ABS)
+        r = _decode_all(P.BatchDecoder(code, max_slots=96), llr, s, cfg)  # 3 groups: compaction, narrowing
+        assert len(set(r.iterations.tolist())) > 4, "stop times must spread for the tail to form"
+        os.environ["BPDEC_NO_NARROW"] = "1"
+        try:
+            w = _decode_all(P.BatchDecoder(code, max_slots=96), llr, s, cfg)
+        finally:
+            del os.environ["BPDEC_NO_NARROW"]
+        _assert_same(w, r)
+        one = P.BatchDecoder(code, max_slots=32)
+        for f in list(range(0, 96, 7)) + [int(np.argmax(r.iterations))]:
+            _assert_same(_decode_all(one, llr[f:f + 1], s[f:f + 1], cfg), r, slice(f, f + 1))
+
+
 # ------------------------------------------- BASELINE configs at full size --
 @pytest.mark.parametrize("key,frames,beta,modes,min_nontie", [
     ("cfg2", 4, 0.95, (("vnr", 500), ("pce", 40)), 0.25),
