@@ -32,6 +32,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -2174,6 +2175,8 @@ class GpuDecoder {
   int64_t dev_bytes = 0;
   bool profiling = false;
   bool no_narrow = false;  // BPDEC_NO_NARROW set at construction
+  bool no_eager = false;   // BPDEC_NO_EAGER: host outputs copied after the decode only (A/B knob)
+
   double prof_ms[kNumKernels] = {};
   int64_t prof_launches[kNumKernels] = {};
   double prof_frame_iters = 0.0;
@@ -2218,6 +2221,14 @@ class GpuDecoder {
   int32_t* h_avail = nullptr;
   size_t h_avail_n = 0;
   cudaEvent_t up_start = nullptr, up_first = nullptr, up_done = nullptr;
+  // eager D2H of finished frames' outputs (host output buffers): while the
+  // tail decodes, rows of frames that already stopped are copied on
+  // out_stream (k_decide writes out_iters at the stop; a snapshot of it,
+  // taken after a polled step, says which rows are final)
+  cudaStream_t out_stream = nullptr;
+  int32_t* h_done = nullptr;  // pinned snapshot of out_iters
+  size_t h_done_cap = 0;
+  cudaEvent_t done_ev = nullptr;
   int grid_check = 0, grid_var = 0, grid_syn = 0, sms_ = 148;
   int turn_item_blocks = 0, turn_check_blocks = 0;
   size_t var_smem = 0;
@@ -2248,6 +2259,7 @@ void GpuDecoder::init(const Code& code, int max_slots) {
     throw CudaError(std::string("device ") + prop.name + " is not sm_100-class; this build targets sm_100a only");
   }
   if (const char* e = std::getenv("BPDEC_NO_NARROW")) no_narrow = e[0] != '\0' && e[0] != '0';
+  if (const char* e = std::getenv("BPDEC_NO_EAGER")) no_eager = e[0] != '\0' && e[0] != '0';
   if (max_slots < 1) throw ValidationError("decoder: max_slots must be positive");
   if (max_slots > 32 * kMaxGroups) throw ValidationError("decoder: max_slots above 32768 is not supported");
   S = (max_slots + 31) / 32 * 32;
@@ -2458,6 +2470,8 @@ void GpuDecoder::init(const Code& code, int max_slots) {
 
   CUDA_OK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming));
   for (auto& sg : staged) CUDA_OK(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
   for (cudaEvent_t* e : {&up_start, &up_first, &up_done}) CUDA_OK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CUDA_OK(cudaHostAlloc(&h_counters, kRing * 4 * sizeof(int32_t), cudaHostAllocDefault));
@@ -2519,6 +2533,13 @@ void GpuDecoder::release() noexcept {
     if (e) cudaEventDestroy(e);
   if (h_avail) cudaFreeHost(h_avail);
   h_avail = nullptr;
+  if (h_done) cudaFreeHost(h_done);
+  h_done = nullptr;
+  h_done_cap = 0;
+  if (done_ev) cudaEventDestroy(done_ev);
+  done_ev = nullptr;
+  if (out_stream) cudaStreamDestroy(out_stream);
+  out_stream = nullptr;
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
   owned.clear();
@@ -2670,6 +2691,50 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   a.out_post = static_cast<float*>(dev_out(b.posteriors, B * a.N * sizeof(float), s_post, &st_post));
   a.out_qtrace = static_cast<double*>(dev_out(b.q_trace, B * p.d_max * sizeof(double), s_qtrace, &st_q));
   if (a.out_qtrace) CUDA_OK(cudaMemsetAsync(a.out_qtrace, 0xff, B * p.d_max * sizeof(double), st));  // NaN
+  // eager output copies: per-frame rows of the staged host outputs
+  const size_t row_bits = b.bits_packed ? a.NW * sizeof(uint32_t) : static_cast<size_t>(a.N);
+  const bool eager = (st_bits || st_post || st_q) && a.out_iters != nullptr && !no_eager;
+  std::vector<char> copied;
+  if (eager) {
+    CUDA_OK(cudaMemsetAsync(a.out_iters, 0, B * sizeof(int32_t), st));  // 0 = still decoding
+    if (h_done_cap < B) {
+      if (h_done) cudaFreeHost(h_done);
+      h_done = nullptr;
+      h_done_cap = 0;
+      CUDA_OK(cudaHostAlloc(&h_done, B * sizeof(int32_t), cudaHostAllocDefault));
+      h_done_cap = B;
+    }
+    copied.assign(B, 0);
+  }
+  // copies rows [f0, f1) of every staged per-frame output on stream `s`
+  auto copy_rows = [&](size_t f0, size_t f1, cudaStream_t s) {
+    const size_t n = f1 - f0;
+    if (st_bits)
+      CUDA_OK(cudaMemcpyAsync(static_cast<char*>(b.bits) + f0 * row_bits, static_cast<char*>(d_bits) + f0 * row_bits,
+                              n * row_bits, cudaMemcpyDeviceToHost, s));
+    if (st_post)
+      CUDA_OK(cudaMemcpyAsync(b.posteriors + f0 * a.N, a.out_post + f0 * a.N, n * a.N * sizeof(float),
+                              cudaMemcpyDeviceToHost, s));
+    if (st_q)
+      CUDA_OK(cudaMemcpyAsync(b.q_trace + f0 * p.d_max, a.out_qtrace + f0 * p.d_max, n * p.d_max * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+  };
+  // frames whose snapshot says "stopped" and that are not copied yet, as ranges
+  auto copy_finished = [&](const int32_t* snap, cudaStream_t s, bool all) {
+    size_t f = 0;
+    while (f < B) {
+      if (copied[f] || (!all && snap[f] == 0)) {
+        ++f;
+        continue;
+      }
+      size_t e = f;
+      while (e < B && !copied[e] && (all || snap[e] != 0)) copied[e++] = 1;
+      copy_rows(f, e, s);
+      f = e;
+    }
+  };
+  int64_t last_done_seen = 0;  // frames-done count when the last snapshot was requested
+  bool snap_pending = false;
 
   // initial slot assignment (frames 0..min(B,S)-1 -> slots 0..) and state
   // reset on the device: no host copies, no host synchronisation
@@ -2741,14 +2806,36 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       CUDA_OK(cudaEventSynchronize(ring_ev[old]));
       if (h_counters[4 * old + 2] != 0) break;  // invalid input detected
       if (h_counters[4 * old + 1] >= b.batch) done = true;
+      if (eager) {
+        // a finished snapshot: copy the rows it marks final
+        if (snap_pending && cudaEventQuery(done_ev) == cudaSuccess) {
+          snap_pending = false;
+          copy_finished(h_done, out_stream, false);
+        } else {
+          (void)cudaGetLastError();  // cudaErrorNotReady is not an error here
+        }
+        // frames stopped since the last snapshot: snapshot out_iters after
+        // that polled step (its outputs are extracted by then)
+        const int64_t nd = h_counters[4 * old + 1];
+        if (!snap_pending && !done && nd >= last_done_seen + 8) {
+          last_done_seen = nd;
+          CUDA_OK(cudaStreamWaitEvent(out_stream, ring_ev[old], 0));
+          CUDA_OK(cudaMemcpyAsync(h_done, a.out_iters, B * sizeof(int32_t), cudaMemcpyDeviceToHost, out_stream));
+          CUDA_OK(cudaEventRecord(done_ev, out_stream));
+          snap_pending = true;
+        }
+      }
     }
   }
   CUDA_OK(cudaStreamSynchronize(st));
   if (up_llr || up_syn) CUDA_OK(cudaEventSynchronize(up_done));  // host buffers no longer read
   int32_t ctr[4];
   CUDA_OK(cudaMemcpy(ctr, a.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
-  if (ctr[2] != 0) throw ValidationError("decode: non-finite input LLR");
-  if (ctr[1] < b.batch) throw CudaError("decode: internal error, frames did not terminate");
+  if (ctr[2] != 0 || ctr[1] < b.batch) {
+    if (eager) CUDA_OK(cudaStreamSynchronize(out_stream));  // no copy into the caller's buffers after the throw
+    if (ctr[2] != 0) throw ValidationError("decode: non-finite input LLR");
+    throw CudaError("decode: internal error, frames did not terminate");
+  }
   if (profiling) {
     unsigned long long fi = 0;
     CUDA_OK(cudaMemcpy(&fi, a.frame_iters, sizeof(fi), cudaMemcpyDeviceToHost));
@@ -2761,13 +2848,24 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
     }
     prof_kid.clear();
   }
-  // copy staged outputs back
-  if (st_bits) CUDA_OK(cudaMemcpyAsync(b.bits, d_bits, bits_bytes, cudaMemcpyDeviceToHost, st));
+  // copy staged outputs back (eager: only the rows not copied during the decode)
+  if (eager) {
+    if (snap_pending) {
+      CUDA_OK(cudaEventSynchronize(done_ev));
+      copy_finished(h_done, out_stream, false);
+    }
+    copy_finished(nullptr, st, true);
+  } else {
+    if (st_bits) CUDA_OK(cudaMemcpyAsync(b.bits, d_bits, bits_bytes, cudaMemcpyDeviceToHost, st));
+    if (st_post)
+      CUDA_OK(cudaMemcpyAsync(b.posteriors, a.out_post, B * a.N * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (st_q)
+      CUDA_OK(cudaMemcpyAsync(b.q_trace, a.out_qtrace, B * p.d_max * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   if (st_it) CUDA_OK(cudaMemcpyAsync(b.iterations, a.out_iters, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   if (st_rs) CUDA_OK(cudaMemcpyAsync(b.reasons, a.out_reasons, B, cudaMemcpyDeviceToHost, st));
-  if (st_post) CUDA_OK(cudaMemcpyAsync(b.posteriors, a.out_post, B * a.N * sizeof(float), cudaMemcpyDeviceToHost, st));
-  if (st_q) CUDA_OK(cudaMemcpyAsync(b.q_trace, a.out_qtrace, B * p.d_max * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_OK(cudaStreamSynchronize(st));
+  if (eager) CUDA_OK(cudaStreamSynchronize(out_stream));
 }
 
 void GpuDecoder::stage_inputs(int32_t batch, const float* llr_host, const uint32_t* syn_host) {

@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B of an env knob on the cfg2 bench (device value only): run as  gpu_ab.sh VAR=VALUE
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; rm -f gpurun_out/ab.txt
-for rep in 1 2; do
+for rep in 1 2 3; do
   for mode in base alt; do
     if [ $mode = alt ]; then export $1; else unset ${1%%=*}; fi
     timeout 600 python bench.py --no-cpu-baseline --no-pce-compare ${BENCH_ARGS} > gpurun_out/ab_$mode.log 2>&1
