@@ -427,7 +427,28 @@ def _with_degree1_checks(P, code, n01=48, n10=24):
     return P.ParityCheckMatrix.from_check_lists(n + n01, lists)
 
 
-@pytest.mark.parametrize("kind", ["cfg1", "deg1checks"])
+def _highdeg_code(P):
+    """Check degree <= 3 (sockets dealt round-robin, as the BASELINE
+    generator does) with variables of degree 3, 14, 20, 27 and 36: split
+    variable batches (wide) / unsplit (narrow), tiles padded to 16 / 20 /
+    32, and the generic variable path (degree 36), plus one degree-1
+    variable per check."""
+    classes = [(3, 600), (14, 40), (20, 40), (27, 20), (36, 20)]
+    m = 3000
+    lists = [[] for _ in range(m)]
+    k = 0
+    v = 0
+    for d, n in classes:
+        for _ in range(n):
+            for _ in range(d):
+                lists[k % m].append(v)
+                k += 1
+            v += 1
+    lists = [sorted(c) + [v + j] for j, c in enumerate(lists)]
+    return P.ParityCheckMatrix.from_check_lists(v + m, lists)
+
+
+@pytest.mark.parametrize("kind", ["cfg1", "deg1checks", "highdeg"])
 def test_narrow_tail_bit_exact(P, cfg1_code, kind):
     """Narrow tail groups (the only live group re-laid out with 16 / 8 lanes
     per row, lane-folded check and variable passes) and group compaction
@@ -439,12 +460,20 @@ def test_narrow_tail_bit_exact(P, cfg1_code, kind):
     frames moved."""
     if kind == "cfg1":
         code = cfg1_code
-    else:
+    elif kind == "deg1checks":
         code = _with_degree1_checks(P, cfg1_code)
         assert (code.check_degrees() == 1).sum() == 48 + 24
+    else:
+        code = _highdeg_code(P)
+        assert code.check_degrees().max() <= 4 and code.var_degrees().max() == 36
     # VNR: stop times spread at any beta; PCE alone: in the converging regime
     for pce, vnr, blo, bhi in ((True, True, 0.2, 1.0), (True, False, 0.05, 0.35)):
         llr, x, s, _ = P.sample_frames_beta(code, blo, bhi, 808, 0, 96)
+        if kind == "highdeg":  # a low-rate-like channel where the code's own SNR map does not apply
+            rng = np.random.default_rng(5)
+            mu = rng.uniform(0.2, 1.6, size=(96, 1)) if not vnr else rng.uniform(0.05, 0.6, size=(96, 1))
+            llr = (mu + rng.normal(0.0, 1.0, size=(96, code.n_vars)) * np.sqrt(2 * mu)).astype(np.float32)
+            s = np.zeros_like(s)
         cfg = P.DecodeConfig(d_max=150, use_pce=pce, use_vnr=vnr, q_mode=P.decoder.Q_ABS)
         r = _decode_all(P.BatchDecoder(code, max_slots=96), llr, s, cfg)  # 3 groups: compaction, narrowing
         assert len(set(r.iterations.tolist())) > 4, "stop times must spread for the tail to form"
