@@ -1518,10 +1518,27 @@ __device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm,
       if (WANT_POST) prow = a.d1post + rix(g, a.N1, dd, lw);
     }
   }
+  // frame of every stopped lane in a register (one load, not one per lane)
+  const int fr = ((sm >> lane) & 1u) ? __ldcg(&a.stop_frame[g * kLanes + lane]) : 0;
+  if (!WANT_POST && a.out_bits_u8 == nullptr && a.out_bits_pk != nullptr && !__any_sync(0xffffffffu, deg0)) {
+    // packed bits only: a 32 x 32 bit transpose (lane i: bit f = frame f's
+    // bit of variable i  ->  lane f: bit i) gives every stopped frame's
+    // word of this chunk at once, the same word a ballot per frame gives
+    uint32_t x = word;
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+      const uint32_t mk = k == 16 ? 0x0000ffffu : k == 8 ? 0x00ff00ffu : k == 4 ? 0x0f0f0f0fu : k == 2 ? 0x33333333u
+                                                                                                    : 0x55555555u;
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, k);
+      x = (lane & k) ? ((x & ~mk) | ((y & ~mk) >> k)) : ((x & mk) | ((y & mk) << k));
+    }
+    if ((sm >> lane) & 1u) a.out_bits_pk[static_cast<size_t>(fr) * a.NW + ch] = x;
+    return;
+  }
   while (sm) {
     const int l = __ffs(sm) - 1;
     sm &= sm - 1;
-    const int f = a.stop_frame[g * kLanes + l];
+    const int f = __shfl_sync(0xffffffffu, fr, l);
     uint32_t bit = (word >> l) & 1u;
     float pv = 0.0f;
     if (deg0) {
