@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbpdec.so")
+LIB_PATH = os.environ.get("BPDEC_LIB") or os.path.join(_HERE, "libbpdec.so")  # BPDEC_LIB: A/B of builds
 
 c_i32p = C.POINTER(C.c_int32)
 c_i64p = C.POINTER(C.c_int64)
