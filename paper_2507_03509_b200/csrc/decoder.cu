@@ -434,7 +434,9 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 // [K*ND llr rows], rows of LW floats.  `lrow`/`lcol` = this lane's 16-byte
 // piece: a warp instruction moves 128/LW rows (LW = 32: four 128-byte
 // rows); `qact` = any of the 4 frames covered by that piece is active.
-template <int NH, int ND, int LW>
+// C2V = false: the previous c2v rows are not needed (steady-state (1,1)
+// checks, whose c2v is a constant of the frame, see check_batch_compute).
+template <int NH, int ND, int LW, bool C2V = true>
 __device__ __forceinline__ void check_batch_issue(float* stage, const float* post0, const float* c2v0,
                                                   const float* llr0, const int32_t* hh, int i0, int lrow, int lcol,
                                                   bool qact, bool qc2v, uint64_t pol) {
@@ -448,7 +450,8 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
     if (r < NPH) {
       const int h = hh[i0 * NH + r];
       cp_async16(stage + r * LW + lcol, post0 + static_cast<size_t>(h) * LW + lcol, qact);
-      cp_async16_ef(stage + (NPH + r) * LW + lcol, c2v0 + static_cast<size_t>(i0 * NH + r) * LW + lcol, qc2v, pol);
+      if (C2V)
+        cp_async16_ef(stage + (NPH + r) * LW + lcol, c2v0 + static_cast<size_t>(i0 * NH + r) * LW + lcol, qc2v, pol);
     }
   }
 #pragma unroll
@@ -489,25 +492,33 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   const float* sl = stage + f + (2 * NPH + q) * LW;   // degree-1 llr rows
   float* cq = c2vg + q * NH * LW;
   float* dq = WANT_POST ? d1p + q * LW : nullptr;
+  // steady-state (1,1) check: the c2v to its degree>=2 variable is
+  // (1-2s)*sign(l)*min(|l|, clamp) in every iteration (the degree-1 edge's
+  // v2c is clamp(l)), so it is formed from l instead of being re-read, and
+  // the stored copy (written in the frame's first iteration, moved with the
+  // frame) is not rewritten: 8 bytes per check and frame less per pass
+  constexpr bool kConstC = NH == 1 && ND == 1 && !FM;
 #pragma unroll
   for (int kb = 0; kb < K; kb += FE) {
     float m[D > 0 ? D : 1];      // |v2c|, clamped (cl = inf in the first iteration)
     uint32_t sm[D > 0 ? D : 1];  // sign masks of v2c (the clamp keeps the sign)
     float l = 0.0f;
+    if (ND) l = sl[kb * LW];
+    const int ci = i0 + kb + (qok ? q : 0);  // this lane's check (chunk-local)
+    const uint32_t sbit = (ssyn[ci] >> f) & 1u;
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const float c = sc[(kb * NH + j) * LW];
+      const float c = kConstC ? __uint_as_float(__float_as_uint(fminf(fabsf(l), clamp)) |
+                                                ((sbit << 31) ^ (__float_as_uint(l) & kSign)))
+                              : sc[(kb * NH + j) * LW];
       const float v = sp[(kb * NH + j) * LW] - (FM && first ? 0.0f : c);
       m[j] = fminf(fabsf(v), FM ? cl : clamp);
       sm[j] = __float_as_uint(v) & kSign;
     }
     if (ND) {
-      l = sl[kb * LW];
       m[NH] = fminf(fabsf(l), FM ? cl : clamp);
       sm[NH] = __float_as_uint(l) & kSign;
     }
-    const int ci = i0 + kb + (qok ? q : 0);  // this lane's check (chunk-local)
-    const uint32_t sbit = (ssyn[ci] >> f) & 1u;
     uint32_t par = sbit << 31;  // sign of the product times (1 - 2 s_c)
 #pragma unroll
     for (int j = 0; j < D; ++j) par ^= sm[j];
@@ -516,7 +527,7 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const float o = __uint_as_float(__float_as_uint(out[j]) | (par ^ sm[j]));
-      stcs_pred(cq + static_cast<size_t>((i0 + kb) * NH + j) * LW, o, on);
+      if (!kConstC) stcs_pred(cq + static_cast<size_t>((i0 + kb) * NH + j) * LW, o, on);
     }
     uint32_t dbit = 0u;
     if (ND) {
@@ -577,7 +588,8 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p) {
     if (p < NB)
-      check_batch_issue<NH, ND, LW>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v, pol);
+      check_batch_issue<NH, ND, LW, !(NH == 1 && ND == 1 && !FM)>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow,
+                                                                   lcol, qact, qc2v, pol);
     else
       cp_async_commit();
   }
@@ -585,7 +597,8 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
     if (b + NS - 1 < NB)
-      check_batch_issue<NH, ND, LW>(ring + slot_i * RS, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow, lcol, qact,
+      check_batch_issue<NH, ND, LW, !(NH == 1 && ND == 1 && !FM)>(ring + slot_i * RS, post0, c2v0, llr0, hh,
+                                                                   (b + NS - 1) * K, lrow, lcol, qact,
                                     qc2v, pol);
     else
       cp_async_commit();
