@@ -44,3 +44,21 @@ for inp in ("dev", "host"):
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) / K * 1e3
         print(f"in={inp:4s} out={outk:4s} {dt:.3f} ms/call")
+
+# device inputs with an unrelated 276 MB H2D copy in flight during each call
+# (is the staged-input cost the DMA's interference with the decode?)
+junk_h = torch.empty((F, N), dtype=torch.float32, pin_memory=True)
+junk_d = torch.empty((F, N), dtype=torch.float32, device="cuda")
+cs = torch.cuda.Stream()
+out = outs["dev"]
+for rep in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(K):
+        with torch.cuda.stream(cs):
+            junk_d.copy_(junk_h, non_blocking=True)
+        dec.decode_batch(d_llr, cfg, syndrome=d_syn, packed=True, out=out)
+        int(out["iterations"].sum().item())
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / K * 1e3
+print(f"in=dev  out=dev  + concurrent 276 MB H2D: {dt:.3f} ms/call")
