@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -2320,10 +2321,24 @@ void GpuDecoder::init(const Code& code, int max_slots) {
       else ++cnd[c];
     }
   }
+  // within a type, checks follow their first (lowest device index)
+  // degree>=2 variable: the c2v rows a tile of consecutive variables gathers
+  // in the variable pass — every row of a (1,1) check, about half of the
+  // others — and the posterior rows the check pass gathers then lie close
+  // together instead of anywhere in the array (sums still follow the
+  // original check order, so results do not change)
+  std::vector<int32_t> minh(M, INT32_MAX);
+  for (int32_t c = 0; c < M; ++c)
+    for (int32_t e = code.check_ptr[c]; e < code.check_ptr[c + 1]; ++e) {
+      const int32_t v = code.check_vars[e];
+      if (deg[v] >= 2) minh[c] = std::min(minh[c], vmap[v]);
+    }
   std::vector<int32_t> corig(M);
   for (int32_t c = 0; c < M; ++c) corig[c] = c;
   std::stable_sort(corig.begin(), corig.end(), [&](int32_t x, int32_t y) {
-    return cnh[x] != cnh[y] ? cnh[x] < cnh[y] : cnd[x] < cnd[y];
+    if (cnh[x] != cnh[y]) return cnh[x] < cnh[y];
+    if (cnd[x] != cnd[y]) return cnd[x] < cnd[y];
+    return minh[x] < minh[y];
   });
   std::vector<int4> cdesc(M);
   std::vector<int32_t> chk_hi_h, dorig(horig), hi_of_edge(code.n_edges(), -1);
