@@ -440,21 +440,27 @@ def run_ours(args):
         if staged:
             dec.stage_inputs(h_llr[i], h_syn[i])
         dec.decode_batch(h_llr[i], cfg, syndrome=h_syn[i], packed=True, out=h_out, stream=sptr)
-    barrier(dist)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e2e_iters = 0
+    # the K-step timed region is short (~0.25 s for cfg2) and a host hiccup
+    # shows in it: it runs three times and the median is reported (all runs
+    # are listed in the JSON line)
     K = max(1, args.steps)
-    if staged:
-        dec.stage_inputs(h_llr[0], h_syn[0])
-    for k in range(K):
-        if staged and k + 1 < K:
-            dec.stage_inputs(h_llr[(k + 1) % 2], h_syn[(k + 1) % 2])
-        dec.decode_batch(h_llr[k % nbuf], cfg, syndrome=h_syn[k % nbuf], packed=True, out=h_out, stream=sptr)
-        e2e_iters += int(h_out["iterations"].numpy().sum())
-    torch.cuda.synchronize()
-    te = max_over_ranks(time.perf_counter() - t0, dist)
-    e2e_value = sum_over_ranks(float(e2e_iters), dist) * code.n_edges / te
+    e2e_runs = []
+    for _rep in range(3):
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_iters = 0
+        if staged:
+            dec.stage_inputs(h_llr[0], h_syn[0])
+        for k in range(K):
+            if staged and k + 1 < K:
+                dec.stage_inputs(h_llr[(k + 1) % 2], h_syn[(k + 1) % 2])
+            dec.decode_batch(h_llr[k % nbuf], cfg, syndrome=h_syn[k % nbuf], packed=True, out=h_out, stream=sptr)
+            e2e_iters += int(h_out["iterations"].numpy().sum())
+        torch.cuda.synchronize()
+        te = max_over_ranks(time.perf_counter() - t0, dist)
+        e2e_runs.append(sum_over_ranks(float(e2e_iters), dist) * code.n_edges / te)
+    e2e_value = float(np.median(e2e_runs))
     h2d = F * N * 4 + F * MW * 4
     d2h = F * NW * 4 + F * 4 + F
 
@@ -527,6 +533,7 @@ def run_ours(args):
                          "frame_iterations": fi},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "runs": e2e_runs, "note": f"median of 3 timed runs of {K} steps",
                     "pipelining": ("upload of step k+1 staged (bpdec_decoder_stage_inputs) during step k" if staged
                                    else "none: two staging copies do not fit in device memory")},
             "gpu_launches": launches,
