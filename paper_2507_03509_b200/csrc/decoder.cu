@@ -14,6 +14,10 @@
 // state: their variable->check message is clamp(llr) (the reference's
 // clamp((llr + c2v) - c2v), decoder.cpp:100-104, without the double rounding
 // residue) and their posterior llr + c2v is formed inside the check kernel.
+// The c2v of a check with one degree>=2 and one degree-1 edge is a constant
+// of the frame; after its first iteration it is not re-read or rewritten.
+// A VNR batch's last few live frames run in a narrow group ([row][16] or
+// [row][8] inside the group's block, lane-folded kernels; rix()).
 //
 // One decoding step = one flooding iteration for every active slot:
 //   k_check     check-node update (decoder.cpp:82-96) + degree-1 posteriors,
@@ -25,7 +29,9 @@
 //               the PCE -> VNR -> d_max decision per frame (:114-123)
 //   k_turnover  outputs of frames that stopped this step (:126-128) and
 //               the next queued frames streamed into the freed slots
-//   k_compact   tail compaction of the live frames into fewer groups
+//   k_compact   tail compaction of the live frames into fewer groups, and
+//               the move of a last group's few live frames into a narrow
+//               (16 / 8-lane) group
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,7 +39,6 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
-#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
