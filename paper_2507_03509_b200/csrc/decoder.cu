@@ -398,9 +398,12 @@ constexpr int kStageRows = 20;  // rows per batch stage (check shapes)
 constexpr int kStages = 3;      // minimum ring depth (stages of kStageRows rows)
 constexpr int kRingRows = kStages * kStageRows;
 
-template <int NH, int ND, int RING = kRingRows>
+// NOC2V: the batch stages no previous-c2v rows (steady-state (1,1) checks,
+// whose c2v is a constant of the frame), so twice as many checks fit a stage.
+template <int NH, int ND, int RING = kRingRows, bool NOC2V = false>
 struct CheckShape {
-  static constexpr int RPC = 2 * NH + ND;  // rows per check
+  static constexpr int CR = NOC2V ? 0 : NH;  // previous-c2v rows per check
+  static constexpr int RPC = NH + CR + ND;   // rows per check
   static constexpr int K = RPC == 0 ? 8 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
   static_assert(K * RPC <= kStageRows, "stage too small");
   // the per-warp ring (kRingRows) is cut into as many stages of this shape's
@@ -446,9 +449,11 @@ template <int NH, int ND, int LW, bool C2V = true>
 __device__ __forceinline__ void check_batch_issue(float* stage, const float* post0, const float* c2v0,
                                                   const float* llr0, const int32_t* hh, int i0, int lrow, int lcol,
                                                   bool qact, bool qc2v, uint64_t pol) {
-  constexpr int K = CheckShape<NH, ND>::K;
-  constexpr int NPH = K * NH;  // posterior / c2v rows
-  constexpr int NPD = K * ND;  // degree-1 rows
+  using SH = CheckShape<NH, ND, kRingRows, !C2V>;
+  constexpr int K = SH::K;
+  constexpr int NPH = K * NH;       // posterior rows
+  constexpr int NPC = K * SH::CR;   // previous-c2v rows (0 without C2V)
+  constexpr int NPD = K * ND;       // degree-1 rows
   constexpr int RPI = 128 / LW;  // rows per warp instruction
 #pragma unroll
   for (int r0 = 0; r0 < NPH; r0 += RPI) {
@@ -464,7 +469,7 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
   for (int r0 = 0; r0 < NPD; r0 += RPI) {
     const int r = r0 + lrow;
     if (r < NPD)
-      cp_async16_ef(stage + (2 * NPH + r) * LW + lcol, llr0 + static_cast<size_t>(i0 + r) * LW + lcol, qact, pol);
+      cp_async16_ef(stage + (NPH + NPC + r) * LW + lcol, llr0 + static_cast<size_t>(i0 + r) * LW + lcol, qact, pol);
   }
   cp_async_commit();
 }
@@ -483,8 +488,17 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
                                                     const uint32_t* ssyn, int i0, int lane, bool act, bool first,
                                                     float cl, float clamp, uint32_t* synw, uint32_t* d1w) {
   constexpr int D = NH + ND;
-  constexpr int K = CheckShape<NH, ND>::K;
+  // steady-state (1,1) check: the c2v to its degree>=2 variable is
+  // (1-2s)*sign(l)*min(|l|, clamp) in every iteration (the degree-1 edge's
+  // v2c is clamp(l)), so it is formed from l instead of being re-read (the
+  // stage has no c2v rows), and the stored copy (written in the frame's
+  // first iteration, moved with the frame) is not rewritten: 8 bytes per
+  // check and frame less per pass
+  constexpr bool kConstC = NH == 1 && ND == 1 && !FM;
+  using SH = CheckShape<NH, ND, kRingRows, kConstC>;
+  constexpr int K = SH::K;
   constexpr int NPH = K * NH;
+  constexpr int NPC = K * SH::CR;
   constexpr int F = 32 / LW;
   constexpr int FE = F < K ? F : K;  // checks per folded step
   constexpr uint32_t kSign = 0x80000000u;
@@ -493,17 +507,11 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   const bool qok = q < FE;
   const bool on = act && qok;
   // this lane's rows: check kb + q of sub-batch kb
-  const float* sp = stage + f + q * NH * LW;          // posterior rows
-  const float* sc = stage + f + (NPH + q * NH) * LW;  // previous c2v rows
-  const float* sl = stage + f + (2 * NPH + q) * LW;   // degree-1 llr rows
+  const float* sp = stage + f + q * NH * LW;                // posterior rows
+  const float* sc = stage + f + (NPH + q * SH::CR) * LW;   // previous c2v rows (none with kConstC)
+  const float* sl = stage + f + (NPH + NPC + q) * LW;      // degree-1 llr rows
   float* cq = c2vg + q * NH * LW;
   float* dq = WANT_POST ? d1p + q * LW : nullptr;
-  // steady-state (1,1) check: the c2v to its degree>=2 variable is
-  // (1-2s)*sign(l)*min(|l|, clamp) in every iteration (the degree-1 edge's
-  // v2c is clamp(l)), so it is formed from l instead of being re-read, and
-  // the stored copy (written in the frame's first iteration, moved with the
-  // frame) is not rewritten: 8 bytes per check and frame less per pass
-  constexpr bool kConstC = NH == 1 && ND == 1 && !FM;
 #pragma unroll
   for (int kb = 0; kb < K; kb += FE) {
     float m[D > 0 ? D : 1];      // |v2c|, clamped (cl = inf in the first iteration)
@@ -568,7 +576,9 @@ template <int NH, int ND, bool WANT_POST, bool FM, int RING, int LW = 32>
 __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
-  constexpr int K = CheckShape<NH, ND>::K;
+  constexpr bool kNoC = NH == 1 && ND == 1 && !FM;  // steady-state (1,1): no c2v rows staged
+  using SH = CheckShape<NH, ND, RING, kNoC>;
+  constexpr int K = SH::K;
   constexpr int NB = 32 / K;
   const int f = LW == 32 ? lane : lane % LW;  // this lane's frame (slot lane)
   if (LW < 32) act = (amask >> f) & 1u;
@@ -587,15 +597,14 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   const bool qact = qbits != 0u;
   const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
   const uint64_t pol = policy_evict_first();
-  constexpr int NS = CheckShape<NH, ND, RING>::NS;
-  constexpr int RS = CheckShape<NH, ND, RING>::ROWS * kLanes;  // stage stride
+  constexpr int NS = SH::NS;
+  constexpr int RS = SH::ROWS * kLanes;  // stage stride
   // one commit group per step (empty past the last batch), so the wait
   // count is a constant
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p) {
     if (p < NB)
-      check_batch_issue<NH, ND, LW, !(NH == 1 && ND == 1 && !FM)>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow,
-                                                                   lcol, qact, qc2v, pol);
+      check_batch_issue<NH, ND, LW, !kNoC>(ring + p * RS, post0, c2v0, llr0, hh, p * K, lrow, lcol, qact, qc2v, pol);
     else
       cp_async_commit();
   }
@@ -603,8 +612,7 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
     if (b + NS - 1 < NB)
-      check_batch_issue<NH, ND, LW, !(NH == 1 && ND == 1 && !FM)>(ring + slot_i * RS, post0, c2v0, llr0, hh,
-                                                                   (b + NS - 1) * K, lrow, lcol, qact,
+      check_batch_issue<NH, ND, LW, !kNoC>(ring + slot_i * RS, post0, c2v0, llr0, hh, (b + NS - 1) * K, lrow, lcol, qact,
                                     qc2v, pol);
     else
       cp_async_commit();
