@@ -400,16 +400,20 @@ constexpr int kRingRows = kStages * kStageRows;
 
 // NOC2V: the batch stages no previous-c2v rows (steady-state (1,1) checks,
 // whose c2v is a constant of the frame), so twice as many checks fit a stage.
-template <int NH, int ND, int RING = kRingRows, bool NOC2V = false>
+// Narrow groups (LW < 32): rows are LW floats, so a stage and the ring
+// hold 32/LW times the rows (bigger batches, fewer per chunk).
+template <int NH, int ND, int RING = kRingRows, bool NOC2V = false, int LW = 32>
 struct CheckShape {
   static constexpr int CR = NOC2V ? 0 : NH;  // previous-c2v rows per check
   static constexpr int RPC = NH + CR + ND;   // rows per check
-  static constexpr int K = RPC == 0 ? 8 : (kStageRows / RPC >= 8 ? 8 : (kStageRows / RPC >= 4 ? 4 : (kStageRows / RPC >= 2 ? 2 : 1)));
-  static_assert(K * RPC <= kStageRows, "stage too small");
+  static constexpr int SR = kStageRows * (32 / LW);  // stage rows
+  static constexpr int RR = RING * (32 / LW);        // ring rows
+  static constexpr int K = RPC == 0 ? 8 : (SR / RPC >= 8 ? 8 : (SR / RPC >= 4 ? 4 : (SR / RPC >= 2 ? 2 : 1)));
+  static_assert(K * RPC <= SR, "stage too small");
   // the per-warp ring (kRingRows) is cut into as many stages of this shape's
   // batch size as fit (light shapes keep more batches in flight)
   static constexpr int ROWS = RPC == 0 ? 1 : K * RPC;
-  static constexpr int NS = RING / ROWS >= 6 ? 6 : RING / ROWS;
+  static constexpr int NS = RR / ROWS >= 6 ? 6 : RR / ROWS;
   static_assert(NS >= kStages, "at least the default ring depth");
 };
 
@@ -449,7 +453,7 @@ template <int NH, int ND, int LW, bool C2V = true>
 __device__ __forceinline__ void check_batch_issue(float* stage, const float* post0, const float* c2v0,
                                                   const float* llr0, const int32_t* hh, int i0, int lrow, int lcol,
                                                   bool qact, bool qc2v, uint64_t pol) {
-  using SH = CheckShape<NH, ND, kRingRows, !C2V>;
+  using SH = CheckShape<NH, ND, kRingRows, !C2V, LW>;
   constexpr int K = SH::K;
   constexpr int NPH = K * NH;       // posterior rows
   constexpr int NPC = K * SH::CR;   // previous-c2v rows (0 without C2V)
@@ -495,7 +499,7 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   // first iteration, moved with the frame) is not rewritten: 8 bytes per
   // check and frame less per pass
   constexpr bool kConstC = NH == 1 && ND == 1 && !FM;
-  using SH = CheckShape<NH, ND, kRingRows, kConstC>;
+  using SH = CheckShape<NH, ND, kRingRows, kConstC, LW>;
   constexpr int K = SH::K;
   constexpr int NPH = K * NH;
   constexpr int NPC = K * SH::CR;
@@ -577,7 +581,7 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   constexpr bool kNoC = NH == 1 && ND == 1 && !FM;  // steady-state (1,1): no c2v rows staged
-  using SH = CheckShape<NH, ND, RING, kNoC>;
+  using SH = CheckShape<NH, ND, RING, kNoC, LW>;
   constexpr int K = SH::K;
   constexpr int NB = 32 / K;
   const int f = LW == 32 ? lane : lane % LW;  // this lane's frame (slot lane)
@@ -598,7 +602,7 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   const bool qc2v = (qbits & ~(fmask >> lcol)) != 0u;  // some active frame past its first iteration
   const uint64_t pol = policy_evict_first();
   constexpr int NS = SH::NS;
-  constexpr int RS = SH::ROWS * kLanes;  // stage stride
+  constexpr int RS = SH::ROWS * LW;  // stage stride (floats)
   // one commit group per step (empty past the last batch), so the wait
   // count is a constant
 #pragma unroll
