@@ -1284,18 +1284,24 @@ constexpr int kSynChunks = 4;  // chunks per warp pass (their loads are in fligh
 // failing frames: once every active frame is known to fail — in the high-FER
 // regime after the first round of passes — the warps stop, so the pass costs
 // about one round of loads instead of a sweep over all checks.
-__device__ __forceinline__ void syndrome_block(const Args& a, uint32_t* s_act) {
+__device__ __forceinline__ void syndrome_block(const Args& a, int b, int nb, uint32_t* s_act) {
   for (int t = threadIdx.x; t < a.G; t += blockDim.x) s_act[t] = a.group_active[t];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int chunks = (a.M + 31) / 32;
   const int passes = (chunks + kSynChunks - 1) / kSynChunks;
-  for (;;) {
-    int q = 0;
-    if (lane == 0) q = atomicAdd(&a.counters[10], 1);
-    q = __shfl_sync(0xffffffffu, q, 0);
+  // first pass by warp index (no atomic round trip), then from counters[10]
+  // (which k_var reset; handed-out passes start after the first round)
+  const int nw = nb * static_cast<int>(blockDim.x >> 5);
+  int q = b * static_cast<int>(blockDim.x >> 5) + static_cast<int>(threadIdx.x >> 5);
+  for (bool first_pass = true;; first_pass = false) {
+    if (!first_pass) {
+      int k = 0;
+      if (lane == 0) k = atomicAdd(&a.counters[10], 1);
+      q = nw + __shfl_sync(0xffffffffu, k, 0);
+    }
     if (q >= passes) break;
-    bool live = false;  // any group with an active frame not yet known to fail
+    bool live = first_pass;  // any group with an active frame not yet known to fail (k_check reset fail)
     for (int g0 = 0; g0 < a.G && !live; g0 += 32) {
       const int g = g0 + lane;
       const uint32_t am = g < a.G ? s_act[g] : 0u;
@@ -1489,7 +1495,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const Args a, int syn_block
   __shared__ int s_last;
   const int b = blockIdx.x;
   if (b < syn_blocks) {
-    syndrome_block(a, s_grp);
+    syndrome_block(a, b, syn_blocks, s_grp);
   } else {
     const int qb = b - syn_blocks;
     q_block(a, qb / kTermBlocks, qb - (qb / kTermBlocks) * kTermBlocks, red);
