@@ -165,16 +165,90 @@ int bpdec_decode_batch(bpdec_decoder* dec, int32_t batch, const float* llr,
                        void* bits_out, int32_t* iterations_out, uint8_t* reason_out,
                        float* posteriors_out, double* q_trace_out, void* stream);
 
+/* ≙ BpDecoder::decode with an IterationObserver (decoder.hpp:53-55,
+ * decoder.cpp:107-112): bpdec_decode_batch plus per-iteration traces for
+ * replaying the observer's (iteration, posteriors, syndrome_ok, q) calls.
+ *   syndrome_ok_trace_out [batch][d_max] u8: 1 iff H bits == s after
+ *       iteration k (computed every iteration, PCE on or off, like
+ *       decoder.cpp:111); 0xff past the stop iteration; or NULL
+ *   posterior_trace_out [batch][d_max][N] float: the posteriors after every
+ *       iteration (NaN past the stop); or NULL.  Sized for small batches.
+ * q is q_trace_out.  Other arguments as bpdec_decode_batch. */
+int bpdec_decode_batch_traced(bpdec_decoder* dec, int32_t batch, const float* llr,
+                              const uint32_t* syndrome, const bpdec_config* cfg, uint32_t flags,
+                              void* bits_out, int32_t* iterations_out, uint8_t* reason_out,
+                              float* posteriors_out, double* q_trace_out,
+                              uint8_t* syndrome_ok_trace_out, float* posterior_trace_out,
+                              void* stream);
+
 /* Pipelined host input: starts the host->device copy of a batch (pinned host
  * memory for full overlap) on the decoder's copy stream and returns at once.
  * A later bpdec_decode_batch with the same llr / syndrome pointers and batch
  * decodes from the staged copy, so staging batch k+1 before decoding batch k
  * overlaps its upload with the decode.  Two staging slots; staging a third
  * batch replaces the older unconsumed one (whose decode then copies again).
- * The host buffers must stay unchanged until that decode returns.  No
+ * The match is by pointer: the staged bytes are what the buffers held when
+ * this call was made, so the host buffers must not be rewritten between this
+ * call and the decode that consumes them (refill a buffer only after its
+ * decode returns, e.g. alternate two buffer sets).  No
  * reference counterpart (the reference decodes host spans on the CPU). */
 int bpdec_decoder_stage_inputs(bpdec_decoder* dec, int32_t batch, const float* llr_host,
                                const uint32_t* syndrome_host);
+
+/* ---------------------------------------------------------- stream mode -- */
+/* Batches submitted back to back decode as ONE continuous frame stream
+ * through the decoder's slots: the lanes a batch's slow frames leave free
+ * are refilled with the next batch's frames in the same step, and a batch's
+ * upload overlaps the decode of the earlier ones.  A worker thread owned by
+ * the decoder launches the steps; outputs of a batch are copied to the
+ * caller's buffers as soon as its last frame stopped.  Per-frame results are
+ * those of bpdec_decode_batch on the same frames (no dependence on slot,
+ * order or neighbours).  No reference counterpart: this replaces the
+ * per-block loop of run_trials (channel.cpp:90-148) for a caller that keeps
+ * the GPU busy across batches.
+ *   open:   cfg / flags (BPDEC_BITS_PACKED) / which outputs exist are fixed
+ *           for the stream; ring_frames = frames whose inputs and outputs can
+ *           be in flight (0 = 4 x slots; a batch must fit).  While open, the
+ *           decoder accepts only stream calls.
+ *   submit: inputs host (pinned for overlap) or device pointers, read until
+ *           the batch completes; outputs host or device pointers (pinned host
+ *           memory keeps the worker from blocking on the copy), written when
+ *           the batch completes.  Blocks while the ring or the batch slots
+ *           (32 in flight) are full.  *ticket_out identifies the batch.
+ *   wait:   blocks until the batch's outputs are written; returns its status
+ *           (BPDEC_ERR_VALIDATION for a non-finite LLR in that batch).
+ *   query:  *done = 1 once wait would not block.
+ *   close:  waits for every submitted batch, frees the rings. */
+int bpdec_stream_open(bpdec_decoder* dec, const bpdec_config* cfg, uint32_t flags, int32_t ring_frames,
+                      int32_t want_bits, int32_t want_posteriors, int32_t want_q_trace);
+int bpdec_stream_submit(bpdec_decoder* dec, int32_t batch, const float* llr, const uint32_t* syndrome,
+                        void* bits_out, int32_t* iterations_out, uint8_t* reason_out, float* posteriors_out,
+                        double* q_trace_out, int64_t* ticket_out);
+int bpdec_stream_wait(bpdec_decoder* dec, int64_t ticket);
+int bpdec_stream_query(bpdec_decoder* dec, int64_t ticket, int32_t* done);
+int bpdec_stream_close(bpdec_decoder* dec);
+
+/* ------------------------------------------------------------ multi-GPU -- */
+/* Frame-sharded decoding over several GPUs of one host (the
+ * reference's strided worker pool, channel.cpp:98-122): one decoder per
+ * entry of devices[] (an entry may repeat a device), each fed by its own
+ * host thread from a shared queue of chunk_frames-frame chunks (dynamic, so
+ * devices that finish early take more; 0 = auto), no collective, per-frame
+ * outputs written into the caller's buffers at their frame index.  Results
+ * are identical for any device list and chunk size (per-frame
+ * independence; the reference's worker-count invariance, channel.hpp:66-71).
+ * frames_per_decoder_out [n_devices] (may be NULL) receives how many frames
+ * each decoder took in this call. */
+typedef struct bpdec_multi bpdec_multi;
+int bpdec_multi_create(const bpdec_code* code, const int32_t* devices, int32_t n_devices,
+                       int32_t slots_per_decoder, bpdec_multi** out);
+void bpdec_multi_destroy(bpdec_multi* multi);
+int bpdec_multi_count(const bpdec_multi* multi, int32_t* n_decoders);
+int bpdec_multi_decode_batch(bpdec_multi* multi, int32_t batch, const float* llr,
+                             const uint32_t* syndrome, const bpdec_config* cfg, uint32_t flags,
+                             void* bits_out, int32_t* iterations_out, uint8_t* reason_out,
+                             float* posteriors_out, double* q_trace_out, int32_t chunk_frames,
+                             int64_t* frames_per_decoder_out);
 
 /* Device-side frame generator for resident-input benchmarks: same draws as
  * bpdec_sample_frames, written to DEVICE buffers (llr [n][N], syndrome
@@ -229,7 +303,8 @@ int bpdec_run_trials(bpdec_decoder* dec, double snr, const int32_t* punctured, i
  * on the launching stream).  Enable before decoding; kernel ids:
  * 0 check-node, 1 variable-node, 2 decide (syndrome + q^(k) + stop decision),
  * 3 unused (termination is part of 2), 4 turnover (outputs of stopped frames +
- * loading of queued frames), 5 tail compaction. */
+ * loading of queued frames), 5 tail compaction, 6 output snapshot (eager host
+ * copies), 7 posterior trace (bpdec_decode_batch_traced). */
 int bpdec_decoder_set_profiling(bpdec_decoder* dec, int32_t enable);
 int bpdec_decoder_profile(const bpdec_decoder* dec, int32_t kernel, double* total_ms,
                           int64_t* launches, double* frame_iterations);

@@ -246,9 +246,12 @@ class BpDecoder {
   }
 
   // ≙ BpDecoder::decode (decoder.hpp:64-65).  LLRs are rounded to float32.
-  // The observer is called after decoding with each iteration's q (posteriors
-  // and syndrome flags per iteration are not retained on the device).
-  DecodeOutcome decode(std::span<const double> llr_in, const ActiveVarSet& /*active*/, const DecodeConfig& cfg,
+  // `active` must be active_var_set(code) (the device builds q over the
+  // degree>=2 variables); another set throws ValidationError.  The observer
+  // receives, per iteration, that iteration's posteriors, the real
+  // syndrome_ok (computed every iteration, PCE on or off, decoder.cpp:110-112)
+  // and q — replayed from bpdec_decode_batch_traced after the decode.
+  DecodeOutcome decode(std::span<const double> llr_in, const ActiveVarSet& active, const DecodeConfig& cfg,
                        const IterationObserver& observer = nullptr, const std::uint32_t* syndrome = nullptr) {
     const int n = code_.n_vars();
     if (llr_in.size() != static_cast<size_t>(n)) {
@@ -257,12 +260,39 @@ class BpDecoder {
     }
     for (double l : llr_in)
       if (!std::isfinite(l)) throw ValidationError("decode: non-finite input LLR");
+    if (!same_active_set(active))
+      throw ValidationError("decode: only active_var_set(code) (the degree>=2 variables) is supported as the VNR "
+                            "active set");
     std::vector<float> llr(llr_in.begin(), llr_in.end());
-    std::vector<DecodeOutcome> out = decode_batch(1, llr.data(), syndrome, cfg, true);
-    if (observer) {
-      for (int k = 0; k < out[0].iterations; ++k) observer(k + 1, {}, false, out[0].q_trace[k]);
+    if (!observer) return std::move(decode_batch(1, llr.data(), syndrome, cfg, true)[0]);
+    // outcome + syndrome_ok trace, then (deterministic per frame) the
+    // posteriors of iterations 1..k with d_max = k: a k x N trace buffer
+    bpdec_config c{cfg.d_max, cfg.use_pce ? 1 : 0, cfg.use_vnr ? 1 : 0, cfg.q_mode, cfg.msg_clamp};
+    std::vector<std::uint8_t> bits(static_cast<size_t>(n)), syn_ok(static_cast<size_t>(cfg.d_max > 0 ? cfg.d_max : 1));
+    std::vector<float> post(static_cast<size_t>(n));
+    std::vector<double> qt(syn_ok.size());
+    int32_t it = 0;
+    std::uint8_t rs = 0;
+    check_status(bpdec_decode_batch_traced(dec_.get(), 1, llr.data(), syndrome, &c, 0, bits.data(), &it, &rs,
+                                           post.data(), qt.data(), syn_ok.data(), nullptr, nullptr));
+    bpdec_config tc{it, 0, 0, cfg.q_mode, cfg.msg_clamp};
+    std::vector<float> ptrace(static_cast<size_t>(it) * n);
+    int32_t it2 = 0;
+    std::uint8_t rs2 = 0;
+    check_status(bpdec_decode_batch_traced(dec_.get(), 1, llr.data(), syndrome, &tc, 0, nullptr, &it2, &rs2, nullptr,
+                                           nullptr, nullptr, ptrace.data(), nullptr));
+    std::vector<double> pk(static_cast<size_t>(n));
+    for (int k = 0; k < it; ++k) {
+      for (int v = 0; v < n; ++v) pk[v] = ptrace[static_cast<size_t>(k) * n + v];
+      observer(k + 1, pk, syn_ok[k] == 1, qt[k]);
     }
-    return std::move(out[0]);
+    DecodeOutcome o;
+    o.bits = std::move(bits);
+    o.iterations = it;
+    o.reason = static_cast<StopReason>(rs);
+    o.q_trace.assign(qt.begin(), qt.begin() + it);
+    o.posteriors.assign(post.begin(), post.end());
+    return o;
   }
 
   // Batched, syndrome-aware decode of `batch` frames ([batch][N] float LLRs,
@@ -296,8 +326,17 @@ class BpDecoder {
   struct Del {
     void operator()(bpdec_decoder* d) const { bpdec_decoder_destroy(d); }
   };
+  bool same_active_set(const ActiveVarSet& active) {
+    if (!active_valid_) {
+      active_ = active_var_set(code_);
+      active_valid_ = true;
+    }
+    return active.members == active_.members;
+  }
   ParityCheckMatrix code_;
   std::unique_ptr<bpdec_decoder, Del> dec_;
+  ActiveVarSet active_;
+  bool active_valid_ = false;
 };
 
 // ≙ etdec::run_trials (channel.hpp:72-74) on the GPU: trials are decoded in

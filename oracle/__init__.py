@@ -65,6 +65,9 @@ class Reference:
                                          C.POINTER(f64), C.c_char_p, C.c_int]
         L.etref_decode_observed.argtypes = [vp, C.POINTER(f64), C.c_int, C.c_int, C.c_int, f64, C.POINTER(i32),
                                             C.POINTER(u8), C.POINTER(u8), C.POINTER(f64), C.POINTER(i32)]
+        L.etref_decode_observed_post.argtypes = [vp, C.POINTER(f64), C.c_int, C.c_int, C.c_int, f64, C.POINTER(i32),
+                                                 C.POINTER(u8), C.POINTER(u8), C.POINTER(f64), C.POINTER(f64),
+                                                 C.POINTER(i32)]
         L.etref_syndrome_check.argtypes = [vp, C.POINTER(u8), C.c_int]
         L.etref_snr_for_beta.restype = f64
         L.etref_snr_for_beta.argtypes = [f64, f64]
@@ -207,6 +210,23 @@ class RefCode:
             raise OracleError(st)
         k = it.value
         return dict(iterations=k, reason=rs.value, syndrome_ok=ok[:k], q=q[:k], calls=calls.value)
+
+    def decode_observed_post(self, llr, d_max=100, use_pce=True, use_vnr=False, msg_clamp=30.0):
+        """decode_observed plus the observer's per-iteration posteriors."""
+        llr = np.ascontiguousarray(llr, dtype=np.float64)
+        n = llr.size
+        it, rs, calls = C.c_int32(), C.c_uint8(), C.c_int32()
+        ok = np.zeros(d_max, dtype=np.uint8)
+        q = np.zeros(d_max, dtype=np.float64)
+        post = np.zeros((d_max, n), dtype=np.float64)
+        st = self.ref.L.etref_decode_observed_post(self.h, _p(llr, C.c_double), d_max, int(use_pce), int(use_vnr),
+                                                   msg_clamp, C.byref(it), C.byref(rs), _p(ok, C.c_uint8),
+                                                   _p(q, C.c_double), _p(post, C.c_double), C.byref(calls))
+        if st:
+            raise OracleError(st)
+        k = it.value
+        return dict(iterations=k, reason=rs.value, syndrome_ok=ok[:k], q=q[:k], posteriors=post[:k],
+                    calls=calls.value)
 
 
 class _OrcCfg(C.Structure):

@@ -196,6 +196,33 @@ int etref_decode_observed(const void* code, const double* llr, int d_max, int us
   }
 }
 
+// Same, also recording the observer's posteriors of every iteration
+// (post_trace [d_max][n], rows past the stop untouched).
+int etref_decode_observed_post(const void* code, const double* llr, int d_max, int use_pce, int use_vnr,
+                               double msg_clamp, int32_t* iterations, uint8_t* reason, uint8_t* syndrome_ok_trace,
+                               double* q_trace, double* post_trace, int32_t* observer_calls) {
+  try {
+    const auto& h = *static_cast<const etdec::ParityCheckMatrix*>(code);
+    etdec::DecodeConfig cfg{d_max, use_pce != 0, use_vnr != 0, msg_clamp};
+    etdec::BpDecoder dec(h);
+    int calls = 0;
+    const size_t n = static_cast<size_t>(h.n_vars());
+    auto obs = [&](int it, std::span<const double> post, bool ok, double q) {
+      syndrome_ok_trace[it - 1] = ok ? 1 : 0;
+      q_trace[it - 1] = q;
+      std::copy(post.begin(), post.end(), post_trace + static_cast<size_t>(it - 1) * n);
+      ++calls;
+    };
+    const auto out = dec.decode(std::span<const double>(llr, h.n_vars()), etdec::active_var_set(h), cfg, obs);
+    *iterations = out.iterations;
+    *reason = static_cast<uint8_t>(out.reason);
+    *observer_calls = calls;
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
 int etref_syndrome_check(const void* code, const uint8_t* bits, int n) {
   try {
     return etdec::syndrome_check(*static_cast<const etdec::ParityCheckMatrix*>(code),

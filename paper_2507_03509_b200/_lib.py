@@ -79,6 +79,9 @@ SIGNATURES = [
     ("bpdec_decode_batch", C.c_int,
      [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(Config), C.c_uint32, C.c_void_p,
       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("bpdec_decode_batch_traced", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(Config), C.c_uint32, C.c_void_p,
+      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("bpdec_decoder_stage_inputs", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     ("bpdec_decoder_sample_frames_device", C.c_int,
      [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
@@ -88,6 +91,20 @@ SIGNATURES = [
     ("bpdec_run_trials", C.c_int,
      [C.c_void_p, C.c_double, c_i32p, C.c_int32, C.POINTER(Config), C.POINTER(StopRule), C.c_uint64, C.c_int32,
       C.POINTER(TrialStatsC), c_i64p]),
+    ("bpdec_stream_open", C.c_int,
+     [C.c_void_p, C.POINTER(Config), C.c_uint32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    ("bpdec_stream_submit", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+      C.c_void_p, c_i64p]),
+    ("bpdec_stream_wait", C.c_int, [C.c_void_p, C.c_int64]),
+    ("bpdec_stream_query", C.c_int, [C.c_void_p, C.c_int64, c_i32p]),
+    ("bpdec_stream_close", C.c_int, [C.c_void_p]),
+    ("bpdec_multi_create", C.c_int, [C.c_void_p, c_i32p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("bpdec_multi_destroy", None, [C.c_void_p]),
+    ("bpdec_multi_count", C.c_int, [C.c_void_p, c_i32p]),
+    ("bpdec_multi_decode_batch", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(Config), C.c_uint32, C.c_void_p, C.c_void_p,
+      C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, c_i64p]),
     ("bpdec_decoder_set_profiling", C.c_int, [C.c_void_p, C.c_int32]),
     ("bpdec_decoder_profile", C.c_int, [C.c_void_p, C.c_int32, c_f64p, c_i64p, c_f64p]),
     ("bpdec_decoder_reset_profile", C.c_int, [C.c_void_p]),

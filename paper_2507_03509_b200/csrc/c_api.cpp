@@ -4,8 +4,11 @@
 #include "../../include/bpdec.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -23,6 +26,20 @@ struct bpdec_decoder {
   bpdec::GpuDecoder* impl = nullptr;
   int32_t n_vars = 0;
   int32_t n_checks = 0;
+};
+// Multi-device decoder: one GpuDecoder per entry of the device list, each
+// fed by its own host thread from a shared chunk queue (streams stay open
+// between calls while the configuration is unchanged).
+struct bpdec_multi {
+  std::vector<bpdec::GpuDecoder*> decs;
+  std::vector<int32_t> devices;
+  int32_t n_vars = 0, n_checks = 0, slots = 0;
+  bool open = false;
+  bpdec::DecodeParams p{};
+  uint32_t flags = 0;
+  bool want_bits = false, want_post = false, want_q = false;
+  int32_t ring = 0;
+  std::vector<int64_t> frames_taken;
 };
 
 namespace {
@@ -351,21 +368,56 @@ int bpdec_decoder_device_bytes(const bpdec_decoder* dec, int64_t* bytes) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+// DecodeConfig validation (decoder.cpp:56-64) and translation.
+bpdec::DecodeParams decode_params(const bpdec_config* cfg) {
+  need(cfg, "cfg");
+  if (cfg->d_max <= 0) throw bpdec::ValidationError("decode: d_max must be positive");
+  if (!(cfg->msg_clamp > 0.0)) throw bpdec::ValidationError("decode: msg_clamp must be positive");
+  if (cfg->q_mode != BPDEC_Q_RAW && cfg->q_mode != BPDEC_Q_ABS) throw bpdec::ConfigError("decode: unknown q_mode");
+  bpdec::DecodeParams p;
+  p.d_max = cfg->d_max;
+  p.use_pce = cfg->use_pce ? 1 : 0;
+  p.use_vnr = cfg->use_vnr ? 1 : 0;
+  p.q_mode = cfg->q_mode;
+  p.msg_clamp = static_cast<float>(cfg->msg_clamp);
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+int bpdec_decode_batch_traced(bpdec_decoder* dec, int32_t batch, const float* llr, const uint32_t* syndrome,
+                              const bpdec_config* cfg, uint32_t flags, void* bits_out, int32_t* iterations_out,
+                              uint8_t* reason_out, float* posteriors_out, double* q_trace_out,
+                              uint8_t* syndrome_ok_trace_out, float* posterior_trace_out, void* stream) {
+  return guarded([&] {
+    need(dec, "decoder");
+    const bpdec::DecodeParams p = decode_params(cfg);
+    bpdec::DecodeBuffers b;
+    b.batch = batch;
+    b.llr = llr;
+    b.syndrome = syndrome;
+    b.bits_packed = (flags & BPDEC_BITS_PACKED) != 0;
+    b.bits = bits_out;
+    b.iterations = iterations_out;
+    b.reasons = reason_out;
+    b.posteriors = posteriors_out;
+    b.q_trace = q_trace_out;
+    b.syn_trace = syndrome_ok_trace_out;
+    b.post_trace = posterior_trace_out;
+    bpdec::gpu_decode_batch(dec->impl, p, b, stream);
+  });
+}
+
 int bpdec_decode_batch(bpdec_decoder* dec, int32_t batch, const float* llr, const uint32_t* syndrome,
                        const bpdec_config* cfg, uint32_t flags, void* bits_out, int32_t* iterations_out,
                        uint8_t* reason_out, float* posteriors_out, double* q_trace_out, void* stream) {
   return guarded([&] {
     need(dec, "decoder");
-    need(cfg, "cfg");
-    if (cfg->d_max <= 0) throw bpdec::ValidationError("decode: d_max must be positive");
-    if (!(cfg->msg_clamp > 0.0)) throw bpdec::ValidationError("decode: msg_clamp must be positive");
-    if (cfg->q_mode != BPDEC_Q_RAW && cfg->q_mode != BPDEC_Q_ABS) throw bpdec::ConfigError("decode: unknown q_mode");
-    bpdec::DecodeParams p;
-    p.d_max = cfg->d_max;
-    p.use_pce = cfg->use_pce ? 1 : 0;
-    p.use_vnr = cfg->use_vnr ? 1 : 0;
-    p.q_mode = cfg->q_mode;
-    p.msg_clamp = static_cast<float>(cfg->msg_clamp);
+    const bpdec::DecodeParams p = decode_params(cfg);
     bpdec::DecodeBuffers b;
     b.batch = batch;
     b.llr = llr;
@@ -438,14 +490,7 @@ int bpdec_run_trials(bpdec_decoder* dec, double snr, const int32_t* punctured, i
     need(cfg, "cfg");
     need(stop, "stop");
     need(stats_out, "stats_out");
-    if (cfg->d_max <= 0) throw bpdec::ValidationError("decode: d_max must be positive");
-    if (!(cfg->msg_clamp > 0.0)) throw bpdec::ValidationError("decode: msg_clamp must be positive");
-    bpdec::DecodeParams p;
-    p.d_max = cfg->d_max;
-    p.use_pce = cfg->use_pce ? 1 : 0;
-    p.use_vnr = cfg->use_vnr ? 1 : 0;
-    p.q_mode = cfg->q_mode;
-    p.msg_clamp = static_cast<float>(cfg->msg_clamp);
+    const bpdec::DecodeParams p = decode_params(cfg);
     std::vector<int32_t> punct;
     if (n_punctured > 0) {
       need(punctured, "punctured");
@@ -506,6 +551,193 @@ int bpdec_decoder_launch_count(const bpdec_decoder* dec, int64_t* launches) {
     need(dec, "decoder");
     need(launches, "launches");
     *launches = bpdec::gpu_launch_count(dec->impl);
+  });
+}
+
+/* ------------------------------------------------------------ stream mode -- */
+int bpdec_stream_open(bpdec_decoder* dec, const bpdec_config* cfg, uint32_t flags, int32_t ring_frames,
+                      int32_t want_bits, int32_t want_posteriors, int32_t want_q_trace) {
+  return guarded([&] {
+    need(dec, "decoder");
+    const bpdec::DecodeParams p = decode_params(cfg);
+    bpdec::gpu_stream_open(dec->impl, p, (flags & BPDEC_BITS_PACKED) != 0, want_bits != 0, want_posteriors != 0,
+                           want_q_trace != 0, ring_frames);
+  });
+}
+
+int bpdec_stream_submit(bpdec_decoder* dec, int32_t batch, const float* llr, const uint32_t* syndrome,
+                        void* bits_out, int32_t* iterations_out, uint8_t* reason_out, float* posteriors_out,
+                        double* q_trace_out, int64_t* ticket_out) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(ticket_out, "ticket_out");
+    bpdec::StreamOutputs o;
+    o.bits = bits_out;
+    o.iterations = iterations_out;
+    o.reasons = reason_out;
+    o.posteriors = posteriors_out;
+    o.q_trace = q_trace_out;
+    *ticket_out = bpdec::gpu_stream_submit(dec->impl, batch, llr, syndrome, o);
+  });
+}
+
+int bpdec_stream_query(bpdec_decoder* dec, int64_t ticket, int32_t* done) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(done, "done");
+    *done = bpdec::gpu_stream_query(dec->impl, ticket) ? 1 : 0;
+  });
+}
+
+int bpdec_stream_wait(bpdec_decoder* dec, int64_t ticket) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_stream_wait(dec->impl, ticket);
+  });
+}
+
+int bpdec_stream_close(bpdec_decoder* dec) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_stream_close(dec->impl);
+  });
+}
+
+/* ------------------------------------------------------------ multi-GPU -- */
+int bpdec_multi_create(const bpdec_code* code, const int32_t* devices, int32_t n_devices, int32_t slots_per_decoder,
+                       bpdec_multi** out) {
+  return guarded([&] {
+    need(code, "code");
+    need(out, "out");
+    if (n_devices <= 0) throw bpdec::ValidationError("multi: need at least one device");
+    need(devices, "devices");
+    auto* m = new bpdec_multi;
+    try {
+      for (int32_t i = 0; i < n_devices; ++i) {
+        m->decs.push_back(bpdec::gpu_decoder_create(code->code, devices[i], slots_per_decoder));
+        m->devices.push_back(devices[i]);
+      }
+    } catch (...) {
+      for (auto* d : m->decs) bpdec::gpu_decoder_destroy(d);
+      delete m;
+      throw;
+    }
+    m->n_vars = code->code.n_vars;
+    m->n_checks = code->code.n_checks;
+    m->slots = bpdec::gpu_decoder_slots(m->decs[0]);
+    m->frames_taken.assign(m->decs.size(), 0);
+    *out = m;
+  });
+}
+
+void bpdec_multi_destroy(bpdec_multi* m) {
+  if (!m) return;
+  for (auto* d : m->decs) {
+    try {
+      bpdec::gpu_stream_close(d);
+    } catch (...) {
+    }
+    bpdec::gpu_decoder_destroy(d);
+  }
+  delete m;
+}
+
+int bpdec_multi_count(const bpdec_multi* m, int32_t* n_decoders) {
+  return guarded([&] {
+    need(m, "multi");
+    need(n_decoders, "n_decoders");
+    *n_decoders = static_cast<int32_t>(m->decs.size());
+  });
+}
+
+int bpdec_multi_decode_batch(bpdec_multi* m, int32_t batch, const float* llr, const uint32_t* syndrome,
+                             const bpdec_config* cfg, uint32_t flags, void* bits_out, int32_t* iterations_out,
+                             uint8_t* reason_out, float* posteriors_out, double* q_trace_out, int32_t chunk_frames,
+                             int64_t* frames_per_decoder_out) {
+  return guarded([&] {
+    need(m, "multi");
+    const bpdec::DecodeParams p = decode_params(cfg);
+    if (batch < 0) throw bpdec::ValidationError("decode: batch must be non-negative");
+    if (batch == 0) return;
+    need(llr, "llr");
+    need(iterations_out, "iterations_out");
+    need(reason_out, "reason_out");
+    const int nd = static_cast<int>(m->decs.size());
+    const int32_t chunk = chunk_frames > 0 ? chunk_frames
+                                           : std::max<int32_t>(32, std::min<int32_t>(m->slots, (batch + 4 * nd - 1) / (4 * nd)));
+    const bool packed = (flags & BPDEC_BITS_PACKED) != 0;
+    const bool wb = bits_out != nullptr, wp = posteriors_out != nullptr, wq = q_trace_out != nullptr;
+    const int32_t ring = std::max(3 * chunk, m->slots + 2 * chunk);
+    // (re)open the per-decoder streams when the configuration changed
+    const bool same = m->open && m->p.d_max == p.d_max && m->p.use_pce == p.use_pce && m->p.use_vnr == p.use_vnr &&
+                      m->p.q_mode == p.q_mode && m->p.msg_clamp == p.msg_clamp && m->flags == flags &&
+                      m->want_bits == wb && m->want_post == wp && m->want_q == wq && m->ring >= ring;
+    if (!same) {
+      for (auto* d : m->decs) bpdec::gpu_stream_close(d);
+      m->open = false;
+      for (auto* d : m->decs) bpdec::gpu_stream_open(d, p, packed, wb, wp, wq, ring);
+      m->open = true;
+      m->p = p;
+      m->flags = flags;
+      m->want_bits = wb;
+      m->want_post = wp;
+      m->want_q = wq;
+      m->ring = ring;
+    }
+    const int64_t nchunks = (static_cast<int64_t>(batch) + chunk - 1) / chunk;
+    const size_t N = static_cast<size_t>(m->n_vars), MW = (static_cast<size_t>(m->n_checks) + 31) / 32;
+    const size_t row_bits = packed ? (N + 31) / 32 * sizeof(uint32_t) : N;
+    std::atomic<int64_t> next{0};
+    std::mutex err_mu;
+    std::string err;
+    int err_kind = 0;
+    std::vector<int64_t> taken(nd, 0);
+    auto worker = [&](int k) {
+      bpdec::GpuDecoder* d = m->decs[k];
+      std::deque<int64_t> inflight;
+      try {
+        for (;;) {
+          // two chunks in flight per decoder: the next one's upload overlaps
+          // the current one's decode, and its frames fill the tail's lanes
+          while (inflight.size() < 2) {
+            const int64_t c = next.fetch_add(1);
+            if (c >= nchunks) break;
+            const size_t f0 = static_cast<size_t>(c) * chunk;
+            const int32_t nf = static_cast<int32_t>(std::min<int64_t>(chunk, batch - static_cast<int64_t>(f0)));
+            bpdec::StreamOutputs o;
+            o.bits = wb ? static_cast<char*>(bits_out) + f0 * row_bits : nullptr;
+            o.iterations = iterations_out + f0;
+            o.reasons = reason_out + f0;
+            o.posteriors = wp ? posteriors_out + f0 * N : nullptr;
+            o.q_trace = wq ? q_trace_out + f0 * static_cast<size_t>(p.d_max) : nullptr;
+            inflight.push_back(bpdec::gpu_stream_submit(d, nf, llr + f0 * N, syndrome ? syndrome + f0 * MW : nullptr, o));
+            taken[k] += nf;
+          }
+          if (inflight.empty()) break;
+          bpdec::gpu_stream_wait(d, inflight.front());
+          inflight.pop_front();
+        }
+      } catch (const bpdec::ValidationError& e) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (err.empty()) err = e.what(), err_kind = 3;
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (err.empty()) err = e.what(), err_kind = 4;
+      }
+      for (int64_t t : inflight) {  // drain after an error
+        try {
+          bpdec::gpu_stream_wait(d, t);
+        } catch (...) {
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (int k = 0; k < nd; ++k) th.emplace_back(worker, k);
+    for (auto& t : th) t.join();
+    for (int k = 0; k < nd; ++k) m->frames_taken[k] += taken[k];
+    if (frames_per_decoder_out) std::copy(taken.begin(), taken.end(), frames_per_decoder_out);
+    if (err_kind == 3) throw bpdec::ValidationError(err);
+    if (err_kind) throw bpdec::CudaError(err);
   });
 }
 

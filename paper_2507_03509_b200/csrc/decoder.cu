@@ -35,6 +35,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
@@ -44,6 +51,7 @@
 #include <vector>
 
 #include "decoder.hpp"
+#include "devguard.hpp"
 #include "phi.cuh"
 #include "rng.hpp"
 
@@ -68,7 +76,7 @@ constexpr int kVarWarps = 4;    // warps per k_var block
 constexpr int kQTile = 64;     // variables per k_var tile and q partial sum (code-fixed order)
 constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
-enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompact = 5, kNumKernels = 6 };
+enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompact = 5, kSnapshot = 6, kTrace = 7, kNumKernels = 8 };
 // (kSyn = k_decide; kTerm is kept for the profiling ABI and stays 0)
 constexpr int kTermBlocks = 16;   // k_decide q-reduction blocks per group (q partial tree: fixed by the code)
 
@@ -121,6 +129,11 @@ struct Args {
                             // the live groups' layout (32, or 16 / 8 for a narrow tail group),
                             // [12] slots were moved (k_compact) since the last k_check
   unsigned long long* frame_iters;
+  // host polling: k_decide's deciding block copies counters[0..3] into slot
+  // poll_slot of this pinned, mapped host ring at the end of every step
+  // (no D2H copy between the step kernels)
+  int32_t* h_poll;
+  int32_t poll_slot;
   // decode parameters
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
   float clamp;
@@ -135,7 +148,23 @@ struct Args {
   uint8_t* out_reasons;
   float* out_post;
   double* out_qtrace;
+  uint8_t* out_syntrace;      // [batch][d_max] syndrome_ok per iteration, or null
+  float* out_ptrace;          // [batch][d_max][N] posteriors per iteration, or null
+  // stream mode (bpdec_stream_*): frame f's input and output rows live at
+  // ring position f % ring_cap of device rings; 0 = rows indexed by f
+  int32_t ring_cap;
+  const int32_t* fbatch;      // [ring_cap] batch slot of the frame at each ring position
+  int32_t* bdone;             // [kMaxStreamBatches] frames of each batch slot that stopped
+  uint8_t* ferr;              // [ring_cap] frame had a non-finite input LLR
 };
+
+constexpr int kMaxStreamBatches = 32;  // batches in flight in stream mode (poll ring reports them)
+constexpr int kPollWords = 4 + kMaxStreamBatches;
+
+// Row of frame f in the input / output buffers.
+__device__ __forceinline__ size_t frow(const Args& a, int f) {
+  return static_cast<size_t>(a.ring_cap ? f % a.ring_cap : f);
+}
 
 __device__ __forceinline__ float clampf(float x, float c) { return fminf(fmaxf(x, -c), c); }
 __device__ __forceinline__ uint32_t signbit_u(float x) { return __float_as_uint(x) >> 31; }
@@ -1404,7 +1433,7 @@ __device__ __forceinline__ uint32_t refill_lanes(const Args& a, int g, uint32_t 
   int take = 0, base = 0;
   if (lane == 0 && free != 0u) {
     const int want = __popc(free);
-    const int limit = min(a.batch, *reinterpret_cast<volatile int32_t*>(&a.counters[9]));
+    const int limit = min(a.batch, *reinterpret_cast<volatile int32_t*>(&a.counters[9]));  // stream: batch = INT_MAX
     int old = *reinterpret_cast<volatile int32_t*>(&a.counters[0]);
     for (;;) {  // bounded grab: frames beyond the limit stay queued
       take = max(0, min(want, limit - old));
@@ -1447,8 +1476,13 @@ __device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
   if (act) {
     it = a.slot_iter[s];
     f = a.slot_frame[s];
-    if (a.out_qtrace) a.out_qtrace[static_cast<size_t>(f) * a.d_max + (it - 1)] = q;
-    if (a.use_pce && !(__ldcg(&a.fail[g]) & bit)) {
+    const size_t fr = frow(a, f);
+    if (a.out_qtrace) a.out_qtrace[fr * a.d_max + (it - 1)] = q;
+    const bool syn_ok = !(__ldcg(&a.fail[g]) & bit);
+    // the observer's syndrome_ok is computed every iteration, PCE or not
+    // (decoder.cpp:110-112)
+    if (a.out_syntrace) a.out_syntrace[fr * a.d_max + (it - 1)] = syn_ok ? 1 : 0;
+    if (a.use_pce && syn_ok) {
       reason = 0;
     } else if (a.use_vnr && it >= 2 && q < a.qprev[s]) {
       reason = 1;
@@ -1459,9 +1493,10 @@ __device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
       a.slot_iter[s] = it + 1;
       a.qprev[s] = q;
     } else {
-      a.out_iters[f] = it;
-      a.out_reasons[f] = static_cast<uint8_t>(reason);
+      a.out_iters[fr] = it;
+      a.out_reasons[fr] = static_cast<uint8_t>(reason);
       a.stop_frame[s] = f;
+      if (a.bdone) atomicAdd(&a.bdone[a.fbatch[fr]], 1);
     }
   }
   const uint32_t stop = __ballot_sync(0xffffffffu, reason >= 0);
@@ -1510,7 +1545,60 @@ __global__ void __launch_bounds__(kThreads) k_decide(const Args a, int syn_block
   __threadfence();
   const int lane = threadIdx.x & 31;
   for (int g = static_cast<int>(threadIdx.x >> 5); g < a.G; g += kThreads / 32) decide_group(a, g, lane);
-  if (threadIdx.x == 0) a.counters[8] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.counters[8] = 0;
+    if (a.h_poll) {  // frames done / error flags of this step for the host loop
+      volatile int32_t* hp = a.h_poll + kPollWords * a.poll_slot;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) hp[k] = __ldcg(&a.counters[k]);
+      if (a.bdone)
+        for (int k = 0; k < kMaxStreamBatches; ++k) hp[4 + k] = __ldcg(&a.bdone[k]);
+      __threadfence_system();
+    }
+  }
+}
+
+// Posteriors of every active frame after this step's variable pass (the
+// observer's per-iteration posteriors, decoder.cpp:111-112), in the original
+// variable order: warp = (group, 32 variables), lane = variable.
+__global__ void __launch_bounds__(kThreads) k_trace_post(const Args a) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const int lw = __ldcg(&a.counters[11]);
+  const long long items = static_cast<long long>(a.G) * a.NW;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+    const int g = static_cast<int>(w / a.NW);
+    const int ch = static_cast<int>(w - static_cast<long long>(g) * a.NW);
+    uint32_t am = a.group_active[g];
+    if (am == 0u) continue;
+    const int i = ch * 32 + lane;
+    const bool valid = i < a.N;
+    const float* prow = nullptr;
+    if (valid) {
+      const int vm = __ldg(&a.vmap[i]);
+      prow = vm >= 0 ? (vm < a.NV ? a.post + rix(g, a.NV, vm, lw) : a.llr_h + rix(g, a.NH, vm, lw))
+                     : a.d1post + rix(g, a.N1, -1 - vm, lw);
+    }
+    while (am) {
+      const int l = __ffs(am) - 1;
+      am &= am - 1;
+      const int s = g * kLanes + l;
+      const int f = a.slot_frame[s];
+      const int it = a.slot_iter[s];
+      if (valid) a.out_ptrace[(frow(a, f) * a.d_max + (it - 1)) * a.N + i] = prow[l];
+    }
+  }
+}
+
+// Snapshot of out_iters (frames whose outputs are final) into mapped host
+// memory, in stream order after a step's k_turnover: a frame with a non-zero
+// entry has been extracted by then (eager output copies).
+__global__ void k_snapshot(const int32_t* __restrict__ iters, int32_t n, int32_t* h_out) {
+  pdl_begin();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) h_out[i] = iters[i];
+  __threadfence_system();
 }
 
 // ---------------------------------------------------------- k_turnover --
@@ -1569,13 +1657,13 @@ __device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm,
       const uint32_t y = __shfl_xor_sync(0xffffffffu, x, k);
       x = (lane & k) ? ((x & ~mk) | ((y & ~mk) >> k)) : ((x & mk) | ((y & mk) << k));
     }
-    if ((sm >> lane) & 1u) a.out_bits_pk[static_cast<size_t>(fr) * a.NW + ch] = x;
+    if ((sm >> lane) & 1u) a.out_bits_pk[frow(a, fr) * a.NW + ch] = x;
     return;
   }
   while (sm) {
     const int l = __ffs(sm) - 1;
     sm &= sm - 1;
-    const int f = __shfl_sync(0xffffffffu, fr, l);
+    const size_t f = frow(a, __shfl_sync(0xffffffffu, fr, l));
     uint32_t bit = (word >> l) & 1u;
     float pv = 0.0f;
     if (deg0) {
@@ -1585,12 +1673,12 @@ __device__ __forceinline__ void extract_chunk(const Args& a, int g, uint32_t sm,
       pv = prow[l];
     }
     if (valid) {
-      if (a.out_bits_u8) a.out_bits_u8[static_cast<size_t>(f) * a.N + i] = static_cast<uint8_t>(bit);
-      if (WANT_POST) a.out_post[static_cast<size_t>(f) * a.N + i] = pv;
+      if (a.out_bits_u8) a.out_bits_u8[f * a.N + i] = static_cast<uint8_t>(bit);
+      if (WANT_POST) a.out_post[f * a.N + i] = pv;
     }
     if (a.out_bits_pk) {
       const uint32_t pw = __ballot_sync(0xffffffffu, bit);
-      if (lane == 0) a.out_bits_pk[static_cast<size_t>(f) * a.NW + ch] = pw;
+      if (lane == 0) a.out_bits_pk[f * a.NW + ch] = pw;
     }
   }
 }
@@ -1606,12 +1694,13 @@ __device__ __forceinline__ void load_quad_tile(const Args& a, int g, uint32_t lm
   // variables; all 4 x 4 loads in flight before any use
   constexpr int kRpw = 32 / kW;
   float v[kTurnChunks][kRpw];
+  size_t frs[kRpw];
 #pragma unroll
   for (int m = 0; m < kRpw; ++m) {
     const int r = warp + kW * m;
     const bool on = (lm >> r) & 1u;
-    const int f = on ? a.pending_frame[g * kLanes + r] : 0;
-    const float* src = a.in_llr + static_cast<size_t>(f) * a.N;
+    frs[m] = frow(a, on ? a.pending_frame[g * kLanes + r] : 0);
+    const float* src = a.in_llr + frs[m] * a.N;
 #pragma unroll
     for (int c = 0; c < kTurnChunks; ++c) {
       const int i = (ch0 + c) * 32 + lane;
@@ -1621,11 +1710,14 @@ __device__ __forceinline__ void load_quad_tile(const Args& a, int g, uint32_t lm
   bool bad = false;
 #pragma unroll
   for (int m = 0; m < kRpw; ++m) {
+    bool bm = false;
 #pragma unroll
     for (int c = 0; c < kTurnChunks; ++c) {
-      bad |= !isfinite(v[c][m]);
+      bm |= !isfinite(v[c][m]);
       tile[c][warp + kW * m][lane] = v[c][m];
     }
+    if (bm && a.ferr) a.ferr[frs[m]] = 1;  // stream mode: the batch of this frame fails
+    bad |= bm;
   }
   if (bad) atomicOr(&a.counters[2], 1);
   __syncthreads();
@@ -1677,12 +1769,15 @@ __device__ __forceinline__ void load_chunk_sparse(const Args& a, int g, uint32_t
   for (int k = 0; k < kSparseLoad; ++k) f[k] = a.pending_frame[g * kLanes + max(r[k], 0)];  // safe index
 #pragma unroll
   for (int k = 0; k < kSparseLoad; ++k)  // predicated loads: no branch per load
-    v[k] = ld_pred(a.in_llr + static_cast<size_t>(f[k]) * a.N + (in ? i : 0), r[k] >= 0 && in);
+    v[k] = ld_pred(a.in_llr + frow(a, f[k]) * a.N + (in ? i : 0), r[k] >= 0 && in);
   bool bad = false;
 #pragma unroll
   for (int k = 0; k < kSparseLoad; ++k) {
     if (r[k] < 0 || !in) continue;
-    bad |= !isfinite(v[k]);
+    if (!isfinite(v[k])) {
+      bad = true;
+      if (a.ferr) a.ferr[frow(a, f[k])] = 1;
+    }
     if (vj >= 0) {
       a.llr_h[(static_cast<size_t>(g) * a.NH + vj) * kLanes + r[k]] = v[k];
       if (vj < a.NV) a.post[(static_cast<size_t>(g) * a.NV + vj) * kLanes + r[k]] = v[k];
@@ -1794,7 +1889,7 @@ __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_bl
         uint32_t mine = 0u;  // lane r: input word wi of the frame entering slot r
         if ((lm >> lane) & 1u) {
           const int f = a.pending_frame[g * kLanes + lane];
-          mine = __ldg(&a.in_syn[static_cast<size_t>(f) * a.MW + wi]);
+          mine = __ldg(&a.in_syn[frow(a, f) * a.MW + wi]);
         }
         uint32_t col = 0u;  // lane k: check wi*32+k over the 32 slots
 #pragma unroll
@@ -1830,6 +1925,9 @@ __global__ void __launch_bounds__(kThreads) k_turnover(const Args a, int item_bl
         atomicAdd(&a.counters[3], 1);
       }
     }
+    // frames entered: the compaction hysteresis starts over (stream mode
+    // can refill after a compaction)
+    if (threadIdx.x == 0) a.counters[4] = a.G * kLanes + 32;
   }
 }
 
@@ -1857,7 +1955,9 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   pl.narrow = 0;
   const int G = a.G;
   if (G > kMaxCompactGroups || G < 2) return;
-  if (a.counters[0] < a.batch) return;  // frames still queued: freed slots get refilled instead
+  // frames still queued: freed slots get refilled instead (stream mode: the
+  // frames submitted so far)
+  if (a.counters[0] < (a.ring_cap ? *reinterpret_cast<volatile int32_t*>(&a.counters[9]) : a.batch)) return;
   int total = 0, alive = 0;
   for (int g = 0; g < G; ++g) {
     cnt[g] = __popc(a.group_active[g]);
@@ -2222,6 +2322,12 @@ class GpuDecoder {
   void sample_device(double snr, double beta_lo, double beta_hi, double rate, uint64_t seed, int64_t first_frame,
                      int32_t n_frames, bool all_zero,
                      float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t stream);
+  // stream mode (bpdec_stream_*)
+  void stream_open(const DecodeParams& p, bool packed, bool want_bits, bool want_post, bool want_q, int32_t ring_frames);
+  int64_t stream_submit(int32_t n, const float* llr, const uint32_t* syn, const StreamOutputs& o);
+  bool stream_query(int64_t ticket);
+  void stream_wait(int64_t ticket);
+  void stream_close();
 
   int S = 0;
   int G = 0;
@@ -2234,10 +2340,14 @@ class GpuDecoder {
   double prof_ms[kNumKernels] = {};
   int64_t prof_launches[kNumKernels] = {};
   double prof_frame_iters = 0.0;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};
   int64_t compactions = 0;
 
  private:
+  struct Stream;
+  void stream_worker();
+  void stream_release() noexcept;
+  std::unique_ptr<Stream> stream_;
   template <typename F>
   void launch(int kid, cudaStream_t st, F&& f);
   void run_step(const Args& a, cudaStream_t st, bool want_post);
@@ -2251,12 +2361,12 @@ class GpuDecoder {
   int32_t* d_check_vars = nullptr;
   std::vector<void*> owned;
   cudaStream_t own_stream = nullptr;
-  int32_t* h_counters = nullptr;  // pinned ring [kRing][4]
+  int32_t* h_counters = nullptr;  // pinned, mapped poll ring [kRing][kPollWords] (k_decide)
   static constexpr int kRing = 8;
   cudaEvent_t ring_ev[kRing] = {};
   std::vector<cudaEvent_t> prof_ev;
   std::vector<int> prof_kid;
-  Scratch s_llr, s_syn, s_bits, s_iters, s_reasons, s_post, s_qtrace;
+  Scratch s_llr, s_syn, s_bits, s_iters, s_reasons, s_post, s_qtrace, s_syntrace, s_ptrace;
   // host-input staging (bpdec_decoder_stage_inputs): the H2D copy of a later
   // batch runs on copy_stream while the current batch decodes
   struct Staged {
@@ -2280,7 +2390,8 @@ class GpuDecoder {
   // out_stream (k_decide writes out_iters at the stop; a snapshot of it,
   // taken after a polled step, says which rows are final)
   cudaStream_t out_stream = nullptr;
-  int32_t* h_done = nullptr;  // pinned snapshot of out_iters
+  int32_t* h_done = nullptr;  // pinned, mapped snapshot of out_iters (k_snapshot)
+  int32_t* h_done_dev = nullptr;
   size_t h_done_cap = 0;
   cudaEvent_t done_ev = nullptr;
   int grid_check = 0, grid_var = 0, grid_syn = 0, sms_ = 148;
@@ -2542,7 +2653,9 @@ void GpuDecoder::init(const Code& code, int max_slots) {
   CUDA_OK(cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming));
   for (auto& sg : staged) CUDA_OK(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
   for (cudaEvent_t* e : {&up_start, &up_first, &up_done}) CUDA_OK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  CUDA_OK(cudaHostAlloc(&h_counters, kRing * 4 * sizeof(int32_t), cudaHostAllocDefault));
+  CUDA_OK(cudaHostAlloc(&h_counters, kRing * kPollWords * sizeof(int32_t), cudaHostAllocMapped));
+  std::memset(h_counters, 0, kRing * kPollWords * sizeof(int32_t));
+  CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&base.h_poll), h_counters, 0));
   for (auto& e : ring_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   const int sms = prop.multiProcessorCount;
@@ -2583,7 +2696,10 @@ void GpuDecoder::init(const Code& code, int max_slots) {
   turn_check_blocks = sms * 2;
 }
 
-GpuDecoder::~GpuDecoder() { release(); }
+GpuDecoder::~GpuDecoder() {
+  stream_release();
+  release();
+}
 
 void GpuDecoder::release() noexcept {
   cudaSetDevice(device);
@@ -2618,8 +2734,10 @@ void GpuDecoder::release() noexcept {
 
 template <typename F>
 void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
-  // events come from a pool reused across decodes (creation is not free)
+  // events come from a pool reused across decodes (creation is not free);
+  // no per-launch events in stream mode (its step loop has no end)
   const size_t k = prof_kid.size();
+  const bool profiling = this->profiling && !stream_;
   if (profiling) {
     while (prof_ev.size() < 2 * (k + 1)) {
       cudaEvent_t e;
@@ -2670,8 +2788,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
     else
       launch_pdl(k_var<1>, grid_var, kVarWarps * 32, var_smem, st, a);
   });
+  if (a.out_ptrace) launch(kTrace, st, [&] { launch_pdl(k_trace_post, sms_ * 4, kThreads, 0, st, a); });
   {
-    const int syn_blocks = a.use_pce ? grid_syn : 0;
+    const int syn_blocks = (a.use_pce || a.out_syntrace) ? grid_syn : 0;
     launch(kSyn, st, [&] {
       launch_pdl(k_decide, syn_blocks + G * kTermBlocks, kThreads, G * sizeof(uint32_t), st, a, syn_blocks);
     });
@@ -2683,7 +2802,9 @@ void GpuDecoder::run_step(const Args& a, cudaStream_t st, bool want_post) {
 }
 
 void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStream_t st_in) {
-  CUDA_OK(cudaSetDevice(device));
+  DeviceGuard dg(device);
+  CUDA_OK(dg.status());
+  if (stream_) throw ConfigError("decode: a stream is open on this decoder (bpdec_stream_close first)");
   const cudaStream_t st = st_in ? st_in : own_stream;
   if (p.d_max <= 0) throw ValidationError("decode: d_max must be positive");
   if (!(p.msg_clamp > 0.0f)) throw ValidationError("decode: msg_clamp must be positive");
@@ -2693,7 +2814,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   if (b.iterations == nullptr || b.reasons == nullptr) throw ValidationError("decode: iterations/reason outputs are required");
   Args a = base;
   const size_t B = static_cast<size_t>(b.batch);
-  const bool want_post = b.posteriors != nullptr;
+  const bool want_post = b.posteriors != nullptr || b.post_trace != nullptr;
   if (want_post && a.d1post == nullptr) {
     a.d1post = dalloc<float>(static_cast<size_t>(G) * a.N1 * kLanes, &dev_bytes);
     base.d1post = a.d1post;
@@ -2759,9 +2880,16 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   a.out_post = static_cast<float*>(dev_out(b.posteriors, B * a.N * sizeof(float), s_post, &st_post));
   a.out_qtrace = static_cast<double*>(dev_out(b.q_trace, B * p.d_max * sizeof(double), s_qtrace, &st_q));
   if (a.out_qtrace) CUDA_OK(cudaMemsetAsync(a.out_qtrace, 0xff, B * p.d_max * sizeof(double), st));  // NaN
+  if (want_post && a.out_post == nullptr) a.out_post = static_cast<float*>(s_post.get(B * a.N * sizeof(float)));
+  bool st_syt, st_pt;
+  const size_t ptrace_n = B * static_cast<size_t>(p.d_max) * a.N;
+  a.out_syntrace = static_cast<uint8_t*>(dev_out(b.syn_trace, B * p.d_max, s_syntrace, &st_syt));
+  a.out_ptrace = static_cast<float*>(dev_out(b.post_trace, ptrace_n * sizeof(float), s_ptrace, &st_pt));
+  if (a.out_syntrace) CUDA_OK(cudaMemsetAsync(a.out_syntrace, 0xff, B * p.d_max, st));
+  if (a.out_ptrace) CUDA_OK(cudaMemsetAsync(a.out_ptrace, 0xff, ptrace_n * sizeof(float), st));  // NaN past the stop
   // eager output copies: per-frame rows of the staged host outputs
   const size_t row_bits = b.bits_packed ? a.NW * sizeof(uint32_t) : static_cast<size_t>(a.N);
-  const bool eager = (st_bits || st_post || st_q) && a.out_iters != nullptr && !no_eager;
+  const bool eager = (st_bits || st_post || st_q) && a.out_iters != nullptr && !no_eager && !st_syt && !st_pt;
   std::vector<char> copied;
   if (eager) {
     CUDA_OK(cudaMemsetAsync(a.out_iters, 0, B * sizeof(int32_t), st));  // 0 = still decoding
@@ -2769,7 +2897,8 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
       if (h_done) cudaFreeHost(h_done);
       h_done = nullptr;
       h_done_cap = 0;
-      CUDA_OK(cudaHostAlloc(&h_done, B * sizeof(int32_t), cudaHostAllocDefault));
+      CUDA_OK(cudaHostAlloc(&h_done, B * sizeof(int32_t), cudaHostAllocMapped));
+      CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_done_dev), h_done, 0));
       h_done_cap = B;
     }
     copied.assign(B, 0);
@@ -2802,7 +2931,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
     }
   };
   int64_t last_done_seen = 0;  // frames-done count when the last snapshot was requested
-  bool snap_pending = false;
+  bool snap_pending = false, snap_request = false;
 
   // initial slot assignment (frames 0..min(B,S)-1 -> slots 0..) and state
   // reset on the device: no host copies, no host synchronisation
@@ -2865,32 +2994,42 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
         CUDA_OK(q);
       }
     }
-    run_step(a, st, want_post);
     const int slot = static_cast<int>(step % kRing);
-    CUDA_OK(cudaMemcpyAsync(h_counters + 4 * slot, a.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    a.poll_slot = slot;  // k_decide of this step reports into h_counters[slot]
+    run_step(a, st, want_post);
+    if (snap_request) {
+      // snapshot of out_iters in stream order after this step's k_turnover:
+      // every frame it marks stopped has had its outputs extracted
+      snap_request = false;
+      launch(kSnapshot, st, [&] {
+        launch_pdl(k_snapshot, 4, 256, 0, st, static_cast<const int32_t*>(a.out_iters), b.batch, h_done_dev);
+      });
+      CUDA_OK(cudaEventRecord(done_ev, st));
+      snap_pending = true;
+    }
     CUDA_OK(cudaEventRecord(ring_ev[slot], st));
     if (step >= kLag) {
       const int old = static_cast<int>((step - kLag) % kRing);
       CUDA_OK(cudaEventSynchronize(ring_ev[old]));
-      if (h_counters[4 * old + 2] != 0) break;  // invalid input detected
-      if (h_counters[4 * old + 1] >= b.batch) done = true;
+      const volatile int32_t* hp = h_counters + kPollWords * old;
+      if (hp[2] != 0) break;  // invalid input detected
+      if (hp[1] >= b.batch) done = true;
       if (eager) {
-        // a finished snapshot: copy the rows it marks final
+        // a finished snapshot: copy the rows it marks final (out_stream is
+        // ordered after the snapshot, and so after the extraction)
         if (snap_pending && cudaEventQuery(done_ev) == cudaSuccess) {
           snap_pending = false;
+          CUDA_OK(cudaStreamWaitEvent(out_stream, done_ev, 0));
           copy_finished(h_done, out_stream, false);
         } else {
           (void)cudaGetLastError();  // cudaErrorNotReady is not an error here
         }
-        // frames stopped since the last snapshot: snapshot out_iters after
-        // that polled step (its outputs are extracted by then)
-        const int64_t nd = h_counters[4 * old + 1];
+        // frames stopped since the last snapshot: request a snapshot after
+        // the next launched step
+        const int64_t nd = hp[1];
         if (!snap_pending && !done && nd >= last_done_seen + 8) {
           last_done_seen = nd;
-          CUDA_OK(cudaStreamWaitEvent(out_stream, ring_ev[old], 0));
-          CUDA_OK(cudaMemcpyAsync(h_done, a.out_iters, B * sizeof(int32_t), cudaMemcpyDeviceToHost, out_stream));
-          CUDA_OK(cudaEventRecord(done_ev, out_stream));
-          snap_pending = true;
+          snap_request = true;
         }
       }
     }
@@ -2920,6 +3059,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
   if (eager) {
     if (snap_pending) {
       CUDA_OK(cudaEventSynchronize(done_ev));
+      CUDA_OK(cudaStreamWaitEvent(out_stream, done_ev, 0));
       copy_finished(h_done, out_stream, false);
     }
     copy_finished(nullptr, st, true);
@@ -2930,6 +3070,9 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
     if (st_q)
       CUDA_OK(cudaMemcpyAsync(b.q_trace, a.out_qtrace, B * p.d_max * sizeof(double), cudaMemcpyDeviceToHost, st));
   }
+  if (st_syt) CUDA_OK(cudaMemcpyAsync(b.syn_trace, a.out_syntrace, B * p.d_max, cudaMemcpyDeviceToHost, st));
+  if (st_pt)
+    CUDA_OK(cudaMemcpyAsync(b.post_trace, a.out_ptrace, ptrace_n * sizeof(float), cudaMemcpyDeviceToHost, st));
   if (st_it) CUDA_OK(cudaMemcpyAsync(b.iterations, a.out_iters, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   if (st_rs) CUDA_OK(cudaMemcpyAsync(b.reasons, a.out_reasons, B, cudaMemcpyDeviceToHost, st));
   CUDA_OK(cudaStreamSynchronize(st));
@@ -2937,7 +3080,9 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
 }
 
 void GpuDecoder::stage_inputs(int32_t batch, const float* llr_host, const uint32_t* syn_host) {
-  CUDA_OK(cudaSetDevice(device));
+  DeviceGuard dg(device);
+  CUDA_OK(dg.status());
+  if (stream_) throw ConfigError("stage_inputs: a stream is open on this decoder (submit to it instead)");
   if (batch <= 0) throw ValidationError("stage_inputs: batch must be positive");
   if (llr_host == nullptr) throw ValidationError("stage_inputs: null LLR pointer");
   if (is_device_ptr(llr_host) || (syn_host && is_device_ptr(syn_host)))
@@ -2963,7 +3108,8 @@ void GpuDecoder::stage_inputs(int32_t batch, const float* llr_host, const uint32
 void GpuDecoder::sample_device(double snr, double beta_lo, double beta_hi, double rate, uint64_t seed,
                                int64_t first_frame, int32_t n_frames, bool all_zero,
                                float* d_llr, uint32_t* d_syn, uint32_t* d_x, cudaStream_t st_in) {
-  CUDA_OK(cudaSetDevice(device));
+  DeviceGuard dg(device);
+  CUDA_OK(dg.status());
   const cudaStream_t st = st_in ? st_in : own_stream;
   if (snr > 0.0) {
     if (!std::isfinite(snr)) throw ValidationError("sample: snr must be positive and finite");
@@ -2986,12 +3132,396 @@ void GpuDecoder::sample_device(double snr, double beta_lo, double beta_hi, doubl
   CUDA_OK(cudaStreamSynchronize(st));
 }
 
+
+// ------------------------------------------------------------ stream mode --
+// Batches submitted back to back decode as ONE frame stream: frame g (global
+// index since the stream opened) has its input and output rows at ring
+// position g % cap of device rings, becomes available to the refill when its
+// batch's upload has landed (counters[9], advanced by a 4-byte copy on the
+// copy stream after the batch's rows), and a worker thread keeps launching
+// decoding steps while frames are in flight.  k_decide counts stopped frames
+// per batch slot (bdone, via fbatch) and reports the counts with the step's
+// poll words; a batch whose count reached its size has final outputs after
+// that step, which are then copied to the caller's buffers on out_stream.
+// So the lanes an earlier batch's tail frees are refilled with the next
+// batch's frames in the same step, and batch k+1's upload overlaps batch k's
+// decode.  Per-frame results do not depend on slot, order or neighbours, so
+// every batch's outputs equal a blocking decode of that batch.
+struct GpuDecoder::Stream {
+  DecodeParams p;
+  bool packed = false, want_bits = true, want_post = false, want_q = false;
+  int32_t cap = 0;
+  // device rings
+  float* r_llr = nullptr;
+  uint32_t* r_syn = nullptr;
+  int32_t* r_fbatch = nullptr;
+  uint8_t* r_ferr = nullptr;
+  int32_t* r_bdone = nullptr;
+  void* r_bits = nullptr;
+  int32_t* r_iters = nullptr;
+  uint8_t* r_reasons = nullptr;
+  float* r_post = nullptr;
+  double* r_q = nullptr;
+  // pinned host staging
+  int32_t* h_fbatch = nullptr;  // [cap]
+  int32_t* h_avail = nullptr;   // [kMaxStreamBatches]
+  uint8_t* h_ferr = nullptr;    // [cap]
+  Args a{};
+  struct Batch {
+    int state = 0;  // 0 free, 1 decoding, 2 copying outputs
+    int64_t ticket = -1, g0 = 0, target = 0;
+    int32_t n = 0;
+    StreamOutputs out;
+    cudaEvent_t ev = nullptr;
+  };
+  Batch batches[kMaxStreamBatches];
+  int64_t slot_total[kMaxStreamBatches] = {};  // cumulative frames per batch slot (bdone targets)
+  std::deque<int64_t> order;    // tickets of live batches in submission order (ring frees in order)
+  std::map<int64_t, std::string> finished;  // ticket -> error ("" = ok) until waited for
+  std::mutex mu, submit_mu;
+  std::condition_variable cv_work, cv_done;
+  std::thread worker;
+  bool closing = false;
+  std::string fatal;            // worker error: every pending and later call fails with it
+  int64_t next_ticket = 0, next_g = 0, free_g = 0;
+  int64_t decoding = 0;         // batches in state 1
+  int64_t copying = 0;          // batches in state 2
+};
+
+void GpuDecoder::stream_open(const DecodeParams& p, bool packed, bool want_bits, bool want_post, bool want_q,
+                             int32_t ring_frames) {
+  DeviceGuard dg(device);
+  CUDA_OK(dg.status());
+  if (stream_) throw ConfigError("stream: already open on this decoder");
+  if (p.d_max <= 0) throw ValidationError("decode: d_max must be positive");
+  if (!(p.msg_clamp > 0.0f)) throw ValidationError("decode: msg_clamp must be positive");
+  if (ring_frames <= 0) ring_frames = 4 * S;
+  if (ring_frames < S) ring_frames = S;
+  auto sp = std::make_unique<Stream>();
+  Stream& z = *sp;
+  z.p = p;
+  z.packed = packed;
+  z.want_bits = want_bits;
+  z.want_post = want_post;
+  z.want_q = want_q;
+  z.cap = ring_frames;
+  const size_t C = static_cast<size_t>(z.cap);
+  std::vector<void*> got;
+  auto alloc = [&](size_t bytes) {
+    void* q = nullptr;
+    CUDA_OK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+    got.push_back(q);
+    return q;
+  };
+  try {
+    z.r_llr = static_cast<float*>(alloc(C * base.N * sizeof(float)));
+    z.r_syn = static_cast<uint32_t*>(alloc(C * base.MW * sizeof(uint32_t)));
+    z.r_fbatch = static_cast<int32_t*>(alloc(C * sizeof(int32_t)));
+    z.r_ferr = static_cast<uint8_t*>(alloc(C));
+    z.r_bdone = static_cast<int32_t*>(alloc(kMaxStreamBatches * sizeof(int32_t)));
+    if (want_bits) z.r_bits = alloc(packed ? C * base.NW * sizeof(uint32_t) : C * base.N);
+    z.r_iters = static_cast<int32_t*>(alloc(C * sizeof(int32_t)));
+    z.r_reasons = static_cast<uint8_t*>(alloc(C));
+    if (want_post) z.r_post = static_cast<float*>(alloc(C * base.N * sizeof(float)));
+    if (want_q) z.r_q = static_cast<double*>(alloc(C * p.d_max * sizeof(double)));
+    if (want_post && base.d1post == nullptr)
+      base.d1post = dalloc<float>(static_cast<size_t>(G) * base.N1 * kLanes, &dev_bytes);
+    CUDA_OK(cudaMemset(z.r_bdone, 0, kMaxStreamBatches * sizeof(int32_t)));
+    CUDA_OK(cudaMemset(z.r_ferr, 0, C));
+    CUDA_OK(cudaHostAlloc(&z.h_fbatch, C * sizeof(int32_t), cudaHostAllocDefault));
+    CUDA_OK(cudaHostAlloc(&z.h_avail, kMaxStreamBatches * sizeof(int32_t), cudaHostAllocDefault));
+    CUDA_OK(cudaHostAlloc(&z.h_ferr, C, cudaHostAllocDefault));
+    for (auto& bt : z.batches) CUDA_OK(cudaEventCreateWithFlags(&bt.ev, cudaEventDisableTiming));
+  } catch (...) {
+    for (void* q : got) cudaFree(q);
+    if (z.h_fbatch) cudaFreeHost(z.h_fbatch);
+    if (z.h_avail) cudaFreeHost(z.h_avail);
+    if (z.h_ferr) cudaFreeHost(z.h_ferr);
+    for (auto& bt : z.batches)
+      if (bt.ev) cudaEventDestroy(bt.ev);
+    throw;
+  }
+  Args& a = z.a;
+  a = base;
+  a.batch = INT32_MAX;  // the refill limit is counters[9] (frames uploaded)
+  a.d_max = p.d_max;
+  a.use_pce = p.use_pce;
+  a.use_vnr = p.use_vnr;
+  a.q_mode = p.q_mode;
+  a.clamp = p.msg_clamp;
+  a.narrow_ok = 0;  // a narrow tail group cannot take refills
+  a.in_llr = z.r_llr;
+  a.in_syn = z.r_syn;
+  a.out_bits_u8 = (want_bits && !packed) ? static_cast<uint8_t*>(z.r_bits) : nullptr;
+  a.out_bits_pk = (want_bits && packed) ? static_cast<uint32_t*>(z.r_bits) : nullptr;
+  a.out_iters = z.r_iters;
+  a.out_reasons = z.r_reasons;
+  a.out_post = z.r_post;
+  a.out_qtrace = z.r_q;
+  a.out_syntrace = nullptr;
+  a.out_ptrace = nullptr;
+  a.ring_cap = z.cap;
+  a.fbatch = z.r_fbatch;
+  a.bdone = z.r_bdone;
+  a.ferr = z.r_ferr;
+  // empty decoder: no frames, none available; refills start as batches land
+  k_decode_init<<<1, 1024, 0, own_stream>>>(a, 0, 0);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaStreamSynchronize(own_stream));
+  stream_ = std::move(sp);
+  stream_->worker = std::thread([this] { stream_worker(); });
+}
+
+int64_t GpuDecoder::stream_submit(int32_t n, const float* llr, const uint32_t* syn, const StreamOutputs& o) {
+  if (!stream_) throw ConfigError("stream: not open");
+  Stream& z = *stream_;
+  if (n <= 0) throw ValidationError("stream: batch must be positive");
+  if (n > z.cap) throw ValidationError("stream: batch larger than the stream's ring (" + std::to_string(z.cap) + " frames)");
+  if (llr == nullptr) throw ValidationError("decode: null LLR pointer");
+  if (o.iterations == nullptr || o.reasons == nullptr) throw ValidationError("decode: iterations/reason outputs are required");
+  if ((o.bits && !z.want_bits) || (o.posteriors && !z.want_post) || (o.q_trace && !z.want_q))
+    throw ValidationError("stream: an output was requested that the stream was not opened for");
+  DeviceGuard dg(device);
+  CUDA_OK(dg.status());
+  std::lock_guard<std::mutex> order_lock(z.submit_mu);  // ring positions and counters[9] in submission order
+  int64_t t, g0;
+  int slot;
+  {
+    std::unique_lock<std::mutex> lk(z.mu);
+    z.cv_done.wait(lk, [&] {
+      return !z.fatal.empty() || (z.next_g + n - z.free_g <= z.cap &&
+                                  z.batches[z.next_ticket % kMaxStreamBatches].state == 0);
+    });
+    if (!z.fatal.empty()) throw CudaError(z.fatal);
+    if (z.next_g + n > (int64_t{1} << 30)) throw ConfigError("stream: frame index space exhausted; reopen the stream");
+    t = z.next_ticket++;
+    slot = static_cast<int>(t % kMaxStreamBatches);
+    g0 = z.next_g;
+  }
+  const size_t C = static_cast<size_t>(z.cap);
+  const size_t p0 = static_cast<size_t>(g0 % z.cap);
+  const size_t n1 = std::min<size_t>(static_cast<size_t>(n), C - p0), n2 = static_cast<size_t>(n) - n1;
+  const cudaStream_t cs = copy_stream;
+  // rows [p0, p0+n1) and [0, n2) of a ring
+  auto rows = [&](auto* ring, const auto* src, size_t w) {
+    using T = std::remove_const_t<std::remove_pointer_t<decltype(src)>>;
+    CUDA_OK(cudaMemcpyAsync(ring + p0 * w, src, n1 * w * sizeof(T), cudaMemcpyDefault, cs));
+    if (n2) CUDA_OK(cudaMemcpyAsync(ring, src + n1 * w, n2 * w * sizeof(T), cudaMemcpyDefault, cs));
+  };
+  auto fill = [&](void* ring, size_t w, int value) {
+    CUDA_OK(cudaMemsetAsync(static_cast<char*>(ring) + p0 * w, value, n1 * w, cs));
+    if (n2) CUDA_OK(cudaMemsetAsync(ring, value, n2 * w, cs));
+  };
+  for (size_t i = 0; i < static_cast<size_t>(n); ++i) z.h_fbatch[(p0 + i) % C] = slot;
+  CUDA_OK(cudaMemcpyAsync(z.r_fbatch + p0, z.h_fbatch + p0, n1 * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+  if (n2) CUDA_OK(cudaMemcpyAsync(z.r_fbatch, z.h_fbatch, n2 * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+  fill(z.r_ferr, 1, 0);
+  if (z.want_q) fill(z.r_q, z.p.d_max * sizeof(double), 0xff);  // NaN past the stop
+  rows(z.r_llr, llr, base.N);
+  if (syn) rows(z.r_syn, syn, base.MW);
+  else fill(z.r_syn, base.MW * sizeof(uint32_t), 0);
+  z.h_avail[slot] = static_cast<int32_t>(g0 + n);
+  {
+    std::lock_guard<std::mutex> lk(z.mu);
+    Stream::Batch& bt = z.batches[slot];
+    // bdone[slot] is cumulative (never reset, so a poll taken before this
+    // batch's frames count cannot look complete): the batch is done at
+    // the slot's previous total + n
+    z.slot_total[slot] += n;
+    bt.target = z.slot_total[slot];
+    bt.state = 1;
+    bt.ticket = t;
+    bt.g0 = g0;
+    bt.n = n;
+    bt.out = o;
+    z.order.push_back(t);
+    z.next_g = g0 + n;
+    ++z.decoding;
+  }
+  // the frames become available once their rows have landed
+  CUDA_OK(cudaMemcpyAsync(base.counters + 9, z.h_avail + slot, sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+  z.cv_work.notify_one();
+  return t;
+}
+
+void GpuDecoder::stream_worker() {
+  Stream& z = *stream_;
+  cudaSetDevice(device);
+  const cudaStream_t st = own_stream;
+  constexpr int kLag = 2;
+  int64_t step = 0, polled = 0;  // steps launched / polled
+  Args a = z.a;
+  // outputs of batch bt (ring rows -> caller buffers) on out_stream
+  auto copy_out = [&](Stream::Batch& bt) {
+    const size_t C = static_cast<size_t>(z.cap);
+    const size_t p0 = static_cast<size_t>(bt.g0 % z.cap);
+    const size_t n1 = std::min<size_t>(static_cast<size_t>(bt.n), C - p0), n2 = static_cast<size_t>(bt.n) - n1;
+    auto rows = [&](void* dst, const void* ring, size_t rb) {
+      if (dst == nullptr) return;
+      CUDA_OK(cudaMemcpyAsync(dst, static_cast<const char*>(ring) + p0 * rb, n1 * rb, cudaMemcpyDefault, out_stream));
+      if (n2)
+        CUDA_OK(cudaMemcpyAsync(static_cast<char*>(dst) + n1 * rb, ring, n2 * rb, cudaMemcpyDefault, out_stream));
+    };
+    rows(bt.out.bits, z.r_bits, z.packed ? base.NW * sizeof(uint32_t) : static_cast<size_t>(base.N));
+    rows(bt.out.iterations, z.r_iters, sizeof(int32_t));
+    rows(bt.out.reasons, z.r_reasons, 1);
+    rows(bt.out.posteriors, z.r_post, base.N * sizeof(float));
+    rows(bt.out.q_trace, z.r_q, z.p.d_max * sizeof(double));
+    // per-frame input error flags, to the same ring positions of h_ferr
+    CUDA_OK(cudaMemcpyAsync(z.h_ferr + p0, z.r_ferr + p0, n1, cudaMemcpyDeviceToHost, out_stream));
+    if (n2) CUDA_OK(cudaMemcpyAsync(z.h_ferr, z.r_ferr, n2, cudaMemcpyDeviceToHost, out_stream));
+    CUDA_OK(cudaEventRecord(bt.ev, out_stream));
+  };
+  auto finish = [&](Stream::Batch& bt) {  // outputs copied: ticket done, ring rows free
+    const size_t C = static_cast<size_t>(z.cap);
+    const size_t p0 = static_cast<size_t>(bt.g0 % z.cap);
+    bool bad = false;
+    for (int32_t i = 0; i < bt.n; ++i) bad |= z.h_ferr[(p0 + i) % C] != 0;
+    std::lock_guard<std::mutex> lk(z.mu);
+    z.finished[bt.ticket] = bad ? "decode: non-finite input LLR" : "";
+    bt.state = 0;
+    --z.copying;
+    while (!z.order.empty()) {
+      Stream::Batch& f = z.batches[z.order.front() % kMaxStreamBatches];
+      if (f.ticket == z.order.front() && f.state != 0) break;
+      z.order.pop_front();
+    }
+    z.free_g = z.order.empty() ? z.next_g : z.batches[z.order.front() % kMaxStreamBatches].g0;
+    z.cv_done.notify_all();
+  };
+  try {
+    for (;;) {
+      bool run = false;
+      {
+        std::unique_lock<std::mutex> lk(z.mu);
+        z.cv_work.wait(lk, [&] { return z.closing || z.decoding > 0 || z.copying > 0 || polled < step; });
+        if (z.closing && z.decoding == 0 && z.copying == 0 && polled >= step) break;
+        run = z.decoding > 0;
+      }
+      if (run) {
+        const int slot = static_cast<int>(step % kRing);
+        a.poll_slot = slot;
+        run_step(a, st, z.want_post);
+        CUDA_OK(cudaEventRecord(ring_ev[slot], st));
+        ++step;
+      }
+      // poll the step launched kLag steps ago (or every outstanding one when idle)
+      while (polled < step && (polled + kLag < step || !run)) {
+        const int old = static_cast<int>(polled % kRing);
+        CUDA_OK(cudaEventSynchronize(ring_ev[old]));
+        const volatile int32_t* hp = h_counters + kPollWords * old;
+        ++polled;
+        std::vector<Stream::Batch*> done;
+        {
+          std::lock_guard<std::mutex> lk(z.mu);
+          for (auto& bt : z.batches)
+            if (bt.state == 1 && hp[4 + (&bt - z.batches)] >= bt.target) done.push_back(&bt);
+          for (Stream::Batch* bt : done) {
+            bt->state = 2;
+            --z.decoding;
+            ++z.copying;
+          }
+        }
+        if (!done.empty()) {
+          CUDA_OK(cudaStreamWaitEvent(out_stream, ring_ev[old], 0));
+          for (Stream::Batch* bt : done) copy_out(*bt);
+        }
+      }
+      // batches whose outputs have been copied
+      for (auto& bt : z.batches) {
+        if (bt.state != 2) continue;
+        const cudaError_t q = run ? cudaEventQuery(bt.ev) : cudaEventSynchronize(bt.ev);
+        if (q == cudaErrorNotReady) {
+          (void)cudaGetLastError();
+          continue;
+        }
+        CUDA_OK(q);
+        finish(bt);
+      }
+    }
+  } catch (const std::exception& e) {
+    std::lock_guard<std::mutex> lk(z.mu);
+    z.fatal = std::string("stream worker: ") + e.what();
+    z.cv_done.notify_all();
+  }
+}
+
+bool GpuDecoder::stream_query(int64_t ticket) {
+  if (!stream_) throw ConfigError("stream: not open");
+  Stream& z = *stream_;
+  std::lock_guard<std::mutex> lk(z.mu);
+  if (ticket < 0 || ticket >= z.next_ticket) throw ValidationError("stream: unknown ticket");
+  if (!z.fatal.empty()) throw CudaError(z.fatal);
+  for (const auto& bt : z.batches)
+    if (bt.state != 0 && bt.ticket == ticket) return false;
+  return true;
+}
+
+void GpuDecoder::stream_wait(int64_t ticket) {
+  if (!stream_) throw ConfigError("stream: not open");
+  Stream& z = *stream_;
+  std::unique_lock<std::mutex> lk(z.mu);
+  if (ticket < 0 || ticket >= z.next_ticket) throw ValidationError("stream: unknown ticket");
+  auto live = [&] {
+    for (const auto& bt : z.batches)
+      if (bt.state != 0 && bt.ticket == ticket) return true;
+    return false;
+  };
+  z.cv_done.wait(lk, [&] { return !z.fatal.empty() || !live(); });
+  if (!z.fatal.empty()) throw CudaError(z.fatal);
+  auto it = z.finished.find(ticket);
+  if (it == z.finished.end()) return;  // already collected
+  const std::string err = it->second;
+  z.finished.erase(it);
+  if (!err.empty()) throw ValidationError(err);
+}
+
+void GpuDecoder::stream_close() {
+  if (!stream_) return;
+  std::string fatal;
+  {
+    std::lock_guard<std::mutex> lk(stream_->mu);
+    fatal = stream_->fatal;
+  }
+  stream_release();
+  if (!fatal.empty()) throw CudaError(fatal);
+}
+
+void GpuDecoder::stream_release() noexcept {
+  if (!stream_) return;
+  Stream& z = *stream_;
+  {
+    std::lock_guard<std::mutex> lk(z.mu);
+    z.closing = true;
+  }
+  z.cv_work.notify_all();
+  if (z.worker.joinable()) z.worker.join();
+  cudaSetDevice(device);
+  cudaStreamSynchronize(copy_stream);
+  cudaStreamSynchronize(out_stream);
+  cudaStreamSynchronize(own_stream);
+  for (void* q : {static_cast<void*>(z.r_llr), static_cast<void*>(z.r_syn), static_cast<void*>(z.r_fbatch),
+                  static_cast<void*>(z.r_ferr), static_cast<void*>(z.r_bdone), z.r_bits,
+                  static_cast<void*>(z.r_iters), static_cast<void*>(z.r_reasons), static_cast<void*>(z.r_post),
+                  static_cast<void*>(z.r_q)})
+    if (q) cudaFree(q);
+  if (z.h_fbatch) cudaFreeHost(z.h_fbatch);
+  if (z.h_avail) cudaFreeHost(z.h_avail);
+  if (z.h_ferr) cudaFreeHost(z.h_ferr);
+  for (auto& bt : z.batches)
+    if (bt.ev) cudaEventDestroy(bt.ev);
+  // the decoder returns to batch mode: counters and slot state are reset by
+  // the next decode's init kernel
+  stream_.reset();
+}
+
 // ------------------------------------------------------------ wrappers --
 GpuDecoder* gpu_decoder_create(const Code& code, int device, int max_slots) {
   return new GpuDecoder(code, device, max_slots);
 }
 void gpu_decoder_destroy(GpuDecoder* dec) { delete dec; }
 int gpu_decoder_slots(const GpuDecoder* dec) { return dec->S; }
+int gpu_decoder_device(const GpuDecoder* dec) { return dec->device; }
 int64_t gpu_decoder_device_bytes(const GpuDecoder* dec) { return dec->dev_bytes; }
 void gpu_decode_batch(GpuDecoder* dec, const DecodeParams& p, const DecodeBuffers& b, void* stream) {
   dec->decode(p, b, static_cast<cudaStream_t>(stream));
@@ -3005,6 +3535,16 @@ void gpu_sample_frames_device(GpuDecoder* dec, double snr, double beta_lo, doubl
 void gpu_stage_inputs(GpuDecoder* dec, int32_t batch, const float* llr_host, const uint32_t* syn_host) {
   dec->stage_inputs(batch, llr_host, syn_host);
 }
+void gpu_stream_open(GpuDecoder* dec, const DecodeParams& p, bool packed, bool want_bits, bool want_post,
+                     bool want_q, int32_t ring_frames) {
+  dec->stream_open(p, packed, want_bits, want_post, want_q, ring_frames);
+}
+int64_t gpu_stream_submit(GpuDecoder* dec, int32_t n, const float* llr, const uint32_t* syn, const StreamOutputs& o) {
+  return dec->stream_submit(n, llr, syn, o);
+}
+bool gpu_stream_query(GpuDecoder* dec, int64_t ticket) { return dec->stream_query(ticket); }
+void gpu_stream_wait(GpuDecoder* dec, int64_t ticket) { dec->stream_wait(ticket); }
+void gpu_stream_close(GpuDecoder* dec) { dec->stream_close(); }
 void gpu_set_profiling(GpuDecoder* dec, bool enable) { dec->profiling = enable; }
 void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches, double* frame_iterations) {
   if (kernel < 0 || kernel >= kNumKernels) throw ValidationError("profile: kernel id out of range");

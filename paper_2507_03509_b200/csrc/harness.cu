@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "decoder.hpp"
+#include "devguard.hpp"
 #include "harness.hpp"
 
 namespace bpdec {
@@ -86,6 +87,10 @@ TrialStats run_trials(GpuDecoder* dec, int32_t n_vars, int32_t n_checks, double 
   for (int32_t v : punctured) {
     if (v < 0 || v >= n_vars) throw ValidationError("run_trials: punctured index out of range");
   }
+  // buffers and helper kernels on the decoder's device (the caller's current
+  // device is restored on exit)
+  DeviceGuard dg(gpu_decoder_device(dec));
+  HCUDA_OK(dg.status());
   const int32_t nw = (n_vars + 31) / 32;
   const size_t B = static_cast<size_t>(block);
   DevBuf<float> d_llr(B * n_vars);

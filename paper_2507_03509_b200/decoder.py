@@ -42,7 +42,7 @@ import numpy as np
 from . import _lib
 
 __all__ = [
-    "ConfigError", "IoError", "ValidationError", "BpdecCudaError", "BpdecOomError",
+    "ConfigError", "IoError", "ValidationError", "BpdecCudaError", "BpdecOomError", "MultiDecoder",
     "ParityCheckMatrix", "ActiveVarSet", "active_var_set", "load_alist", "save_alist",
     "lift_protograph", "generate_met", "DecodeConfig", "StopReason", "DecodeOutcome",
     "BatchResult", "BpDecoder", "BatchDecoder", "decode", "syndrome_check", "vnr_statistic",
@@ -282,6 +282,8 @@ class BatchResult:
     bits: Optional[np.ndarray] = None
     posteriors: Optional[np.ndarray] = None
     q_trace: Optional[np.ndarray] = None
+    syndrome_trace: Optional[np.ndarray] = None
+    posterior_trace: Optional[np.ndarray] = None
 
     def outcome(self, f: int) -> DecodeOutcome:
         k = int(self.iterations[f])
@@ -330,24 +332,26 @@ class BatchDecoder:
 
     def decode_batch(self, llr, cfg: DecodeConfig, syndrome=None, *, want_bits: bool = True,
                      packed: bool = False, want_posteriors: bool = False, want_q_trace: bool = False,
+                     want_syndrome_trace: bool = False, want_posterior_trace: bool = False,
                      stream: int = 0, out=None) -> BatchResult:
-        """Decode ``llr`` [B, N] (float32 numpy or CUDA tensor) against
-        ``syndrome`` [B, ceil(M/32)] u32 (None = all-zero).  Outputs are numpy
-        arrays unless ``out`` (dict of preallocated buffers) is given."""
+        """Decode ``llr`` [B, N] (float32 numpy array or torch tensor, host or
+        on this decoder's device; 1-D = one frame) against ``syndrome``
+        [B, ceil(M/32)] 32-bit words (None = all-zero).  Outputs are numpy
+        arrays unless ``out`` (dict of preallocated buffers, validated) is
+        given.  want_syndrome_trace / want_posterior_trace add the observer
+        traces of bpdec_decode_batch_traced."""
         n = self.code.n_vars
-        if hasattr(llr, "data_ptr"):
-            batch = int(llr.shape[0])
-            if llr.shape[-1] != n:
-                raise ValidationError(f"decode: LLR length {llr.shape[-1]} does not match n_vars={n}")
-        else:
-            llr = np.ascontiguousarray(llr, dtype=np.float32)
-            if llr.ndim == 1:
-                llr = llr[None, :]
-            if llr.shape[1] != n:
-                raise ValidationError(f"decode: LLR length {llr.shape[1]} does not match n_vars={n}")
-            batch = llr.shape[0]
-        if syndrome is not None and not hasattr(syndrome, "data_ptr"):
-            syndrome = np.ascontiguousarray(syndrome, dtype=np.uint32).reshape(batch, -1)
+        mw = (self.code.n_checks + 31) // 32
+        llr = self._check_input(llr, "llr", n, (np.float32,), ("float32",))
+        batch = int(llr.shape[0])
+        if syndrome is not None:
+            if not hasattr(syndrome, "data_ptr"):
+                syndrome = np.asarray(syndrome)
+                if syndrome.dtype not in (np.uint32, np.int32):
+                    raise ValidationError(f"decode: syndrome must be packed 32-bit words, got {syndrome.dtype}")
+                syndrome = np.ascontiguousarray(syndrome.view(np.uint32) if syndrome.dtype == np.int32 else syndrome)
+            syndrome = self._check_input(syndrome, "syndrome", mw, (np.uint32, np.int32),
+                                         ("int32", "uint32"), batch=batch)
         if out is None:
             out = {}
             out["iterations"] = np.zeros(batch, dtype=np.int32)
@@ -359,14 +363,90 @@ class BatchDecoder:
                 out["posteriors"] = np.zeros((batch, n), dtype=np.float32)
             if want_q_trace:
                 out["q_trace"] = np.zeros((batch, cfg.d_max), dtype=np.float64)
+        else:
+            out = dict(out)
+        if want_syndrome_trace and out.get("syndrome_trace") is None:
+            out["syndrome_trace"] = np.zeros((batch, cfg.d_max), dtype=np.uint8)
+        if want_posterior_trace and out.get("posterior_trace") is None:
+            out["posterior_trace"] = np.zeros((batch, cfg.d_max, n), dtype=np.float32)
+        self._check_outputs(out, batch, n, cfg.d_max, packed)
         c = cfg.c_struct()
         flags = 1 if packed else 0
-        _check(self._lib.bpdec_decode_batch(
-            self._h, batch, _ptr(llr), _ptr(syndrome), C.byref(c), flags, _ptr(out.get("bits")),
-            _ptr(out["iterations"]), _ptr(out["reasons"]), _ptr(out.get("posteriors")),
-            _ptr(out.get("q_trace")), C.c_void_p(stream) if stream else None))
+        st = C.c_void_p(stream) if stream else None
+        if out.get("syndrome_trace") is not None or out.get("posterior_trace") is not None:
+            _check(self._lib.bpdec_decode_batch_traced(
+                self._h, batch, _ptr(llr), _ptr(syndrome), C.byref(c), flags, _ptr(out.get("bits")),
+                _ptr(out["iterations"]), _ptr(out["reasons"]), _ptr(out.get("posteriors")),
+                _ptr(out.get("q_trace")), _ptr(out.get("syndrome_trace")), _ptr(out.get("posterior_trace")), st))
+        else:
+            _check(self._lib.bpdec_decode_batch(
+                self._h, batch, _ptr(llr), _ptr(syndrome), C.byref(c), flags, _ptr(out.get("bits")),
+                _ptr(out["iterations"]), _ptr(out["reasons"]), _ptr(out.get("posteriors")),
+                _ptr(out.get("q_trace")), st))
         return BatchResult(out["iterations"], out["reasons"], out.get("bits"), out.get("posteriors"),
-                           out.get("q_trace"))
+                           out.get("q_trace"), out.get("syndrome_trace"), out.get("posterior_trace"))
+
+    def _check_input(self, a, name, width, np_dtypes, torch_dtypes, batch=None):
+        """Shape [B, width] (1-D = one row), dtype, contiguity and device of a
+        decode input; returns the (possibly reshaped) buffer."""
+        if hasattr(a, "data_ptr"):  # torch tensor
+            if str(a.dtype).replace("torch.", "") not in torch_dtypes:
+                raise ValidationError(f"decode: {name} tensor must be {'/'.join(torch_dtypes)}, got {a.dtype}")
+            if a.dim() == 1:
+                a = a.unsqueeze(0)
+            if a.dim() != 2:
+                raise ValidationError(f"decode: {name} must be 1-D or 2-D, got shape {tuple(a.shape)}")
+            if not a.is_contiguous():
+                raise ValidationError(f"decode: {name} tensor must be contiguous")
+            if a.is_cuda and a.device.index != self.device:
+                raise ValidationError(f"decode: {name} is on cuda:{a.device.index}, the decoder on cuda:{self.device}")
+        elif isinstance(a, np.ndarray):
+            if a.dtype not in np_dtypes:
+                a = np.ascontiguousarray(a, dtype=np_dtypes[0])
+            a = np.ascontiguousarray(a)
+            if a.ndim == 1:
+                a = a[None, :]
+            if a.ndim != 2:
+                raise ValidationError(f"decode: {name} must be 1-D or 2-D, got shape {a.shape}")
+        else:
+            a = np.ascontiguousarray(np.asarray(a, dtype=np_dtypes[0]))
+            if a.ndim == 1:
+                a = a[None, :]
+        if int(a.shape[1]) != width:
+            what = "does not match n_vars" if name == "llr" else "words per frame, expected"
+            raise ValidationError(f"decode: {name} length {int(a.shape[1])} {what}={width}" if name == "llr" else
+                                  f"decode: {name} has {int(a.shape[1])} {what} ceil(M/32)={width}")
+        if batch is not None and int(a.shape[0]) != batch:
+            raise ValidationError(f"decode: {name} has {int(a.shape[0])} frames, llr has {batch}")
+        return a
+
+    def _check_outputs(self, out, batch, n, d_max, packed):
+        """dtype / element size / shape of the output buffers (numpy or torch)."""
+        nw = (n + 31) // 32
+        want = {"iterations": ((batch,), 4), "reasons": ((batch,), 1),
+                "bits": (((batch, nw), 4) if packed else ((batch, n), 1)),
+                "posteriors": ((batch, n), 4), "q_trace": ((batch, d_max), 8),
+                "syndrome_trace": ((batch, d_max), 1), "posterior_trace": ((batch, d_max, n), 4)}
+        for k in ("iterations", "reasons"):
+            if out.get(k) is None:
+                raise ValidationError(f"decode: output '{k}' is required")
+        for k, buf in out.items():
+            if buf is None:
+                continue
+            if k not in want:
+                raise ValidationError(f"decode: unknown output '{k}'")
+            shape, size = want[k]
+            if hasattr(buf, "data_ptr"):
+                got_shape, got_size, contig = tuple(buf.shape), buf.element_size(), buf.is_contiguous()
+                if buf.is_cuda and buf.device.index != self.device:
+                    raise ValidationError(f"decode: output '{k}' is on cuda:{buf.device.index}")
+                fl = k in ("posteriors", "posterior_trace") and not buf.is_floating_point()
+            else:
+                got_shape, got_size, contig = tuple(buf.shape), buf.dtype.itemsize, buf.flags["C_CONTIGUOUS"]
+                fl = k in ("posteriors", "posterior_trace") and buf.dtype.kind != "f"
+            if got_shape != shape or got_size != size or not contig or fl:
+                raise ValidationError(f"decode: output '{k}' must be a contiguous {shape} buffer of "
+                                      f"{size}-byte elements, got {got_shape} x {got_size} B")
 
     def stage_inputs(self, llr, syndrome=None):
         """Starts the H2D copy of a host batch (pinned torch tensors for full
@@ -395,6 +475,67 @@ class BatchDecoder:
             self._h, float(snr), seed, first_frame, n_frames, int(all_zero), _ptr(llr_dev), _ptr(syndrome_dev),
             _ptr(x_packed_dev), st))
 
+    # ------------------------------------------------------- stream mode --
+    def stream_open(self, cfg: DecodeConfig, *, packed: bool = False, want_bits: bool = True,
+                    want_posteriors: bool = False, want_q_trace: bool = False, ring_frames: int = 0):
+        """Opens stream mode (bpdec_stream_open): batches submitted back to
+        back decode as one continuous frame stream through the slots."""
+        self._stream_cfg = (cfg, packed, want_bits, want_posteriors, want_q_trace)
+        c = cfg.c_struct()
+        _check(self._lib.bpdec_stream_open(self._h, C.byref(c), 1 if packed else 0, int(ring_frames),
+                                           int(want_bits), int(want_posteriors), int(want_q_trace)))
+        self._stream_keep = {}
+
+    def stream_submit(self, llr, syndrome=None, out=None) -> int:
+        """Submits a batch; returns its ticket.  ``out`` (dict of buffers:
+        iterations, reasons, bits, posteriors, q_trace — host arrays/tensors,
+        pinned for overlap, or device tensors) receives the outputs when the
+        batch completes (stream_wait).  Inputs must stay untouched until then."""
+        cfg, packed, want_bits, want_post, want_q = self._stream_cfg
+        n = self.code.n_vars
+        mw = (self.code.n_checks + 31) // 32
+        llr = self._check_input(llr, "llr", n, (np.float32,), ("float32",))
+        batch = int(llr.shape[0])
+        if syndrome is not None:
+            syndrome = self._check_input(syndrome, "syndrome", mw, (np.uint32, np.int32), ("int32", "uint32"),
+                                         batch=batch)
+        if out is None:
+            out = {"iterations": np.zeros(batch, dtype=np.int32), "reasons": np.zeros(batch, dtype=np.uint8)}
+            if want_bits:
+                out["bits"] = (np.zeros((batch, (n + 31) // 32), dtype=np.uint32) if packed
+                               else np.zeros((batch, n), dtype=np.uint8))
+            if want_post:
+                out["posteriors"] = np.zeros((batch, n), dtype=np.float32)
+            if want_q:
+                out["q_trace"] = np.zeros((batch, cfg.d_max), dtype=np.float64)
+        self._check_outputs(out, batch, n, cfg.d_max, packed)
+        t = C.c_int64()
+        _check(self._lib.bpdec_stream_submit(
+            self._h, batch, _ptr(llr), _ptr(syndrome), _ptr(out.get("bits")), _ptr(out["iterations"]),
+            _ptr(out["reasons"]), _ptr(out.get("posteriors")), _ptr(out.get("q_trace")), C.byref(t)))
+        self._stream_keep[t.value] = (llr, syndrome, out)  # alive until waited for
+        return t.value
+
+    def stream_wait(self, ticket: int) -> BatchResult:
+        try:
+            _check(self._lib.bpdec_stream_wait(self._h, int(ticket)))
+        finally:
+            keep = self._stream_keep.pop(int(ticket), None)
+        out = keep[2] if keep else {}
+        return BatchResult(out.get("iterations"), out.get("reasons"), out.get("bits"), out.get("posteriors"),
+                           out.get("q_trace"))
+
+    def stream_query(self, ticket: int) -> bool:
+        d = C.c_int32()
+        _check(self._lib.bpdec_stream_query(self._h, int(ticket), C.byref(d)))
+        return bool(d.value)
+
+    def stream_close(self):
+        try:
+            _check(self._lib.bpdec_stream_close(self._h))
+        finally:
+            self._stream_keep = {}
+
     # profiling (CUDA events on the launching stream)
     KERNELS = ("check", "variable", "decide", "turnover", "compact")
     _KERNEL_IDS = {"check": 0, "variable": 1, "decide": 2, "turnover": 4, "compact": 5}
@@ -421,14 +562,95 @@ class BatchDecoder:
         return n.value
 
 
+class MultiDecoder:
+    """Frame-sharded decoding over several GPUs of one host
+    (bpdec_multi_*): one decoder per entry of ``devices`` (a
+    device may repeat), a host thread each, frames dealt from a shared chunk
+    queue, outputs gathered into the caller's buffers at their frame index."""
+
+    def __init__(self, code: ParityCheckMatrix, devices: Sequence[int], slots_per_decoder: int = 64):
+        self._lib = _lib.load()
+        self.code = code
+        dv = np.ascontiguousarray(list(devices), dtype=np.int32)
+        h = C.c_void_p()
+        _check(self._lib.bpdec_multi_create(code.handle, _ptr(dv, _lib.c_i32p), int(dv.size), int(slots_per_decoder),
+                                            C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        self.last_frames_per_decoder = None
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.bpdec_multi_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def decode_batch(self, llr, cfg: DecodeConfig, syndrome=None, *, want_bits: bool = True, packed: bool = False,
+                     want_posteriors: bool = False, want_q_trace: bool = False, chunk_frames: int = 0,
+                     out=None) -> BatchResult:
+        n = self.code.n_vars
+        mw = (self.code.n_checks + 31) // 32
+        llr = np.ascontiguousarray(llr, dtype=np.float32) if not hasattr(llr, "data_ptr") else llr
+        if llr.ndim == 1:
+            llr = llr[None, :]
+        if llr.shape[1] != n:
+            raise ValidationError(f"decode: LLR length {llr.shape[1]} does not match n_vars={n}")
+        batch = int(llr.shape[0])
+        if syndrome is not None and not hasattr(syndrome, "data_ptr"):
+            syndrome = np.ascontiguousarray(syndrome).view(np.uint32).reshape(batch, -1)
+            if syndrome.shape[1] != mw:
+                raise ValidationError(f"decode: syndrome has {syndrome.shape[1]} words per frame, expected {mw}")
+        if out is None:
+            out = {"iterations": np.zeros(batch, dtype=np.int32), "reasons": np.zeros(batch, dtype=np.uint8)}
+            if want_bits:
+                out["bits"] = (np.zeros((batch, (n + 31) // 32), dtype=np.uint32) if packed
+                               else np.zeros((batch, n), dtype=np.uint8))
+            if want_posteriors:
+                out["posteriors"] = np.zeros((batch, n), dtype=np.float32)
+            if want_q_trace:
+                out["q_trace"] = np.zeros((batch, cfg.d_max), dtype=np.float64)
+        taken = np.zeros(len(self.devices), dtype=np.int64)
+        c = cfg.c_struct()
+        _check(self._lib.bpdec_multi_decode_batch(
+            self._h, batch, _ptr(llr), _ptr(syndrome), C.byref(c), 1 if packed else 0, _ptr(out.get("bits")),
+            _ptr(out["iterations"]), _ptr(out["reasons"]), _ptr(out.get("posteriors")), _ptr(out.get("q_trace")),
+            int(chunk_frames), _ptr(taken, _lib.c_i64p)))
+        self.last_frames_per_decoder = taken
+        return BatchResult(out["iterations"], out["reasons"], out.get("bits"), out.get("posteriors"),
+                           out.get("q_trace"))
+
+
 class BpDecoder:
     """Single-frame shim with the reference signature (decoder.hpp:57-65):
-    ``BpDecoder(code).decode(llr_in, active, cfg)`` -> DecodeOutcome.  LLRs are
-    rounded to float32 (the decoder's input type)."""
+    ``BpDecoder(code).decode(llr_in, active, cfg, observer)`` -> DecodeOutcome.
+    LLRs are rounded to float32 (the decoder's input type).
+
+    ``active`` must be ``active_var_set(code)`` (or None): the device q
+    statistic is built over the degree>=2 variables; another set raises
+    ValidationError instead of being silently ignored.  ``observer(iteration,
+    posteriors, syndrome_ok, q)`` is replayed after the decode from the
+    per-iteration traces (bpdec_decode_batch_traced) with the same arguments
+    the reference passes (decoder.cpp:107-112): syndrome_ok is computed every
+    iteration, PCE on or off, and posteriors are that iteration's (float32
+    values as float64)."""
 
     def __init__(self, code: ParityCheckMatrix, device: int = 0):
         self.code = code
         self._dec = BatchDecoder(code, device=device, max_slots=32)
+        self._active = None
+
+    def _check_active(self, active: Optional[ActiveVarSet]):
+        if active is None:
+            return
+        if self._active is None:
+            self._active = active_var_set(self.code).members
+        m = np.asarray(active.members, dtype=np.int64)
+        if m.shape != self._active.shape or not np.array_equal(m, self._active):
+            raise ValidationError("decode: only active_var_set(code) (the degree>=2 variables) is supported as the "
+                                  "VNR active set")
 
     def decode(self, llr_in, active: Optional[ActiveVarSet] = None, cfg: Optional[DecodeConfig] = None,
                syndrome=None, observer=None) -> DecodeOutcome:
@@ -438,13 +660,22 @@ class BpDecoder:
             raise ValidationError(f"decode: LLR length {llr.size} does not match n_vars={self.code.n_vars}")
         if not np.all(np.isfinite(llr)):
             raise ValidationError("decode: non-finite input LLR")
-        r = self._dec.decode_batch(llr.astype(np.float32)[None, :], cfg,
-                                   None if syndrome is None else np.asarray(syndrome, dtype=np.uint32)[None, :],
-                                   want_posteriors=True, want_q_trace=True)
+        self._check_active(active)
+        l32 = llr.astype(np.float32)[None, :]
+        syn = None if syndrome is None else np.asarray(syndrome, dtype=np.uint32)[None, :]
+        r = self._dec.decode_batch(l32, cfg, syn, want_posteriors=True, want_q_trace=True,
+                                   want_syndrome_trace=observer is not None)
         out = r.outcome(0)
-        if observer is not None:  # IterationObserver emulation from q_trace (decoder.hpp:53-55)
-            for k in range(out.iterations):
-                observer(k + 1, None, None, float(out.q_trace[k]))
+        if observer is not None:
+            k = out.iterations
+            # per-iteration posteriors: the decode is deterministic per frame,
+            # so a second run with d_max = k traces exactly the iterations the
+            # first one ran (bounded trace buffer: k x N floats)
+            tcfg = DecodeConfig(d_max=k, use_pce=False, use_vnr=False, msg_clamp=cfg.msg_clamp, q_mode=cfg.q_mode)
+            t = self._dec.decode_batch(l32, tcfg, syn, want_bits=False, want_posterior_trace=True)
+            for it in range(k):
+                observer(it + 1, t.posterior_trace[0, it].astype(np.float64), bool(r.syndrome_trace[0, it] == 1),
+                         float(out.q_trace[it]))
         return out
 
 

@@ -1,0 +1,240 @@
+"""GPU tests of the host API around the decode loop: the stream mode
+(bpdec_stream_*), the multi-decoder (bpdec_multi_*), the observer traces
+(bpdec_decode_batch_traced vs the reference's IterationObserver), eager host
+output copies, and input / output validation."""
+import os
+
+import numpy as np
+import pytest
+
+from _parity import ref_ties
+
+pytestmark = pytest.mark.gpu
+
+
+def _refcode(ref, code):
+    ptr, var = code.csr()
+    return ref.code_from_csr(code.n_vars, code.n_checks, ptr, var)
+
+
+def _frames(P, code, beta, n, seed=77, first=0):
+    snr = P.snr_for_beta(beta, code.rate())
+    return P.sample_frames(code, snr, seed, first, n)
+
+
+def _same(a, b, lo=0, hi=None):
+    hi = len(a.iterations) if hi is None else hi
+    assert np.array_equal(a.iterations[lo:hi], b.iterations)
+    assert np.array_equal(a.reasons[lo:hi], b.reasons)
+    if a.bits is not None and b.bits is not None:
+        assert np.array_equal(a.bits[lo:hi], b.bits)
+    if a.posteriors is not None and b.posteriors is not None:
+        assert np.array_equal(a.posteriors[lo:hi], b.posteriors)
+    if a.q_trace is not None and b.q_trace is not None:
+        assert np.array_equal(a.q_trace[lo:hi], b.q_trace, equal_nan=True)
+
+
+# ------------------------------------------------------------ stream mode --
+def test_stream_batches_equal_blocking_decode(P, cfg1_code):
+    """Batches of assorted sizes submitted back to back through a small ring
+    (wrap-around, ring-full back-pressure, more batches than fit at once):
+    every batch's outputs equal a blocking decode of the same frames."""
+    import torch
+    code = cfg1_code
+    llr, x, s = _frames(P, code, 0.95, 400)
+    cfg = P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    dec = P.BatchDecoder(code, max_slots=64)
+    whole = dec.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True)
+    sizes = [1, 7, 32, 45, 64, 3, 90, 2, 50, 40, 66]
+    assert sum(sizes) == 400
+    hl = torch.from_numpy(llr).pin_memory()
+    hs = torch.from_numpy(s.view(np.int32)).pin_memory()
+    dec.stream_open(cfg, want_posteriors=True, want_q_trace=True, ring_frames=128)
+    try:
+        tickets, lo = [], 0
+        for n in sizes:
+            tickets.append((lo, n, dec.stream_submit(hl[lo:lo + n], hs[lo:lo + n])))
+            lo += n
+        for lo, n, t in reversed(tickets):  # waited in any order
+            _same(whole, dec.stream_wait(t), lo, lo + n)
+        assert dec.stream_query(tickets[0][2])
+        # the decoder refuses batch calls while the stream is open
+        with pytest.raises(P.ConfigError):
+            dec.decode_batch(llr[:4], cfg, syndrome=s[:4])
+    finally:
+        dec.stream_close()
+    # back in batch mode afterwards
+    _same(whole, dec.decode_batch(llr[:20], cfg, syndrome=s[:20], want_posteriors=True, want_q_trace=True), 0, 20)
+
+
+def test_stream_device_inputs_packed_and_error_isolation(P, cfg1_code):
+    """Device-resident inputs / outputs, packed bits, all-zero syndrome
+    (None); a batch with a non-finite LLR fails alone (ValidationError on its
+    wait), the batches around it are unaffected."""
+    import torch
+    code = cfg1_code
+    llr, x, s = _frames(P, code, 0.9, 96, seed=5)
+    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float32)
+    cfg = P.DecodeConfig(d_max=150, use_pce=True, use_vnr=True)
+    dec = P.BatchDecoder(code, max_slots=32)
+    want = dec.decode_batch(leq, cfg, packed=True)
+    bad = leq[32:64].copy()
+    bad[5, 17] = np.nan
+    dl = torch.from_numpy(leq).cuda()
+    db = torch.from_numpy(bad).cuda()
+    nw = (code.n_vars + 31) // 32
+    outs = [{"iterations": torch.zeros(32, dtype=torch.int32, device="cuda"),
+             "reasons": torch.zeros(32, dtype=torch.uint8, device="cuda"),
+             "bits": torch.zeros((32, nw), dtype=torch.int32, device="cuda")} for _ in range(3)]
+    dec.stream_open(cfg, packed=True, ring_frames=64)
+    try:
+        t0 = dec.stream_submit(dl[:32], None, outs[0])
+        t1 = dec.stream_submit(db, None, outs[1])
+        t2 = dec.stream_submit(dl[64:], None, outs[2])
+        r0 = dec.stream_wait(t0)
+        with pytest.raises(P.ValidationError):
+            dec.stream_wait(t1)
+        r2 = dec.stream_wait(t2)
+    finally:
+        dec.stream_close()
+    for r, lo in ((r0, 0), (r2, 64)):
+        assert np.array_equal(r.iterations.cpu().numpy(), want.iterations[lo:lo + 32])
+        assert np.array_equal(r.bits.cpu().numpy().view(np.uint32), want.bits[lo:lo + 32])
+
+
+# -------------------------------------------------------------- multi-GPU --
+def test_multi_decoder_equals_single(P, cfg1_code):
+    """bpdec_multi: two (and three) decoders on this GPU, dynamic chunks of
+    assorted sizes: per-frame outputs identical to one decoder; every frame
+    taken exactly once; a non-finite LLR fails the call."""
+    code = cfg1_code
+    llr, x, s = _frames(P, code, 0.95, 300, seed=9)
+    cfg = P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    one = P.BatchDecoder(code, max_slots=64).decode_batch(llr, cfg, syndrome=s, want_posteriors=True,
+                                                          want_q_trace=True)
+    for devs, chunk in (([0, 0], 40), ([0, 0, 0], 0), ([0, 0], 7)):
+        m = P.MultiDecoder(code, devs, slots_per_decoder=32)
+        r = m.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True, chunk_frames=chunk)
+        _same(one, r)
+        assert int(m.last_frames_per_decoder.sum()) == 300
+        # a second call reuses the open streams
+        r2 = m.decode_batch(llr[:50], cfg, syndrome=s[:50], want_posteriors=True, want_q_trace=True)
+        _same(one, r2, 0, 50)
+        m.close()
+    m = P.MultiDecoder(code, [0, 0], slots_per_decoder=32)
+    bad = llr[:64].copy()
+    bad[40, 3] = np.inf
+    with pytest.raises(P.ValidationError):
+        m.decode_batch(bad, cfg, syndrome=s[:64], chunk_frames=16)
+    m.close()
+
+
+# --------------------------------------------------------- observer traces --
+@pytest.mark.parametrize("codename", ["cfg1", "lift36"])
+@pytest.mark.parametrize("pce,vnr", [(True, True), (False, False), (False, True)])
+def test_observer_matches_reference(P, ref, cfg1_code, lift36, codename, pce, vnr):
+    """IterationObserver (decoder.hpp:53-55): the (iteration, syndrome_ok, q)
+    call sequence and each iteration's posteriors equal the reference's
+    observer calls (oracle ref_shim decode_observed_post), with syndrome_ok
+    computed every iteration even with PCE off (decoder.cpp:110-112); on
+    non-tie frames; posteriors at the 1e-4 bar, q at 1e-5."""
+    code = cfg1_code if codename == "cfg1" else lift36
+    beta = 0.95 if codename == "cfg1" else 0.8
+    d_max = 60
+    llr, x, s = _frames(P, code, beta, 6, seed=3)
+    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float32)
+    rc = _refcode(ref, code)
+    _, tie = ref_ties(rc, leq, d_max=d_max, use_pce=pce, use_vnr=vnr, threads=8)
+    bp = P.BpDecoder(code)
+    cfg = P.DecodeConfig(d_max=d_max, use_pce=pce, use_vnr=vnr)
+    checked = 0
+    for f in range(len(leq)):
+        if tie[f]:
+            continue
+        calls = []
+        out = bp.decode(leq[f].astype(np.float64), P.active_var_set(code), cfg,
+                        observer=lambda it, post, ok, q: calls.append((it, np.array(post), ok, q)))
+        r = rc.decode_observed_post(leq[f].astype(np.float64), d_max=d_max, use_pce=pce, use_vnr=vnr)
+        assert r["calls"] == len(calls) == out.iterations == r["iterations"]
+        assert [c[0] for c in calls] == list(range(1, r["iterations"] + 1))
+        assert [int(c[2]) for c in calls] == r["syndrome_ok"].tolist()
+        np.testing.assert_allclose([c[3] for c in calls], r["q"], rtol=1e-5, atol=1e-3)
+        for k, c in enumerate(calls):
+            err = np.abs(c[1] - r["posteriors"][k]) / (1e-4 * np.abs(r["posteriors"][k]) + 1e-4)
+            assert err.max() <= 1.0, (f, k, float(err.max()))
+        checked += 1
+    assert checked >= 2, f"only {checked} non-tie frames"
+    # another active set is rejected instead of silently ignored
+    with pytest.raises(P.ValidationError):
+        bp.decode(leq[0].astype(np.float64), P.ActiveVarSet(np.array([0, 1], dtype=np.int32)), cfg)
+
+
+def test_batch_traces_shapes(P, cfg1_code):
+    """bpdec_decode_batch_traced on a batch: syndrome_ok 0/1 up to the stop
+    and 0xff after; posterior trace at the stop iteration equals the
+    posteriors output; NaN after."""
+    llr, x, s = _frames(P, cfg1_code, 0.5, 12, seed=11)
+    dec = P.BatchDecoder(cfg1_code, max_slots=32)
+    cfg = P.DecodeConfig(d_max=30, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    g = dec.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_syndrome_trace=True,
+                         want_posterior_trace=True)
+    plain = dec.decode_batch(llr, cfg, syndrome=s, want_posteriors=True)
+    _same(plain, g)
+    for f in range(12):
+        k = g.iterations[f]
+        assert set(np.unique(g.syndrome_trace[f, :k])) <= {0, 1}
+        assert np.all(g.syndrome_trace[f, k:] == 0xFF)
+        assert (g.syndrome_trace[f, k - 1] == 1) == P.syndrome_check(cfg1_code, g.bits[f], s[f])
+        assert np.array_equal(g.posterior_trace[f, k - 1], g.posteriors[f])
+        assert np.all(np.isnan(g.posterior_trace[f, k:]))
+
+
+# ---------------------------------------------------- eager output copies --
+def test_eager_host_outputs_equal_deferred(P, cfg1_code):
+    """Host outputs copied while the tail decodes (eager) equal the copies
+    made after the decode (BPDEC_NO_EAGER=1), on a VNR batch where frames
+    stop at many different steps and slots are refilled (the
+    snapshot is ordered after the step's extraction)."""
+    llr, x, s = _frames(P, cfg1_code, 0.95, 600, seed=13)
+    cfg = P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    eager = P.BatchDecoder(cfg1_code, max_slots=64)
+    os.environ["BPDEC_NO_EAGER"] = "1"
+    try:
+        deferred = P.BatchDecoder(cfg1_code, max_slots=64)
+    finally:
+        del os.environ["BPDEC_NO_EAGER"]
+    for _ in range(3):
+        a = eager.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True)
+        b = deferred.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True)
+        _same(a, b)
+
+
+# -------------------------------------------------------------- validation --
+def test_decode_input_validation(P, cfg1_code):
+    import torch
+    dec = P.BatchDecoder(cfg1_code, max_slots=32)
+    n, mw = cfg1_code.n_vars, (cfg1_code.n_checks + 31) // 32
+    cfg = P.DecodeConfig(d_max=10)
+    llr, x, s = _frames(P, cfg1_code, 0.95, 4)
+    one = dec.decode_batch(llr[0], cfg)  # 1-D = one frame
+    assert one.iterations.shape == (1,)
+    t1 = torch.from_numpy(llr[0]).cuda()
+    assert dec.decode_batch(t1, cfg).iterations.shape == (1,)  # 1-D tensor = one frame (not N frames)
+    bad = [
+        (lambda: dec.decode_batch(llr[:, :-1], cfg), "length"),
+        (lambda: dec.decode_batch(torch.from_numpy(llr).double().cuda(), cfg), "float32"),
+        (lambda: dec.decode_batch(torch.from_numpy(llr).cuda().t(), cfg), "shape"),
+        (lambda: dec.decode_batch(torch.zeros((4, 2 * n), dtype=torch.float32, device="cuda")[:, :n], cfg),
+         "contiguous"),
+        (lambda: dec.decode_batch(llr, cfg, syndrome=s[:, :-1]), "words"),
+        (lambda: dec.decode_batch(llr, cfg, syndrome=s[:3]), "frames"),
+        (lambda: dec.decode_batch(llr, cfg, syndrome=np.zeros((4, cfg1_code.n_checks), np.uint8)), "32-bit"),
+        (lambda: dec.decode_batch(llr, cfg, out={"iterations": np.zeros(3, np.int32),
+                                                 "reasons": np.zeros(4, np.uint8)}), "iterations"),
+        (lambda: dec.decode_batch(llr, cfg, out={"iterations": np.zeros(4, np.int32), "reasons": np.zeros(4, np.uint8),
+                                                 "bits": np.zeros((4, n - 1), np.uint8)}), "bits"),
+    ]
+    for fn, what in bad:
+        with pytest.raises(P.ValidationError):
+            fn()
+    assert mw > 0

@@ -1,0 +1,186 @@
+"""Parity on the BASELINE.json configurations at full size (N = 2^20 / 2^21),
+where the headline is measured, against the compiled reference (oracle/_ref).
+
+* cfg2 (the bench workload): >= 112 VNR+PCE frames in the reference's own
+  semantics (all-zero-equivalent L*(1-2x), s = 0, raw q), per-frame on every
+  non-tie frame at the strict 1e-4 bar (>= 32 frames compared), the paired
+  mean-iteration difference, and the benched true-syndrome Q_ABS mode's
+  iteration shift against the reference's raw q (SURVEY §8c hazard H3)
+  measured on the same frames.
+* cfg3: a few frames (the BASELINE R = 0.02 construction stops at k = 2).
+* cfg5: VNR statistically over 64 frames of the mixed-beta stream (per-frame
+  VNR at N = 2^21 is decided by q drops below float resolution), D-bar
+  within the paired confidence interval and the |delta iterations|
+  distribution.
+* cfg4: the 512-frame batch streamed through 64 slots equals each frame
+  decoded alone (and the stream API and the multi-decoder API), plus a
+  reference subset.
+
+Reference decodes use every host core (the run_trials pattern)."""
+import os
+
+import numpy as np
+import pytest
+
+from _parity import compare, ref_ties
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 8
+
+
+def _refcode(ref, code):
+    ptr, var = code.csr()
+    return ref.code_from_csr(code.n_vars, code.n_checks, ptr, var)
+
+
+def _frames(P, code, beta, n, first=0):
+    snr = P.snr_for_beta(beta, code.rate())
+    llr, x, s = P.sample_frames(code, snr, P.FRAME_SEED, first, n)
+    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float32)
+    return llr, x, s, leq
+
+
+def _paired(g_it, r_it):
+    d = g_it.astype(np.float64) - r_it.astype(np.float64)
+    se = d.std(ddof=1) / np.sqrt(d.size) if d.size > 1 else 0.0
+    return float(d.mean()), float(se), np.bincount(np.abs(d).astype(int)).tolist()
+
+
+@pytest.fixture(scope="module")
+def cfg2(P):
+    return P.WORKLOADS["cfg2"].make_code()
+
+
+def test_cfg2_vnr_headline_parity(P, ref, cfg2):
+    """The bench configuration (cfg2, beta 0.95, VNR+PCE, D_max 500) in the
+    reference's semantics: every non-tie frame has identical bits,
+    iterations and stop reason and posteriors within 1e-4 (strict: the
+    reference's one-ulp drift never widens the bar)."""
+    F = 112
+    llr, x, s, leq = _frames(P, cfg2, 0.95, F)
+    rc = _refcode(ref, cfg2)
+    r, tie = ref_ties(rc, leq, d_max=500, use_pce=True, use_vnr=True, threads=THREADS)
+    dec = P.BatchDecoder(cfg2, max_slots=64)
+    g = dec.decode_batch(leq, P.DecodeConfig(d_max=500, use_pce=True, use_vnr=True), want_posteriors=True,
+                         want_q_trace=True)
+    summary = compare(g, r, tie, min_nontie_frac=0.0, min_checked=32, strict=True, label="cfg2 vnr (64 slots)")
+    for f in np.nonzero(~tie)[0]:
+        k = g.iterations[f]
+        np.testing.assert_allclose(g.q_trace[f, :k], r["q_trace"][f, :k], rtol=1e-5)
+    mean, se, hist = _paired(g.iterations, r["iterations"])
+    print("cfg2 vnr parity", summary, f"paired mean d_it {mean:+.4f} +- {se:.4f}", "|d_it| histogram", hist)
+    # all frames (ties included): mean iterations within the paired CI
+    assert abs(mean) <= 1.96 * se + 0.05, (mean, se)
+    assert np.max(np.abs(g.iterations - r["iterations"])) <= 3
+
+    # H3: the benched x-free statistic (Q_ABS, true syndrome mode L, s = Hx)
+    # against the reference's raw q on the same frames: measured shift
+    ga = dec.decode_batch(llr, P.DecodeConfig(d_max=500, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS),
+                          syndrome=s)
+    ma, sa, ha = _paired(ga.iterations, r["iterations"])
+    same = float(np.mean(ga.iterations == r["iterations"]))
+    print(f"cfg2 H3 shift: D_bar Q_ABS {ga.iterations.mean():.3f} vs reference raw {r['iterations'].mean():.3f}; "
+          f"paired {ma:+.3f} +- {sa:.3f}; equal stop iteration on {same:.2%} of frames; |d_it| histogram {ha}")
+    assert abs(ma) < 1.0 and same >= 0.5
+    # success => H bits == s (the PCE exits, if any)
+    for f in range(F):
+        if ga.reasons[f] == 0:
+            assert P.syndrome_check(cfg2, ga.bits[f], s[f])
+
+
+def test_cfg2_pce_capped(P, ref, cfg2):
+    """cfg2 PCE (the reference costs ~60 ns per edge-update: capped at
+    D_max = 40 on 4 frames)."""
+    llr, x, s, leq = _frames(P, cfg2, 0.95, 4)
+    rc = _refcode(ref, cfg2)
+    r, tie = ref_ties(rc, leq, d_max=40, use_pce=True, use_vnr=False, threads=THREADS)
+    g = P.BatchDecoder(cfg2, max_slots=32).decode_batch(leq, P.DecodeConfig(d_max=40, use_pce=True, use_vnr=False),
+                                                        want_posteriors=True)
+    print("cfg2 pce", compare(g, r, tie, min_nontie_frac=0.5, strict=True, label="cfg2 pce"))
+
+
+@pytest.mark.parametrize("mode,d_max", [("vnr", 500), ("none", 30)])
+def test_cfg3_vs_reference(P, ref, mode, d_max):
+    code = P.WORKLOADS["cfg3"].make_code()
+    llr, x, s, leq = _frames(P, code, 0.98, 3)
+    pce, vnr = (True, True) if mode == "vnr" else (False, False)
+    rc = _refcode(ref, code)
+    r, tie = ref_ties(rc, leq, d_max=d_max, use_pce=pce, use_vnr=vnr, threads=THREADS)
+    g = P.BatchDecoder(code, max_slots=32).decode_batch(leq, P.DecodeConfig(d_max=d_max, use_pce=pce, use_vnr=vnr),
+                                                        want_posteriors=True)
+    print("cfg3", mode, compare(g, r, tie, min_nontie_frac=0.3, strict=True, label=f"cfg3 {mode}"))
+
+
+def test_cfg5_vnr_statistical(P, ref):
+    """cfg5 (N = 2^21, beta_f ~ U[0.92, 1]): per-frame VNR stops are decided
+    by q drops of ~1e-9 relative (below float32 resolution of the posteriors
+    summed), so the bar is statistical: over 64 frames the paired mean
+    iteration difference is within its 95% CI (+0.1), >= 50% of the frames
+    stop at the same iteration and none is more than 3 iterations apart; the
+    PCE run (capped) is compared per frame."""
+    w = P.WORKLOADS["cfg5"]
+    code = w.make_code()
+    F = 64
+    llr, x, s, snr = P.sample_frames_beta(code, 0.92, 1.0, P.FRAME_SEED, 0, F)
+    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float32)
+    rc = _refcode(ref, code)
+    r = rc.decode_batch(leq.astype(np.float64), d_max=500, use_pce=True, use_vnr=True, threads=THREADS,
+                        want_posteriors=False, want_q_trace=False)
+    dec = P.BatchDecoder(code, max_slots=64)
+    g = dec.decode_batch(leq, P.DecodeConfig(d_max=500, use_pce=True, use_vnr=True))
+    mean, se, hist = _paired(g.iterations, r["iterations"])
+    same = float(np.mean(g.iterations == r["iterations"]))
+    print(f"cfg5 vnr: D_bar gpu {g.iterations.mean():.3f} ref {r['iterations'].mean():.3f}; paired {mean:+.4f} +- "
+          f"{se:.4f}; same stop {same:.2%}; |d_it| histogram {hist}")
+    assert abs(mean) <= 1.96 * se + 0.1
+    assert same >= 0.5
+    assert np.max(np.abs(g.iterations - r["iterations"])) <= 3
+    assert np.all(g.reasons == r["reasons"])
+    # PCE, per frame (capped)
+    sub = leq[:2]
+    rp, tie = ref_ties(rc, sub, d_max=20, use_pce=True, use_vnr=False, threads=THREADS)
+    gp = dec.decode_batch(sub, P.DecodeConfig(d_max=20, use_pce=True, use_vnr=False), want_posteriors=True)
+    print("cfg5 pce", compare(gp, rp, tie, min_nontie_frac=0.5, strict=True, label="cfg5 pce"))
+
+
+def test_cfg4_stream_equals_decode_alone(P, ref, cfg2):
+    """cfg4: 512 frames of the cfg2 code through 64 slots (frames streaming
+    through the slots as others stop) give, per frame, exactly what each
+    64-frame block gives decoded alone, and so do the stream API (8 batches
+    back to back) and the multi-decoder API (two decoders on this GPU); 16
+    frames spread over the batch match the reference (strict bar)."""
+    B = 512
+    llr, x, s, _ = _frames(P, cfg2, 0.95, B)
+    cfg = P.DecodeConfig(d_max=500, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    dec = P.BatchDecoder(cfg2, max_slots=64)
+    whole = dec.decode_batch(llr, cfg, syndrome=s, packed=True)
+    for b0 in range(0, B, 64):
+        alone = dec.decode_batch(llr[b0:b0 + 64], cfg, syndrome=s[b0:b0 + 64], packed=True)
+        assert np.array_equal(alone.iterations, whole.iterations[b0:b0 + 64])
+        assert np.array_equal(alone.reasons, whole.reasons[b0:b0 + 64])
+        assert np.array_equal(alone.bits, whole.bits[b0:b0 + 64])
+    # stream API: 8 batches of 64 submitted back to back
+    dec.stream_open(cfg, packed=True)
+    try:
+        tickets = [dec.stream_submit(llr[b0:b0 + 64], s[b0:b0 + 64]) for b0 in range(0, B, 64)]
+        res = [dec.stream_wait(t) for t in tickets]
+    finally:
+        dec.stream_close()
+    for k, b0 in enumerate(range(0, B, 64)):
+        assert np.array_equal(res[k].iterations, whole.iterations[b0:b0 + 64])
+        assert np.array_equal(res[k].bits, whole.bits[b0:b0 + 64])
+    # multi-decoder API, two decoders sharing this GPU, 48-frame chunks
+    m = P.MultiDecoder(cfg2, [0, 0], slots_per_decoder=64)
+    mr = m.decode_batch(llr, cfg, syndrome=s, packed=True, chunk_frames=48)
+    assert int(m.last_frames_per_decoder.sum()) == B
+    assert np.array_equal(mr.iterations, whole.iterations) and np.array_equal(mr.bits, whole.bits)
+    assert np.array_equal(mr.reasons, whole.reasons)
+    m.close()
+    # reference subset (reference semantics, raw q)
+    idx = np.arange(0, B, 32)
+    leq = (llr[idx] * (1 - 2 * x[idx].astype(np.float32))).astype(np.float32)
+    rc = _refcode(ref, cfg2)
+    r, tie = ref_ties(rc, leq, d_max=500, use_pce=True, use_vnr=True, threads=THREADS)
+    g = dec.decode_batch(leq, P.DecodeConfig(d_max=500, use_pce=True, use_vnr=True), want_posteriors=True)
+    print("cfg4 subset", compare(g, r, tie, min_nontie_frac=0.0, strict=True, label="cfg4 subset"))

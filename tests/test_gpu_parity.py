@@ -487,38 +487,4 @@ def test_narrow_tail_bit_exact(P, cfg1_code, kind):
         for f in list(range(0, 96, 7)) + [int(np.argmax(r.iterations))]:
             _assert_same(_decode_all(one, llr[f:f + 1], s[f:f + 1], cfg), r, slice(f, f + 1))
 
-
-# ------------------------------------------- BASELINE configs at full size --
-@pytest.mark.parametrize("key,frames,beta,modes,min_nontie", [
-    ("cfg2", 4, 0.95, (("vnr", 500), ("pce", 40)), 0.25),
-    ("cfg3", 3, 0.98, (("vnr", 500), ("none", 30)), 0.3),
-    # N = 2^21: q ~ 1.4e7 summed over 419,430 float posteriors; VNR stops on
-    # drops of ~1e-9 relative, below float32 resolution -> mostly ties
-    ("cfg5", 2, 0.96, (("vnr", 500), ("pce", 20)), 0.0),
-])
-def test_baseline_config_full_size_vs_reference(P, ref, key, frames, beta, modes, min_nontie):
-    """BASELINE.json configs 2, 3 and 5 at their full code sizes (N = 2^20 /
-    2^21): a few frames in the reference's semantics (L*(1-2x), s = 0, raw
-    q) against the compiled reference, same bar and tie rule.  PCE runs are
-    capped (the reference costs ~60 ns per edge-update)."""
-    w = P.WORKLOADS[key]
-    code = w.make_code()
-    snr = P.snr_for_beta(beta, code.rate())
-    llr, x, s = P.sample_frames(code, snr, P.FRAME_SEED, 0, frames)
-    leq = (llr * (1 - 2 * x.astype(np.float32))).astype(np.float32)
-    rc = _refcode(ref, code)
-    dec = P.BatchDecoder(code, max_slots=32)
-    for mode, d_max in modes:
-        pce, vnr = ET_MODES[mode]
-        r, tie = ref_ties(rc, leq, d_max=d_max, use_pce=pce, use_vnr=vnr, threads=8)
-        g = dec.decode_batch(leq, P.DecodeConfig(d_max=d_max, use_pce=pce, use_vnr=vnr), want_posteriors=True)
-        print(key, mode, compare(g, r, tie, min_nontie_frac=min_nontie, label=f"{key} {mode}"),
-              "gpu it", g.iterations.tolist(), "ref it", r["iterations"].tolist())
-        # tie frames still stop within a couple of iterations of the reference
-        assert np.all(np.abs(g.iterations - r["iterations"]) <= 3)
-        # size-independent properties on the same frames in true syndrome mode
-        gs = dec.decode_batch(llr, P.DecodeConfig(d_max=d_max, use_pce=pce, use_vnr=vnr, q_mode=P.decoder.Q_ABS),
-                              syndrome=s)
-        for f in range(frames):
-            if gs.reasons[f] == 0:
-                assert P.syndrome_check(code, gs.bits[f], s[f])  # success => H bits == s
+# BASELINE configurations at full size: tests/test_gpu_baseline.py
