@@ -14,12 +14,12 @@ CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -I$(CSRC) -Iinclude -I/usr/local/
 NVFLAGS  := -O3 -std=c++20 $(ARCH) -lineinfo -Xcompiler -fPIC,-Wall -I$(CSRC) -Iinclude \
             -Xptxas -v $(NVFLAGS_EXTRA)
 
-HOST_SRC := $(CSRC)/code.cpp $(CSRC)/c_api.cpp
+HOST_SRC := $(CSRC)/code.cpp $(CSRC)/c_api.cpp $(CSRC)/devmem.cpp
 HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))
 CU_OBJ   := $(OBJDIR)/decoder.o $(OBJDIR)/harness.o
 HDRS     := $(wildcard $(CSRC)/*.hpp $(CSRC)/*.cuh) include/bpdec.h
 
-.PHONY: all lib oracle ref clean
+.PHONY: all lib oracle ref clean guard
 all: lib oracle
 
 lib: $(LIB)
@@ -55,3 +55,28 @@ $(COMPAT_TEST): tests/cpp/compat_test.cpp include/bpdec/etdec_compat.hpp include
 
 compat_test: $(COMPAT_TEST)
 .PHONY: compat_test
+
+# Guard build (bounds-checking stand-in for compute-sanitizer, which this GPU
+# pool does not allow): guard zones + poisoned allocations, verified at the
+# end of every C-ABI call (csrc/devmem.hpp).  Tests run against it with
+# BPDEC_LIB=paper_2507_03509_b200/libbpdec_guard.so (scripts/guard_tests.sh).
+GUARD_LIB := $(PKG)/libbpdec_guard.so
+GOBJ      := build/gobj
+GUARD_HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(GOBJ)/%.o,$(HOST_SRC))
+
+$(GOBJ)/%.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(GOBJ)
+	$(CXX) $(CXXFLAGS) -DBPDEC_GUARD -c $< -o $@
+
+$(GOBJ)/decoder.o: $(CSRC)/decoder.cu $(HDRS)
+	@mkdir -p $(GOBJ)
+	$(NVCC) $(NVFLAGS) -DBPDEC_GUARD -c $< -o $@ 2> $(GOBJ)/ptxas.log || (cat $(GOBJ)/ptxas.log; false)
+
+$(GOBJ)/harness.o: $(CSRC)/harness.cu $(HDRS)
+	@mkdir -p $(GOBJ)
+	$(NVCC) $(NVFLAGS) -DBPDEC_GUARD -c $< -o $@ 2> $(GOBJ)/ptxas_harness.log || (cat $(GOBJ)/ptxas_harness.log; false)
+
+$(GUARD_LIB): $(GUARD_HOST_OBJ) $(GOBJ)/decoder.o $(GOBJ)/harness.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
+
+guard: $(GUARD_LIB)

@@ -227,6 +227,13 @@ int bpdec_stream_submit(bpdec_decoder* dec, int32_t batch, const float* llr, con
 int bpdec_stream_wait(bpdec_decoder* dec, int64_t ticket);
 int bpdec_stream_query(bpdec_decoder* dec, int64_t ticket, int32_t* done);
 int bpdec_stream_close(bpdec_decoder* dec);
+/* Device timer of the stream (for throughput measurement): reset (only
+ * while no batch is in flight) arms it; the first step launched afterwards
+ * records the start on the decoder's stream, every batch's output copy the
+ * end.  device_ms = the time between them, CUDA events (waits for the last
+ * copy). */
+int bpdec_stream_timer_reset(bpdec_decoder* dec);
+int bpdec_stream_device_ms(bpdec_decoder* dec, double* ms);
 
 /* ------------------------------------------------------------ multi-GPU -- */
 /* Frame-sharded decoding over several GPUs of one host (the

@@ -99,6 +99,8 @@ SIGNATURES = [
     ("bpdec_stream_wait", C.c_int, [C.c_void_p, C.c_int64]),
     ("bpdec_stream_query", C.c_int, [C.c_void_p, C.c_int64, c_i32p]),
     ("bpdec_stream_close", C.c_int, [C.c_void_p]),
+    ("bpdec_stream_timer_reset", C.c_int, [C.c_void_p]),
+    ("bpdec_stream_device_ms", C.c_int, [C.c_void_p, c_f64p]),
     ("bpdec_multi_create", C.c_int, [C.c_void_p, c_i32p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     ("bpdec_multi_destroy", None, [C.c_void_p]),
     ("bpdec_multi_count", C.c_int, [C.c_void_p, c_i32p]),

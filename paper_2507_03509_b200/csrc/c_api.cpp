@@ -16,6 +16,7 @@
 
 #include "code.hpp"
 #include "decoder.hpp"
+#include "devmem.hpp"
 #include "harness.hpp"
 #include "rng.hpp"
 
@@ -50,6 +51,13 @@ template <typename F>
 int guarded(F&& f) {
   try {
     f();
+#ifdef BPDEC_GUARD
+    // guard build: every entry point ends with the guard-zone check of all
+    // live device allocations (devmem.hpp)
+    const char* where = nullptr;
+    if (bpdec::dev_verify(&where) != cudaSuccess)
+      throw bpdec::CudaError(std::string("guard build: ") + (where ? where : "device error during verify"));
+#endif
     g_last_error.clear();
     return BPDEC_OK;
   } catch (const bpdec::ConfigError& e) {
@@ -600,6 +608,21 @@ int bpdec_stream_close(bpdec_decoder* dec) {
   return guarded([&] {
     need(dec, "decoder");
     bpdec::gpu_stream_close(dec->impl);
+  });
+}
+
+int bpdec_stream_timer_reset(bpdec_decoder* dec) {
+  return guarded([&] {
+    need(dec, "decoder");
+    bpdec::gpu_stream_timer_reset(dec->impl);
+  });
+}
+
+int bpdec_stream_device_ms(bpdec_decoder* dec, double* ms) {
+  return guarded([&] {
+    need(dec, "decoder");
+    need(ms, "ms");
+    *ms = bpdec::gpu_stream_device_ms(dec->impl);
   });
 }
 

@@ -52,6 +52,7 @@
 
 #include "decoder.hpp"
 #include "devguard.hpp"
+#include "devmem.hpp"
 #include "phi.cuh"
 #include "rng.hpp"
 
@@ -2257,7 +2258,7 @@ template <typename T>
 T* dalloc(size_t count, int64_t* bytes) {
   T* p = nullptr;
   if (count == 0) count = 1;
-  CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+  CUDA_OK(dev_malloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
   *bytes += static_cast<int64_t>(count * sizeof(T));
   return p;
 }
@@ -2298,15 +2299,15 @@ struct Scratch {
   size_t size = 0;
   void* get(size_t n) {
     if (n <= size) return ptr;
-    if (ptr) CUDA_OK(cudaFree(ptr));
+    if (ptr) CUDA_OK(dev_free(ptr));
     ptr = nullptr;
     size = 0;
-    CUDA_OK(cudaMalloc(&ptr, n));
+    CUDA_OK(dev_malloc(&ptr, n));
     size = n;
     return ptr;
   }
   ~Scratch() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) dev_free(ptr);
   }
 };
 
@@ -2328,6 +2329,8 @@ class GpuDecoder {
   bool stream_query(int64_t ticket);
   void stream_wait(int64_t ticket);
   void stream_close();
+  void stream_timer_reset();
+  double stream_device_ms();
 
   int S = 0;
   int G = 0;
@@ -2352,6 +2355,7 @@ class GpuDecoder {
   void launch(int kid, cudaStream_t st, F&& f);
   void run_step(const Args& a, cudaStream_t st, bool want_post);
   void launch_turnover(const Args& a, cudaStream_t st, bool want_post);
+  cudaError_t harvest_profile(const unsigned long long* d_frame_iters) noexcept;
   void init(const Code& code, int max_slots);
   void release() noexcept;
 
@@ -2703,8 +2707,8 @@ GpuDecoder::~GpuDecoder() {
 
 void GpuDecoder::release() noexcept {
   cudaSetDevice(device);
-  for (void* p : owned) cudaFree(p);
-  if (base.d1post) cudaFree(base.d1post);
+  for (void* p : owned) dev_free(p);
+  if (base.d1post) dev_free(base.d1post);
   for (auto& e : ring_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : prof_ev) cudaEventDestroy(e);
@@ -2735,9 +2739,10 @@ void GpuDecoder::release() noexcept {
 template <typename F>
 void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
   // events come from a pool reused across decodes (creation is not free);
-  // no per-launch events in stream mode (its step loop has no end)
+  // in stream mode the worker thread records them and stream_release
+  // harvests them once the stream is closed
   const size_t k = prof_kid.size();
-  const bool profiling = this->profiling && !stream_;
+  const bool profiling = this->profiling;
   if (profiling) {
     while (prof_ev.size() < 2 * (k + 1)) {
       cudaEvent_t e;
@@ -2753,6 +2758,24 @@ void GpuDecoder::launch(int kid, cudaStream_t st, F&& f) {
     CUDA_OK(cudaEventRecord(prof_ev[2 * k + 1], st));
     prof_kid.push_back(kid);
   }
+}
+
+// per-launch event times (and the frame-iterations counter) of the launches
+// recorded since the last harvest; the launching stream is idle
+cudaError_t GpuDecoder::harvest_profile(const unsigned long long* d_frame_iters) noexcept {
+  unsigned long long fi = 0;
+  cudaError_t e = cudaMemcpy(&fi, d_frame_iters, sizeof(fi), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  prof_frame_iters += static_cast<double>(fi);
+  for (size_t k = 0; k < prof_kid.size(); ++k) {
+    float ms = 0.0f;
+    e = cudaEventElapsedTime(&ms, prof_ev[2 * k], prof_ev[2 * k + 1]);
+    if (e != cudaSuccess) break;
+    prof_ms[prof_kid[k]] += ms;
+    prof_launches[prof_kid[k]] += 1;
+  }
+  prof_kid.clear();
+  return e;
 }
 
 void GpuDecoder::launch_turnover(const Args& a, cudaStream_t st, bool want_post) {
@@ -3043,18 +3066,7 @@ void GpuDecoder::decode(const DecodeParams& p, const DecodeBuffers& b, cudaStrea
     if (ctr[2] != 0) throw ValidationError("decode: non-finite input LLR");
     throw CudaError("decode: internal error, frames did not terminate");
   }
-  if (profiling) {
-    unsigned long long fi = 0;
-    CUDA_OK(cudaMemcpy(&fi, a.frame_iters, sizeof(fi), cudaMemcpyDeviceToHost));
-    prof_frame_iters += static_cast<double>(fi);
-    for (size_t k = 0; k < prof_kid.size(); ++k) {
-      float ms = 0.0f;
-      CUDA_OK(cudaEventElapsedTime(&ms, prof_ev[2 * k], prof_ev[2 * k + 1]));
-      prof_ms[prof_kid[k]] += ms;
-      prof_launches[prof_kid[k]] += 1;
-    }
-    prof_kid.clear();
-  }
+  if (profiling) CUDA_OK(harvest_profile(a.frame_iters));
   // copy staged outputs back (eager: only the rows not copied during the decode)
   if (eager) {
     if (snap_pending) {
@@ -3186,6 +3198,10 @@ struct GpuDecoder::Stream {
   int64_t next_ticket = 0, next_g = 0, free_g = 0;
   int64_t decoding = 0;         // batches in state 1
   int64_t copying = 0;          // batches in state 2
+  // device timer (bpdec_stream_device_ms): t_first before the first step
+  // launched after a reset, t_last after each batch's output copies
+  cudaEvent_t t_first = nullptr, t_last = nullptr;
+  bool timer_armed = true, t_first_set = false, t_last_set = false;
 };
 
 void GpuDecoder::stream_open(const DecodeParams& p, bool packed, bool want_bits, bool want_post, bool want_q,
@@ -3209,7 +3225,7 @@ void GpuDecoder::stream_open(const DecodeParams& p, bool packed, bool want_bits,
   std::vector<void*> got;
   auto alloc = [&](size_t bytes) {
     void* q = nullptr;
-    CUDA_OK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+    CUDA_OK(dev_malloc(&q, std::max<size_t>(bytes, 16)));
     got.push_back(q);
     return q;
   };
@@ -3232,13 +3248,17 @@ void GpuDecoder::stream_open(const DecodeParams& p, bool packed, bool want_bits,
     CUDA_OK(cudaHostAlloc(&z.h_avail, kMaxStreamBatches * sizeof(int32_t), cudaHostAllocDefault));
     CUDA_OK(cudaHostAlloc(&z.h_ferr, C, cudaHostAllocDefault));
     for (auto& bt : z.batches) CUDA_OK(cudaEventCreateWithFlags(&bt.ev, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreate(&z.t_first));
+    CUDA_OK(cudaEventCreate(&z.t_last));
   } catch (...) {
-    for (void* q : got) cudaFree(q);
+    for (void* q : got) dev_free(q);
     if (z.h_fbatch) cudaFreeHost(z.h_fbatch);
     if (z.h_avail) cudaFreeHost(z.h_avail);
     if (z.h_ferr) cudaFreeHost(z.h_ferr);
     for (auto& bt : z.batches)
       if (bt.ev) cudaEventDestroy(bt.ev);
+    if (z.t_first) cudaEventDestroy(z.t_first);
+    if (z.t_last) cudaEventDestroy(z.t_last);
     throw;
   }
   Args& a = z.a;
@@ -3371,6 +3391,13 @@ void GpuDecoder::stream_worker() {
     CUDA_OK(cudaMemcpyAsync(z.h_ferr + p0, z.r_ferr + p0, n1, cudaMemcpyDeviceToHost, out_stream));
     if (n2) CUDA_OK(cudaMemcpyAsync(z.h_ferr, z.r_ferr, n2, cudaMemcpyDeviceToHost, out_stream));
     CUDA_OK(cudaEventRecord(bt.ev, out_stream));
+    {
+      std::lock_guard<std::mutex> lk(z.mu);
+      if (z.t_first_set) {
+        CUDA_OK(cudaEventRecord(z.t_last, out_stream));
+        z.t_last_set = true;
+      }
+    }
   };
   auto finish = [&](Stream::Batch& bt) {  // outputs copied: ticket done, ring rows free
     const size_t C = static_cast<size_t>(z.cap);
@@ -3399,6 +3426,15 @@ void GpuDecoder::stream_worker() {
         run = z.decoding > 0;
       }
       if (run) {
+        {
+          std::lock_guard<std::mutex> lk(z.mu);
+          if (z.timer_armed) {
+            CUDA_OK(cudaEventRecord(z.t_first, st));
+            z.timer_armed = false;
+            z.t_first_set = true;
+            z.t_last_set = false;
+          }
+        }
         const int slot = static_cast<int>(step % kRing);
         a.poll_slot = slot;
         run_step(a, st, z.want_post);
@@ -3476,6 +3512,34 @@ void GpuDecoder::stream_wait(int64_t ticket) {
   if (!err.empty()) throw ValidationError(err);
 }
 
+void GpuDecoder::stream_timer_reset() {
+  if (!stream_) throw ConfigError("stream: not open");
+  Stream& z = *stream_;
+  std::lock_guard<std::mutex> lk(z.mu);
+  if (z.decoding > 0 || z.copying > 0) throw ConfigError("stream: timer reset while batches are in flight");
+  z.timer_armed = true;
+  z.t_first_set = z.t_last_set = false;
+}
+
+double GpuDecoder::stream_device_ms() {
+  if (!stream_) throw ConfigError("stream: not open");
+  Stream& z = *stream_;
+  cudaEvent_t a, b;
+  {
+    std::lock_guard<std::mutex> lk(z.mu);
+    if (!z.fatal.empty()) throw CudaError(z.fatal);
+    if (!z.t_first_set || !z.t_last_set) throw ConfigError("stream: no batch completed since the timer reset");
+    a = z.t_first;
+    b = z.t_last;
+  }
+  DeviceGuard dg(device);
+  CUDA_OK(dg.status());
+  CUDA_OK(cudaEventSynchronize(b));
+  float ms = 0.0f;
+  CUDA_OK(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
 void GpuDecoder::stream_close() {
   if (!stream_) return;
   std::string fatal;
@@ -3500,16 +3564,20 @@ void GpuDecoder::stream_release() noexcept {
   cudaStreamSynchronize(copy_stream);
   cudaStreamSynchronize(out_stream);
   cudaStreamSynchronize(own_stream);
+  if (!prof_kid.empty()) (void)harvest_profile(base.frame_iters);
+  (void)cudaGetLastError();
   for (void* q : {static_cast<void*>(z.r_llr), static_cast<void*>(z.r_syn), static_cast<void*>(z.r_fbatch),
                   static_cast<void*>(z.r_ferr), static_cast<void*>(z.r_bdone), z.r_bits,
                   static_cast<void*>(z.r_iters), static_cast<void*>(z.r_reasons), static_cast<void*>(z.r_post),
                   static_cast<void*>(z.r_q)})
-    if (q) cudaFree(q);
+    if (q) dev_free(q);
   if (z.h_fbatch) cudaFreeHost(z.h_fbatch);
   if (z.h_avail) cudaFreeHost(z.h_avail);
   if (z.h_ferr) cudaFreeHost(z.h_ferr);
   for (auto& bt : z.batches)
     if (bt.ev) cudaEventDestroy(bt.ev);
+  if (z.t_first) cudaEventDestroy(z.t_first);
+  if (z.t_last) cudaEventDestroy(z.t_last);
   // the decoder returns to batch mode: counters and slot state are reset by
   // the next decode's init kernel
   stream_.reset();
@@ -3545,6 +3613,8 @@ int64_t gpu_stream_submit(GpuDecoder* dec, int32_t n, const float* llr, const ui
 bool gpu_stream_query(GpuDecoder* dec, int64_t ticket) { return dec->stream_query(ticket); }
 void gpu_stream_wait(GpuDecoder* dec, int64_t ticket) { dec->stream_wait(ticket); }
 void gpu_stream_close(GpuDecoder* dec) { dec->stream_close(); }
+void gpu_stream_timer_reset(GpuDecoder* dec) { dec->stream_timer_reset(); }
+double gpu_stream_device_ms(GpuDecoder* dec) { return dec->stream_device_ms(); }
 void gpu_set_profiling(GpuDecoder* dec, bool enable) { dec->profiling = enable; }
 void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches, double* frame_iterations) {
   if (kernel < 0 || kernel >= kNumKernels) throw ValidationError("profile: kernel id out of range");
@@ -3561,3 +3631,36 @@ void gpu_reset_profile(GpuDecoder* dec) {
 int64_t gpu_launch_count(const GpuDecoder* dec) { return dec->launches; }
 
 }  // namespace bpdec
+
+#ifdef BPDEC_GUARD
+// Guard-build self-test (not in include/bpdec.h; tests/test_guard_build.py):
+// 0 when (a) fresh allocations read as poison, (b) a one-element write past
+// the end of an allocation is reported by dev_verify, and (c) an in-bounds
+// write is not.
+namespace {
+__global__ void k_guard_probe(uint32_t* p, int n, int write_at, uint32_t* first) {
+  if (threadIdx.x == 0) {
+    *first = p[0];
+    if (write_at >= 0) p[write_at] = 7u;
+    (void)n;
+  }
+}
+}  // namespace
+extern "C" int bpdec_guard_selftest() {
+  using namespace bpdec;
+  void *a = nullptr, *r = nullptr;
+  if (dev_malloc(&a, 1000 * sizeof(uint32_t)) != cudaSuccess) return 1;
+  if (cudaMalloc(&r, sizeof(uint32_t)) != cudaSuccess) return 1;
+  uint32_t first = 0;
+  int rc = 0;
+  k_guard_probe<<<1, 32>>>(static_cast<uint32_t*>(a), 1000, 999, static_cast<uint32_t*>(r));  // in bounds
+  cudaMemcpy(&first, r, sizeof(first), cudaMemcpyDeviceToHost);
+  if (first != 0xFFFFFFFFu) rc |= 2;  // poison
+  if (dev_verify(nullptr) != cudaSuccess) rc |= 4;  // false positive
+  k_guard_probe<<<1, 32>>>(static_cast<uint32_t*>(a), 1000, 1000, static_cast<uint32_t*>(r));  // one past the end
+  if (dev_verify(nullptr) == cudaSuccess) rc |= 8;  // missed
+  cudaFree(r);
+  dev_free(a);
+  return rc;
+}
+#endif

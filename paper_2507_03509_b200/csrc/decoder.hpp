@@ -66,6 +66,8 @@ int64_t gpu_stream_submit(GpuDecoder* dec, int32_t n, const float* llr, const ui
 bool gpu_stream_query(GpuDecoder* dec, int64_t ticket);
 void gpu_stream_wait(GpuDecoder* dec, int64_t ticket);
 void gpu_stream_close(GpuDecoder* dec);
+void gpu_stream_timer_reset(GpuDecoder* dec);
+double gpu_stream_device_ms(GpuDecoder* dec);
 void gpu_set_profiling(GpuDecoder* dec, bool enable);
 void gpu_profile(const GpuDecoder* dec, int kernel, double* total_ms, int64_t* launches,
                  double* frame_iterations);

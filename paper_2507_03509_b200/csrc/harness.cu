@@ -14,6 +14,7 @@
 
 #include "decoder.hpp"
 #include "devguard.hpp"
+#include "devmem.hpp"
 #include "harness.hpp"
 
 namespace bpdec {
@@ -54,9 +55,9 @@ __global__ void k_any_bit(const uint32_t* bits, int32_t nw, int32_t frames, uint
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
-  explicit DevBuf(size_t n) { HCUDA_OK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
+  explicit DevBuf(size_t n) { HCUDA_OK(dev_malloc(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T))); }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;

@@ -530,6 +530,17 @@ class BatchDecoder:
         _check(self._lib.bpdec_stream_query(self._h, int(ticket), C.byref(d)))
         return bool(d.value)
 
+    def stream_timer_reset(self):
+        """Arms the stream's device timer (no batch may be in flight)."""
+        _check(self._lib.bpdec_stream_timer_reset(self._h))
+
+    def stream_device_ms(self) -> float:
+        """CUDA-event time from the first step launched after
+        stream_timer_reset to the last completed batch's output copy."""
+        ms = C.c_double()
+        _check(self._lib.bpdec_stream_device_ms(self._h, C.byref(ms)))
+        return ms.value
+
     def stream_close(self):
         try:
             _check(self._lib.bpdec_stream_close(self._h))

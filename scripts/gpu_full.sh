@@ -11,9 +11,9 @@ for wl in cfg3 cfg4 cfg5; do
   timeout 900 python bench.py --workload $wl --no-cpu-baseline > gpurun_out/bench_$wl.log 2>&1; echo "bench_$wl=$?" >> gpurun_out/status.txt
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "bench_ref=$?" >> gpurun_out/status.txt
-python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-pce-compare > gpurun_out/ncu_plain.log 2>&1 && \
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-pce-compare --no-traffic > gpurun_out/ncu_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_bench.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-pce-compare > gpurun_out/ncu_launch.log 2>&1
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-pce-compare --no-traffic > gpurun_out/ncu_launch.log 2>&1
 echo "ncu_launches=$?" >> gpurun_out/status.txt
 cat gpurun_out/status.txt
 timeout 900 python scripts/vnr_pce_sweep.py gpurun_out/et_sweep_cfg2.json > gpurun_out/sweep2.log 2>&1; echo "sweep2=$?" >> gpurun_out/status.txt
