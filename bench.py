@@ -36,7 +36,7 @@ E_BYTES_MODEL_A = None  # filled per code: 16E + 4N + (N+M)/8 per frame-iteratio
 
 # frames per GPU per step for each BASELINE workload (cfg4/cfg5 are the
 # 8-GPU streams 512..4096 / 8192 frames; per GPU at N=1 the first shard)
-FRAMES = {"cfg1": 16, "cfg2": 64, "cfg3": 32, "cfg4": 512, "cfg5": 1024}
+FRAMES = {"cfg1": 16, "cfg2": 64, "cfg3": 32, "cfg4": 512, "cfg5": 1024, "met": 64, "met_s": 16}
 
 
 def workload_beta(args):
@@ -45,8 +45,9 @@ def workload_beta(args):
         return None, (0.92, 1.0)
     if args.beta is not None:
         return args.beta, None
-    # cfg2/cfg4: the middle of configs[1]'s swept grid (0.92 .. 0.99)
-    return (0.98 if args.workload == "cfg3" else 0.96), None
+    # cfg2/cfg4: the middle of configs[1]'s swept grid (0.92 .. 0.99); met:
+    # inside its waterfall (FER between 0 and 1)
+    return {"cfg3": 0.98, "met": 0.82, "met_s": 0.75}.get(args.workload, 0.96), None
 
 
 def parse():

@@ -96,6 +96,15 @@ int bpdec_code_lift_protograph(const int32_t* base, int32_t rows, int32_t cols, 
 int bpdec_code_generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1,
                             int32_t n_classes, const int32_t* degrees, const double* probs,
                             uint64_t seed, bpdec_code** out);
+/* Two-edge-type low-rate construction with a core code (new; SURVEY §8f#2
+ * "a MET-style generator so FER < 1"): core variables 0..nc-1 (nc = N -
+ * n_deg1) with type-1 degrees core_degrees[i] in proportions core_probs[i]
+ * on the M - n_deg1 core checks; each of the n_deg1 extension checks holds
+ * ext_degree type-2 edges to core variables (dealt evenly, seeded shuffle)
+ * and one degree-1 variable (nc + j).  Rule in csrc/code.cpp. */
+int bpdec_code_generate_met_core(int32_t n_vars, int32_t n_checks, int32_t n_deg1, int32_t n_classes,
+                                 const int32_t* core_degrees, const double* core_probs, int32_t ext_degree,
+                                 uint64_t seed, bpdec_code** out);
 void bpdec_code_destroy(bpdec_code* code);
 /* n_active = |{v : deg(v) >= 2}| (ActiveVarSet, parity_check_matrix.hpp:66-70) */
 int bpdec_code_dims(const bpdec_code* code, int32_t* n_vars, int32_t* n_checks,

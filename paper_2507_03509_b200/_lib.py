@@ -57,6 +57,8 @@ SIGNATURES = [
      [c_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
     ("bpdec_code_generate_met", C.c_int,
      [C.c_int32, C.c_int32, C.c_double, C.c_int32, c_i32p, c_f64p, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("bpdec_code_generate_met_core", C.c_int,
+     [C.c_int32, C.c_int32, C.c_int32, C.c_int32, c_i32p, c_f64p, C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
     ("bpdec_code_destroy", None, [C.c_void_p]),
     ("bpdec_code_dims", C.c_int, [C.c_void_p, c_i32p, c_i32p, c_i64p, c_i32p]),
     ("bpdec_code_csr", C.c_int, [C.c_void_p, c_i32p, c_i32p]),

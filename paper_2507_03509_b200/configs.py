@@ -24,9 +24,17 @@ class Workload:
     frames: int
     d_max: int
     betas: Tuple[float, ...]
+    # > 0: the two-edge-type construction with a core code (generate_met_core,
+    # ext_degree type-2 edges per extension check; `degrees` / `probs` are
+    # the core variables' type-1 degrees) instead of the BASELINE generator
+    ext_degree: int = 0
 
     def make_code(self):
-        from .decoder import generate_met
+        from .decoder import generate_met, generate_met_core
+        if self.ext_degree:
+            n1 = int(self.frac_deg1 * self.n_vars + 0.5)
+            return generate_met_core(self.n_vars, self.n_checks, n1, self.degrees, self.probs, self.ext_degree,
+                                     CODE_SEED)
         return generate_met(self.n_vars, self.n_checks, self.frac_deg1, self.degrees, self.probs, CODE_SEED)
 
 
@@ -49,4 +57,12 @@ WORKLOADS = {
     # configs[4]: mixed-SNR streaming, beta ~ U[0.92, 1.0] per frame
     "cfg5": Workload("cfg5_r0.05_n2^21_stream", 1 << 21, _m(1 << 21, 0.05), 0.80, (3, 8, 16), (0.5, 0.3, 0.2),
                      8192, 500, (0.92, 1.0)),
+    # a code family whose FER falls below 1 (the BASELINE
+    # construction's never does): rate 0.1, 85% degree-1 variables on
+    # extension checks with 3 core edges each, core variables of type-1
+    # degree 2 / 3 on a core code; waterfall around beta = 0.8
+    "met": Workload("met_r0.1_n2^20", 1 << 20, _m(1 << 20, 0.1), 0.85, (2, 3), (0.5, 0.5), 64, 500,
+                    (0.74, 0.76, 0.78, 0.80, 0.82, 0.84, 0.86), ext_degree=3),
+    "met_s": Workload("met_r0.1_n8192", 8192, _m(8192, 0.1), 0.85, (2, 3), (0.5, 0.5), 16, 200, (0.6, 0.75, 0.85),
+                      ext_degree=3),
 }

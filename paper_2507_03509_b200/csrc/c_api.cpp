@@ -176,6 +176,20 @@ int bpdec_code_generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1, 
   });
 }
 
+int bpdec_code_generate_met_core(int32_t n_vars, int32_t n_checks, int32_t n_deg1, int32_t n_classes,
+                                 const int32_t* core_degrees, const double* core_probs, int32_t ext_degree,
+                                 uint64_t seed, bpdec_code** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (n_classes <= 0) throw bpdec::ValidationError("met core generator: need at least one degree class");
+    need(core_degrees, "core_degrees");
+    need(core_probs, "core_probs");
+    std::vector<int32_t> d(core_degrees, core_degrees + n_classes);
+    std::vector<double> p(core_probs, core_probs + n_classes);
+    *out = new bpdec_code{bpdec::generate_met_core(n_vars, n_checks, n_deg1, d, p, ext_degree, seed)};
+  });
+}
+
 void bpdec_code_destroy(bpdec_code* code) { delete code; }
 
 int bpdec_code_dims(const bpdec_code* code, int32_t* n_vars, int32_t* n_checks, int64_t* n_edges,

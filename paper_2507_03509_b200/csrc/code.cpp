@@ -422,6 +422,111 @@ Code generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1,
   return Code::from_csr(n_vars, n_checks, ptr.data(), vars.data());
 }
 
+// Two-edge-type low-rate construction (a multi-edge-type code in the sense
+// of SURVEY §8f#2; new, not in the reference).  Variables: core 0..nc-1,
+// degree-1 nc..N-1 (nc = N - n1).  Checks: core 0..Mc-1 (Mc = M - n1), which
+// hold only type-1 edges of core variables, and extension checks Mc+j, which
+// hold ext_degree type-2 edges of core variables plus the degree-1 variable
+// nc+j.  Every codeword restricted to the core variables is a codeword of
+// the core code, so its minimum distance is not capped by the degree-1
+// block (the BASELINE construction has distance ~4: a degree-3 variable and
+// the degree-1 variables of its checks).
+//   type 1: core class counts round(nc * p_i) (remainder in the last class),
+//           classes in variable order; check sockets k mod Mc after a
+//           SplitMix Fisher-Yates shuffle; duplicates repaired by swaps.
+//   type 2: socket i belongs to extension check Mc + i / ext_degree; its
+//           variable is i mod nc after a Fisher-Yates shuffle of those
+//           (same engine, continued), so type-2 degrees differ by <= 1;
+//           duplicates within a check repaired by swaps.
+Code generate_met_core(int32_t n_vars, int32_t n_checks, int32_t n_deg1, const std::vector<int32_t>& core_degrees,
+                       const std::vector<double>& core_probs, int32_t ext_degree, uint64_t seed) {
+  check_dims(n_vars, n_checks);
+  if (core_degrees.empty() || core_degrees.size() != core_probs.size())
+    throw ValidationError("met core generator: degree and probability lists must be non-empty and aligned");
+  if (n_deg1 <= 0 || n_deg1 >= n_checks || n_deg1 >= n_vars)
+    throw ValidationError("met core generator: need 0 < n_deg1 < min(n_checks, n_vars)");
+  const int32_t nc = n_vars - n_deg1, mc = n_checks - n_deg1, n1 = n_deg1;
+  if (ext_degree < 1 || ext_degree > nc)
+    throw ValidationError("met core generator: ext_degree must lie in [1, number of core variables]");
+  std::vector<int64_t> counts(core_degrees.size());
+  int64_t assigned = 0;
+  for (size_t i = 0; i < core_degrees.size(); ++i) {
+    if (core_degrees[i] < 1 || core_degrees[i] > mc)
+      throw ValidationError("met core generator: core degrees must lie in [1, number of core checks]");
+    if (i + 1 < core_degrees.size()) {
+      counts[i] = static_cast<int64_t>(std::floor(nc * core_probs[i] + 0.5));
+      assigned += counts[i];
+    }
+  }
+  counts.back() = nc - assigned;
+  if (counts.back() < 0) throw ValidationError("met core generator: class proportions exceed 1");
+  SplitMixEngine rng(seed);
+  // ---- type 1: core variables x core checks
+  std::vector<int64_t> sp(static_cast<size_t>(nc) + 1, 0);
+  {
+    int64_t v = 0;
+    for (size_t i = 0; i < core_degrees.size(); ++i)
+      for (int64_t k = 0; k < counts[i]; ++k, ++v) sp[v + 1] = sp[v] + core_degrees[i];
+  }
+  const int64_t e1 = sp[nc];
+  const int64_t e2 = static_cast<int64_t>(n1) * ext_degree;
+  if (e1 + e2 + n1 > INT32_MAX) throw ValidationError("met core generator: too many edges");
+  std::vector<int32_t> own1(e1), cs1(e1);
+  for (int32_t v = 0; v < nc; ++v)
+    for (int64_t k = sp[v]; k < sp[v + 1]; ++k) own1[k] = v;
+  for (int64_t k = 0; k < e1; ++k) cs1[k] = static_cast<int32_t>(k % mc);
+  for (int64_t i = e1 - 1; i > 0; --i) std::swap(cs1[i], cs1[rng.bounded(static_cast<uint64_t>(i + 1))]);
+  auto holds1 = [&](int32_t v, int32_t c, int64_t except) {
+    for (int64_t k = sp[v]; k < sp[v + 1]; ++k)
+      if (k != except && cs1[k] == c) return true;
+    return false;
+  };
+  for (int64_t k = 0; k < e1; ++k) {
+    const int32_t v = own1[k];
+    if (!holds1(v, cs1[k], k)) continue;
+    for (long budget = 1L << 20;; ) {
+      if (--budget < 0) throw ValidationError("met core generator: cannot remove duplicate type-1 edges");
+      const int64_t k2 = static_cast<int64_t>(rng.bounded(static_cast<uint64_t>(e1)));
+      const int32_t w = own1[k2];
+      if (w == v || holds1(v, cs1[k2], k) || holds1(w, cs1[k], k2)) continue;
+      std::swap(cs1[k], cs1[k2]);
+      break;
+    }
+  }
+  // ---- type 2: core variables x extension checks (ext_degree sockets each)
+  std::vector<int32_t> own2(e2);
+  for (int64_t i = 0; i < e2; ++i) own2[i] = static_cast<int32_t>(i % nc);
+  for (int64_t i = e2 - 1; i > 0; --i) std::swap(own2[i], own2[rng.bounded(static_cast<uint64_t>(i + 1))]);
+  auto in_check2 = [&](int64_t i, int32_t v) {  // another socket of i's check holds v
+    const int64_t b = (i / ext_degree) * ext_degree;
+    for (int64_t k = b; k < b + ext_degree; ++k)
+      if (k != i && own2[k] == v) return true;
+    return false;
+  };
+  for (int64_t i = 0; i < e2; ++i) {
+    if (!in_check2(i, own2[i])) continue;
+    for (long budget = 1L << 20;; ) {
+      if (--budget < 0) throw ValidationError("met core generator: cannot remove duplicate type-2 edges");
+      const int64_t i2 = static_cast<int64_t>(rng.bounded(static_cast<uint64_t>(e2)));
+      if (i2 / ext_degree == i / ext_degree || in_check2(i, own2[i2]) || in_check2(i2, own2[i])) continue;
+      std::swap(own2[i], own2[i2]);
+      break;
+    }
+  }
+  // ---- CSR (check lists ascending)
+  std::vector<int32_t> ptr(static_cast<size_t>(n_checks) + 1, 0);
+  for (int64_t k = 0; k < e1; ++k) ++ptr[cs1[k] + 1];
+  for (int32_t j = 0; j < n1; ++j) ptr[mc + j + 1] = ext_degree + 1;
+  for (int32_t c = 0; c < n_checks; ++c) ptr[c + 1] += ptr[c];
+  std::vector<int32_t> vars(ptr[n_checks]);
+  std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+  for (int64_t k = 0; k < e1; ++k) vars[fill[cs1[k]]++] = own1[k];
+  for (int64_t i = 0; i < e2; ++i) vars[fill[mc + i / ext_degree]++] = own2[i];
+  for (int32_t j = 0; j < n1; ++j) vars[fill[mc + j]++] = nc + j;
+  for (int32_t c = 0; c < n_checks; ++c) std::sort(vars.begin() + ptr[c], vars.begin() + ptr[c + 1]);
+  return Code::from_csr(n_vars, n_checks, ptr.data(), vars.data());
+}
+
 std::vector<int32_t> apply_puncture(const Code& code, double target_rate, uint64_t seed, double* effective_rate) {
   const double rate = code.rate();
   if (target_rate >= 1.0) throw ValidationError("puncture: target rate must be below 1");

@@ -77,6 +77,10 @@ Code generate_met(int32_t n_vars, int32_t n_checks, double frac_deg1,
                   const std::vector<int32_t>& degrees, const std::vector<double>& probs,
                   uint64_t seed);
 
+// Two-edge-type low-rate construction with a core code (see code.cpp).
+Code generate_met_core(int32_t n_vars, int32_t n_checks, int32_t n_deg1, const std::vector<int32_t>& core_degrees,
+                       const std::vector<double>& core_probs, int32_t ext_degree, uint64_t seed);
+
 // ≙ apply_puncture (puncture.cpp:16-48): round(N - (N-M)/target) positions
 // drawn uniformly (partial Fisher-Yates, SplitMixEngine(seed)) from the
 // degree>=2 variables, ascending.  Returns the positions; *effective_rate set.

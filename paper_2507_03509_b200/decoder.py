@@ -44,7 +44,7 @@ from . import _lib
 __all__ = [
     "ConfigError", "IoError", "ValidationError", "BpdecCudaError", "BpdecOomError", "MultiDecoder",
     "ParityCheckMatrix", "ActiveVarSet", "active_var_set", "load_alist", "save_alist",
-    "lift_protograph", "generate_met", "DecodeConfig", "StopReason", "DecodeOutcome",
+    "lift_protograph", "generate_met", "generate_met_core", "DecodeConfig", "StopReason", "DecodeOutcome",
     "BatchResult", "BpDecoder", "BatchDecoder", "decode", "syndrome_check", "vnr_statistic",
     "vnr_should_stop", "snr_for_beta", "sample_frames", "sample_frames_beta", "pack_bits", "unpack_bits",
     "PunctureMask", "no_puncture", "apply_puncture", "StopRule", "TrialStats", "wilson_interval", "run_trials",
@@ -231,6 +231,22 @@ def generate_met(n_vars: int, n_checks: int, frac_deg1: float, degrees: Sequence
     h = C.c_void_p()
     _check(lib.bpdec_code_generate_met(n_vars, n_checks, float(frac_deg1), d.size, _ptr(d, _lib.c_i32p),
                                        _ptr(p, _lib.c_f64p), seed, C.byref(h)))
+    return ParityCheckMatrix(h)
+
+
+def generate_met_core(n_vars: int, n_checks: int, n_deg1: int, core_degrees: Sequence[int],
+                      core_probs: Sequence[float], ext_degree: int, seed: int) -> ParityCheckMatrix:
+    """Two-edge-type low-rate construction with a core code (rule in
+    csrc/code.cpp, bpdec_code_generate_met_core): a code family whose FER
+    falls below 1 (the BASELINE construction's never does)."""
+    lib = _lib.load()
+    d = np.ascontiguousarray(core_degrees, dtype=np.int32)
+    p = np.ascontiguousarray(core_probs, dtype=np.float64)
+    if d.size != p.size:
+        raise ValidationError("met core generator: degree and probability lists must be aligned")
+    h = C.c_void_p()
+    _check(lib.bpdec_code_generate_met_core(int(n_vars), int(n_checks), int(n_deg1), d.size, _ptr(d, _lib.c_i32p),
+                                            _ptr(p, _lib.c_f64p), int(ext_degree), seed, C.byref(h)))
     return ParityCheckMatrix(h)
 
 

@@ -5,7 +5,13 @@ D_max = 500, ET in {none, PCE, VNR(+PCE)}: mean iterations, FER with the
 reference's Wilson interval (channel.cpp:63-72), edge-updates/s and info
 bits/s, and the VNR/PCE gains.
 
-Usage: python scripts/vnr_pce_sweep.py [out.json] [--workload cfg2|cfg5] [--no-none]
+For codes whose FER falls below 1 (--workload met): decoded info bits/s per
+policy and the decoder throughput ratio of Eq. (2),
+K_VNR / K = (D_bar_Dmax / D_bar_VNR) * (1 - FER_VNR) / (1 - FER_Dmax), for
+D_max in --dmax (PCE-ET in both, as in the paper's simulations).
+
+Usage: python scripts/vnr_pce_sweep.py [out.json] [--workload W] [--betas ...]
+       [--frames F] [--batches B] [--dmax 250 500] [--no-none]
 (GPU required)
 """
 import argparse
@@ -24,47 +30,75 @@ from paper_2507_03509_b200.decoder import Q_ABS  # noqa: E402
 BETAS = [0.10, 0.20, 0.30, 0.40, 0.50, 0.70, 0.80, 0.90, 0.92, 0.94, 0.96, 0.98, 0.99]
 
 
-def policies(w, with_none):
+def policies(w, with_none, dmaxes):
     out = []
     if with_none:
         out.append(("none", P.DecodeConfig(d_max=w.d_max, use_pce=False, use_vnr=False, q_mode=Q_ABS)))
     out.append(("pce", P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=False, q_mode=Q_ABS)))
+    for d in dmaxes:
+        if d != w.d_max:
+            out.append((f"pce{d}", P.DecodeConfig(d_max=d, use_pce=True, use_vnr=False, q_mode=Q_ABS)))
     out.append(("vnr", P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS)))
     return out
 
 
-def measure(dec, code, cfg, llr, syn, x, out, frames):
-    N, M, E = code.n_vars, code.n_checks, code.n_edges
-    dec.decode_batch(llr, cfg, syndrome=syn, packed=True, out=out)  # warm
+class Acc:
+    """Per-policy totals over the batches of one beta point."""
+
+    def __init__(self):
+        self.frames = self.errors = self.success = self.undetected = self.iters = 0
+        self.seconds = 0.0
+        self.stops = [0, 0, 0]
+
+    def add(self, cfg, out, x, dt):
+        it = out["iterations"].cpu().numpy()
+        rs = out["reasons"].cpu().numpy()
+        ok_bits = (out["bits"] == x).all(dim=1).cpu().numpy()
+        # a frame is decoded when its bits equal the message; without PCE the
+        # reason is max_iterations even for a correct frame
+        success = ok_bits if not cfg.use_pce else (rs == 0) & ok_bits
+        self.frames += len(it)
+        self.success += int(success.sum())
+        self.errors += int(len(it) - success.sum())
+        self.undetected += int(((rs == 0) & ~ok_bits).sum())
+        self.iters += int(it.sum())
+        self.seconds += dt
+        for k in range(3):
+            self.stops[k] += int((rs == k).sum())
+
+    def row(self, code):
+        N, M, E = code.n_vars, code.n_checks, code.n_edges
+        lo, hi = P.wilson_interval(self.errors, self.frames)
+        return {"frames": self.frames, "d_bar": self.iters / self.frames, "fer": self.errors / self.frames,
+                "fer_ci": [lo, hi],
+                "stops": {"syndrome": self.stops[0], "vnr": self.stops[1], "max_iter": self.stops[2]},
+                "undetected": self.undetected, "seconds": self.seconds,
+                "edge_updates_per_s": self.iters * E / self.seconds,
+                "decoded_info_bits_per_s": self.success * (N - M) / self.seconds,
+                "processed_info_bits_per_s": self.frames * (N - M) / self.seconds}
+
+
+def timed_decode(dec, cfg, llr, syn, out):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     dec.decode_batch(llr, cfg, syndrome=syn, packed=True, out=out)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    it = out["iterations"].cpu().numpy()
-    rs = out["reasons"].cpu().numpy()
-    ok_bits = (out["bits"] == x).all(dim=1).cpu().numpy()
-    # a frame is decoded when its bits equal the message; without PCE the
-    # reason is max_iterations even for a correct frame
-    success = ok_bits if not cfg.use_pce else (rs == 0) & ok_bits
-    errors = int(frames - success.sum())
-    lo, hi = P.wilson_interval(errors, frames)
-    return {"d_bar": float(it.mean()), "fer": errors / frames, "fer_ci": [lo, hi],
-            "stops": {"syndrome": int((rs == 0).sum()), "vnr": int((rs == 1).sum()), "max_iter": int((rs == 2).sum())},
-            "undetected": int(((rs == 0) & ~ok_bits).sum()),
-            "seconds": dt, "edge_updates_per_s": float(it.sum()) * E / dt,
-            "decoded_info_bits_per_s": float(success.sum()) * (N - M) / dt,
-            "processed_info_bits_per_s": frames * (N - M) / dt}
+    return time.perf_counter() - t0
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("out", nargs="?", default=None)
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--betas", type=float, nargs="*", default=None)
+    ap.add_argument("--frames", type=int, default=None, help="frames per batch")
+    ap.add_argument("--batches", type=int, default=1, help="batches per beta point (frames for the FER CI)")
+    ap.add_argument("--dmax", type=int, nargs="*", default=[], help="extra PCE-only D_max values (Eq. 2 ratios)")
     ap.add_argument("--no-none", action="store_true", help="skip ET none (D_max iterations per frame)")
     args = ap.parse_args()
     w = P.WORKLOADS[args.workload]
-    frames = 64 if args.workload == "cfg2" else 1024  # cfg5: one GPU's share of the 8192-frame stream
+    mixed = args.workload == "cfg5"
+    frames = args.frames or (1024 if mixed else 64)  # cfg5: one GPU's share of the 8192-frame stream
     out_path = args.out or os.path.join(ROOT, "gpurun_out", f"et_sweep_{args.workload}.json")
     code = w.make_code()
     N, M, E = code.n_vars, code.n_checks, code.n_edges
@@ -75,29 +109,48 @@ def main():
     out = {"iterations": torch.zeros(frames, dtype=torch.int32, device="cuda"),
            "reasons": torch.zeros(frames, dtype=torch.uint8, device="cuda"),
            "bits": torch.zeros((frames, (N + 31) // 32), dtype=torch.int32, device="cuda")}
-    points = [(b, None) for b in BETAS] if args.workload == "cfg2" else [(None, (0.92, 1.0))]
+    betas = args.betas if args.betas else (BETAS if args.workload == "cfg2" else list(w.betas))
+    points = [(None, (0.92, 1.0))] if mixed else [(b, None) for b in betas]
+    pols = policies(w, not args.no_none, args.dmax)
     rows = []
+    warmed = False
     for beta, brange in points:
+        acc = {name: Acc() for name, _ in pols}
+        for bi in range(args.batches):
+            first = bi * frames
+            if brange is None:
+                snr = P.snr_for_beta(beta, code.rate())
+                dec.sample_frames_device(snr, P.FRAME_SEED, first, frames, llr, syn, x)
+            else:
+                dec.sample_frames_device(0.0, P.FRAME_SEED, first, frames, llr, syn, x, beta_range=brange)
+            for name, cfg in pols:
+                if not warmed:
+                    timed_decode(dec, cfg, llr, syn, out)
+                    warmed = True
+                acc[name].add(cfg, out, x, timed_decode(dec, cfg, llr, syn, out))
+        row = {"beta": beta, "frames": frames * args.batches} if brange is None else \
+            {"beta_range": list(brange), "frames": frames * args.batches}
         if brange is None:
-            snr = P.snr_for_beta(beta, code.rate())
-            dec.sample_frames_device(snr, P.FRAME_SEED, 0, frames, llr, syn, x)
-            row = {"beta": beta, "snr": snr, "frames": frames}
-        else:
-            dec.sample_frames_device(0.0, P.FRAME_SEED, 0, frames, llr, syn, x, beta_range=brange)
-            row = {"beta_range": list(brange), "frames": frames}
-        for name, cfg in policies(w, not args.no_none):
-            row[name] = measure(dec, code, cfg, llr, syn, x, out, frames)
+            row["snr"] = P.snr_for_beta(beta, code.rate())
+        for name, _ in pols:
+            row[name] = acc[name].row(code)
         row["iteration_gain"] = row["pce"]["d_bar"] / row["vnr"]["d_bar"]
         row["frame_throughput_gain"] = row["pce"]["seconds"] / row["vnr"]["seconds"]
+        # Eq. (2): K = N R (1 - FER) / D_bar per iteration latency
+        for name, _ in pols:
+            if name.startswith("pce") and row[name]["fer"] < 1.0:
+                row[f"k_vnr_over_k_{name}"] = (row[name]["d_bar"] / row["vnr"]["d_bar"]) * \
+                    (1.0 - row["vnr"]["fer"]) / (1.0 - row[name]["fer"])
         rows.append(row)
         print(json.dumps({"point": beta if brange is None else list(brange),
-                          **{f"d_{k}": row[k]["d_bar"] for k in ("none", "pce", "vnr") if k in row},
-                          **{f"fer_{k}": row[k]["fer"] for k in ("none", "pce", "vnr") if k in row},
-                          **{f"eu_{k}": row[k]["edge_updates_per_s"] for k in ("none", "pce", "vnr") if k in row},
+                          **{f"d_{k}": row[k]["d_bar"] for k, _ in pols},
+                          **{f"fer_{k}": row[k]["fer"] for k, _ in pols},
+                          **{f"dec_bits_{k}": row[k]["decoded_info_bits_per_s"] for k, _ in pols},
+                          **{k: v for k, v in row.items() if k.startswith("k_vnr")},
                           "gain_it": row["iteration_gain"], "gain_frames": row["frame_throughput_gain"]}),
               flush=True)
     res = {"workload": w.name, "code": {"N": N, "M": M, "E": E, "rate": code.rate()}, "d_max": w.d_max,
-           "q_mode": "abs", "data": "synthetic (seeded BASELINE generator, device-generated syndrome-mode frames)",
+           "q_mode": "abs", "data": "synthetic (seeded generator, device-generated syndrome-mode frames)",
            "gpu": torch.cuda.get_device_name(0), "rows": rows}
     with open(out_path, "w") as f:
         json.dump(res, f, indent=1)

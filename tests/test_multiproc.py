@@ -89,3 +89,56 @@ def test_shard_partition(total, world):
         a, b = bench.shard(total, r, world)
         seen.extend(range(a, b))
     assert seen == list(range(total))
+
+
+def _gpu_worker(rank, world, port, total, q):
+    """One rank of the frame-sharded GPU decode: its shard of global frames
+    through its own BatchDecoder (both ranks share cuda:0 here: one GPU per
+    gpurun box; the ranks never wait on each other's kernels), results
+    gathered to rank 0 over gloo (the host gather of SURVEY §8e)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import bench
+    import paper_2507_03509_b200 as P
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    code = P.WORKLOADS["cfg1"].make_code()
+    a, b = bench.shard(total, rank, world)
+    llr, x, s = P.sample_frames(code, P.snr_for_beta(0.95, code.rate()), P.FRAME_SEED, a, b - a)
+    dec = P.BatchDecoder(code, device=0, max_slots=32)
+    r = dec.decode_batch(llr, P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS),
+                         syndrome=s, packed=True)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (a, b, r.iterations.tolist(), r.reasons.tolist(), r.bits.tolist()))
+    if rank == 0:
+        q.put(gathered)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_gpu_decode_gloo():
+    """Two ranks decode disjoint shards of 100 cfg1 frames on the GPU; the
+    gathered per-frame outputs equal one decoder decoding all 100."""
+    total = 100
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, total, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import paper_2507_03509_b200 as P
+    code = P.WORKLOADS["cfg1"].make_code()
+    llr, x, s = P.sample_frames(code, P.snr_for_beta(0.95, code.rate()), P.FRAME_SEED, 0, total)
+    want = P.BatchDecoder(code, device=0, max_slots=64).decode_batch(
+        llr, P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS), syndrome=s, packed=True)
+    its = [i for a, b, it, rs, bt in sorted(gathered) for i in it]
+    rss = [i for a, b, it, rs, bt in sorted(gathered) for i in rs]
+    bits = np.array([w for a, b, it, rs, bt in sorted(gathered) for w in bt], dtype=np.uint32)
+    assert its == want.iterations.tolist() and rss == want.reasons.tolist()
+    assert np.array_equal(bits, want.bits.view(np.uint32))
