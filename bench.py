@@ -47,7 +47,7 @@ def workload_beta(args):
         return args.beta, None
     # cfg2/cfg4: the middle of configs[1]'s swept grid (0.92 .. 0.99); met:
     # inside its waterfall (FER between 0 and 1)
-    return {"cfg3": 0.98, "met": 0.82, "met_s": 0.75}.get(args.workload, 0.96), None
+    return {"cfg3": 0.98, "met": 0.87, "met_s": 0.8}.get(args.workload, 0.96), None
 
 
 def parse():

@@ -58,11 +58,11 @@ WORKLOADS = {
     "cfg5": Workload("cfg5_r0.05_n2^21_stream", 1 << 21, _m(1 << 21, 0.05), 0.80, (3, 8, 16), (0.5, 0.3, 0.2),
                      8192, 500, (0.92, 1.0)),
     # a code family whose FER falls below 1 (the BASELINE
-    # construction's never does): rate 0.1, 85% degree-1 variables on
-    # extension checks with 3 core edges each, core variables of type-1
-    # degree 2 / 3 on a core code; waterfall around beta = 0.8
-    "met": Workload("met_r0.1_n2^20", 1 << 20, _m(1 << 20, 0.1), 0.85, (2, 3), (0.5, 0.5), 64, 500,
-                    (0.74, 0.76, 0.78, 0.80, 0.82, 0.84, 0.86), ext_degree=3),
-    "met_s": Workload("met_r0.1_n8192", 8192, _m(8192, 0.1), 0.85, (2, 3), (0.5, 0.5), 16, 200, (0.6, 0.75, 0.85),
-                      ext_degree=3),
+    # construction's never does): rate 0.1, 70% degree-1 variables on
+    # extension checks with 2 core edges each, core variables of type-1
+    # degree 2 / 3 on a core code (check degrees 3 / 4)
+    "met": Workload("met_r0.1_n2^20", 1 << 20, _m(1 << 20, 0.1), 0.70, (2, 3), (0.5, 0.5), 64, 500,
+                    (0.84, 0.85, 0.86, 0.87, 0.88, 0.89, 0.90), ext_degree=2),
+    "met_s": Workload("met_r0.1_n8192", 8192, _m(8192, 0.1), 0.70, (2, 3), (0.5, 0.5), 16, 200, (0.7, 0.8, 0.9),
+                      ext_degree=2),
 }

@@ -79,6 +79,20 @@ constexpr int kThreads = 256;
 constexpr int kCheckThreads = 128;  // k_check blocks: 4 warps (per-warp smem ring)
 enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompact = 5, kSnapshot = 6, kTrace = 7, kNumKernels = 8 };
 // (kSyn = k_decide; kTerm is kept for the profiling ABI and stays 0)
+#ifndef BPDEC_CHECK_MINB
+#define BPDEC_CHECK_MINB 5
+#endif
+#ifndef BPDEC_SPLIT_MAXD
+#define BPDEC_SPLIT_MAXD 4
+#endif
+constexpr int kCheckMinBlocks = BPDEC_CHECK_MINB;  // k_check blocks per SM (register budget)
+// k_check kernels (by maximum check degree) with a separate steady-state
+// copy of every typed chunk loop, which also uses the phi-domain degree-1
+// edge (kPhiD in check_batch_compute); wider kernels keep one copy
+// (instruction cache; splitting k_check<8> measured -2% on a (3,1) code)
+constexpr int kSplitMaxD = BPDEC_SPLIT_MAXD;
+constexpr int kCheckGrab = 1;     // k_check chunks per scheduler atomic (2: -9% on cfg2, the two
+                                  // chunks of a grab run back to back on one warp instead of side by side)
 constexpr int kTermBlocks = 16;   // k_decide q-reduction blocks per group (q partial tree: fixed by the code)
 
 // ------------------------------------------------------------ arguments --
@@ -249,9 +263,15 @@ __device__ __forceinline__ int sched_issue(const Args& a, int ctr, int lane) {
   return k;  // valid in lane 0 only
 }
 
-__device__ __forceinline__ long long sched_resolve(const Args& a, int k, int lane, int per_group,
-                                                   const int32_t* __restrict__ sched) {
-  k = __shfl_sync(0xffffffffu, k, 0);
+__device__ __forceinline__ int sched_issue_n(const Args& a, int ctr, int lane, int n) {
+  int k = 0;
+  if (lane == 0) k = atomicAdd(&a.counters[ctr], n);
+  return k;  // valid in lane 0 only
+}
+
+// k uniform across the warp
+__device__ __forceinline__ long long sched_map(const Args& a, int k, int lane, int per_group,
+                                               const int32_t* __restrict__ sched) {
   const long long total = static_cast<long long>(a.G) * per_group;
   int gi = k / per_group;
   if (gi >= a.G) return total;
@@ -268,6 +288,11 @@ __device__ __forceinline__ long long sched_resolve(const Args& a, int k, int lan
     gi -= n;
   }
   return total;
+}
+
+__device__ __forceinline__ long long sched_resolve(const Args& a, int k, int lane, int per_group,
+                                                   const int32_t* __restrict__ sched) {
+  return sched_map(a, __shfl_sync(0xffffffffu, k, 0), lane, per_group, sched);
 }
 
 // ------------------------------------------------------------- k_check --
@@ -357,6 +382,48 @@ __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&ou
     }
     out[0] = fminf(dev::phi(suf), clamp);
   }
+}
+
+// Check with NH edges to degree>=2 variables and one degree-1 edge whose
+// phi value phd is given: outputs of the NH hi edges (same prefix / suffix
+// order as check_magnitudes<NH+1>, so bit-identical to it when phd =
+// phi(m[NH])) and s_hi = sum of the hi edges' phi (the degree-1 edge's
+// output is phi(s_hi), not formed here).
+template <int NH>
+__device__ __forceinline__ void check_magnitudes_d1(const float (&m)[NH + 1], float phd, float (&out)[NH + 1],
+                                                    float clamp, float& s_hi) {
+  constexpr int D = NH + 1;
+  float ph[D];
+  float pre[D];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) ph[j] = dev::phi(m[j]);
+  ph[NH] = phd;
+  pre[1] = ph[0];
+#pragma unroll
+  for (int j = 2; j < D; ++j) pre[j] = pre[j - 1] + ph[j - 1];
+  s_hi = pre[D - 1];
+  float suf = ph[D - 1];
+#pragma unroll
+  for (int j = D - 2; j >= 1; --j) {
+    out[j] = fminf(dev::phi(pre[j] + suf), clamp);
+    suf += ph[j];
+  }
+  out[0] = fminf(dev::phi(suf), clamp);
+}
+
+// Hard decision of a degree-1 variable, post = l + o (o its check's output
+// to it), decided in the phi domain without forming o: |o| = min(phi(s_hi),
+// clamp) against |l| through phd = phi(min(|l|, clamp)) (phi decreasing;
+// phd <= phc = phi(clamp) means |l| >= clamp).  sl / so: sign bits of l and
+// o.  Same decision as (l + o < 0) except where |o| and |l| agree to float
+// rounding (a posterior at zero: a tie).
+__device__ __forceinline__ uint32_t d1_bit_phi(uint32_t sl, uint32_t so, float s_hi, float phd, float phc) {
+  const float kInf = __int_as_float(0x7f800000);
+  if (sl == so) return (phd == kInf && s_hi == kInf) ? 0u : sl;  // same signs: l's sign (0 + 0: +0 or -0, not < 0)
+  const bool l_small = phd > phc;                                 // |l| < clamp
+  if (l_small && s_hi < phd) return so;                           // |o| > |l|
+  if (!l_small || s_hi > phd) return sl;                          // |l| > |o|
+  return 0u;                                                      // |o| == |l|: post = +0
 }
 
 template <int MAXD, bool WANT_POST>
@@ -517,11 +584,21 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
 // costs ~LW/32 of the instructions as well as of the bytes.  The arithmetic
 // of every (check, frame) is that of LW = 32; the 32-bit words (degree-1
 // hard bits, syndrome part) of check kb + qq are bits qq*LW .. of one ballot.
-template <int NH, int ND, bool WANT_POST, bool FM, int LW>
-__device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p,
+//
+// kPhiD (one degree-1 edge and >= 2 hi edges, no posterior output): the
+// degree-1 LLR row holds, after the frame's first iteration, phi(min(|l|,
+// clamp)) with l's sign (written back by the first iteration), so the steady
+// state reads the degree-1 edge's phi instead of computing it and decides
+// the degree-1 hard bit in the phi domain (d1_bit_phi) instead of forming
+// its output: two phi evaluations less per check.  The messages to the hi
+// edges are bit-identical to the plain path.
+template <int NH, int ND, bool WANT_POST, bool FM, int LW, bool PHID>
+__device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p, float* llrg,
                                                     const uint32_t* ssyn, int i0, int lane, bool act, bool first,
-                                                    float cl, float clamp, uint32_t* synw, uint32_t* d1w) {
+                                                    float cl, float clamp, float phc, uint32_t* synw,
+                                                    uint32_t* d1w) {
   constexpr int D = NH + ND;
+  constexpr bool kPhiD = PHID && ND == 1 && NH >= 2 && !WANT_POST;
   // steady-state (1,1) check: the c2v to its degree>=2 variable is
   // (1-2s)*sign(l)*min(|l|, clamp) in every iteration (the degree-1 edge's
   // v2c is clamp(l)), so it is formed from l instead of being re-read (the
@@ -571,14 +648,40 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 #pragma unroll
     for (int j = 0; j < D; ++j) par ^= sm[j];
     float out[D > 0 ? D : 1];
-    check_magnitudes<D>(m, out, clamp);
+    uint32_t dbit = 0u;
+    if constexpr (kPhiD) {
+      // steady lanes: l is the stored phi (sign = l's); first-iteration
+      // lanes (FM copy only): l is the LLR, phi formed here and stored
+      float phd = fabsf(l);
+      float phf = 0.0f;
+      if (FM) {
+        phf = dev::phi(m[NH]);  // unclamped in the first iteration (cl = inf)
+        if (first) phd = phf;
+      }
+      float s_hi;
+      check_magnitudes_d1<NH>(m, phd, out, clamp, s_hi);
+      const uint32_t so = (par ^ sm[NH]) >> 31, sl = sm[NH] >> 31;
+      if (FM) {
+        // first lanes: the plain decision on the LLR, and the phi of the
+        // clamped magnitude written back for the steady state
+        const float o = __uint_as_float(__float_as_uint(fminf(dev::phi(s_hi), clamp)) | (par ^ sm[NH]));
+        const uint32_t fb = (l + o < 0.0f) ? 1u : 0u;
+        dbit = first ? fb : d1_bit_phi(sl, so, s_hi, phd, phc);
+        const float stored = __uint_as_float(__float_as_uint(fabsf(l) > clamp ? phc : phf) | sm[NH]);
+        st_pred(llrg + static_cast<size_t>(i0 + kb) * LW, stored, on && first);
+      } else {
+        dbit = d1_bit_phi(sl, so, s_hi, phd, phc);
+      }
+      dbit = on ? dbit : 0u;
+    } else {
+      check_magnitudes<D>(m, out, clamp);
+    }
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const float o = __uint_as_float(__float_as_uint(out[j]) | (par ^ sm[j]));
       if (!kConstC) stcs_pred(cq + static_cast<size_t>((i0 + kb) * NH + j) * LW, o, on);
     }
-    uint32_t dbit = 0u;
-    if (ND) {
+    if (ND && !kPhiD) {
       const float o = __uint_as_float(__float_as_uint(out[NH]) | (par ^ sm[NH]));
       const float pd = l + o;  // posterior of the degree-1 variable
       dbit = (on && pd < 0.0f) ? 1u : 0u;
@@ -606,7 +709,7 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   }
 }
 
-template <int NH, int ND, bool WANT_POST, bool FM, int RING, int LW = 32>
+template <int NH, int ND, bool WANT_POST, bool FM, int RING, int LW = 32, bool PHID = false>
 __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
@@ -621,8 +724,10 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   const float* llr0 = a.llr_d + rix(g, a.N1, db, LW);
   float* c2vg = a.c2v + rix(g, a.EH, hb, LW) + f;
   float* d1p = WANT_POST ? a.d1post + rix(g, a.N1, db, LW) + f : nullptr;
+  float* llrg = a.llr_d + rix(g, a.N1, db, LW) + f;
   const float clamp = a.clamp;
   const float cl = first ? __int_as_float(0x7f800000) : clamp;
+  const float phc = dev::phi(clamp);
   // this lane's 16-byte piece: frames lcol .. lcol+3 of row lrow of a row group
   constexpr int QPR = LW / 4;  // 16-byte pieces per row
   const int lrow = lane / QPR;
@@ -653,8 +758,8 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
     if (++slot_i == NS) slot_i = 0;
     cp_async_wait<NS - 1>();
     __syncwarp();  // rows were copied by other lanes
-    check_batch_compute<NH, ND, WANT_POST, FM, LW>(ring + slot_c * RS, c2vg, d1p, ssyn, b * K, lane, act, first, cl,
-                                                   clamp, synw, d1w);
+    check_batch_compute<NH, ND, WANT_POST, FM, LW, PHID>(ring + slot_c * RS, c2vg, d1p, llrg, ssyn, b * K, lane, act, first,
+                                                   cl, clamp, phc, synw, d1w);
     if (++slot_c == NS) slot_c = 0;
     __syncwarp();  // stage is refilled in the next round
   }
@@ -669,15 +774,17 @@ template <int NH, int ND, bool WANT_POST, bool SPLIT_FM, int RING, int LW>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
                                                   const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
                                                   uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
+  // the phi-domain degree-1 edge needs the steady-state copy (the general
+  // copy would evaluate both forms: measured slower)
   if constexpr (LW < 32)
-    check_chunk_loop<NH, ND, WANT_POST, false, RING, LW>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, 0u,
-                                                         synw, d1w);
+    check_chunk_loop<NH, ND, WANT_POST, false, RING, LW, SPLIT_FM>(a, g, hb, db, hh, ssyn, ring, lane, act, first,
+                                                                   amask, 0u, synw, d1w);
   else if (!SPLIT_FM || fmask)
-    check_chunk_loop<NH, ND, WANT_POST, true, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask, synw,
-                                                    d1w);
+    check_chunk_loop<NH, ND, WANT_POST, true, RING, 32, SPLIT_FM>(a, g, hb, db, hh, ssyn, ring, lane, act, first,
+                                                                  amask, fmask, synw, d1w);
   else
-    check_chunk_loop<NH, ND, WANT_POST, false, RING>(a, g, hb, db, hh, ssyn, ring, lane, act, first, amask, fmask,
-                                                     synw, d1w);
+    check_chunk_loop<NH, ND, WANT_POST, false, RING, 32, SPLIT_FM>(a, g, hb, db, hh, ssyn, ring, lane, act, first,
+                                                                   amask, fmask, synw, d1w);
 }
 
 template <int MAXD>
@@ -707,10 +814,23 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
   const bool moved = __ldcg(&a.counters[12]) != 0;
   const int chunks = (a.M + 31) / 32;
   const long long total = static_cast<long long>(a.G) * chunks;
-  // dynamic chunk schedule (counters[7], generic chunks first), one grab ahead
-  long long w = sched_resolve(a, sched_issue(a, 7, lane), lane, chunks, a.csched);
+  // dynamic chunk schedule (counters[7], generic chunks first): a grab is
+  // kCheckGrab consecutive chunks (one atomic per kCheckGrab chunks: at one
+  // per chunk the counter's atomics queued in L2 and their latency showed
+  // as stalls), the next grab in flight while the current one is processed
+  int kbase = __shfl_sync(0xffffffffu, sched_issue_n(a, 7, lane, kCheckGrab), 0);
+  int kpend = sched_issue_n(a, 7, lane, kCheckGrab);
+  int sub = 0;
+  auto next_chunk = [&]() {
+    if (++sub == kCheckGrab) {
+      sub = 0;
+      kbase = __shfl_sync(0xffffffffu, kpend, 0);
+      kpend = sched_issue_n(a, 7, lane, kCheckGrab);
+    }
+    return sched_map(a, kbase + sub, lane, chunks, a.csched);
+  };
+  long long w = sched_map(a, kbase, lane, chunks, a.csched);
   while (w < total) {
-    const int kpend = sched_issue(a, 7, lane);
     const int g = static_cast<int>(w / chunks);
     const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
     const int c0 = ch * 32;
@@ -725,7 +845,7 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
     // degree-1 checks only change in a frame's first iteration (and their
     // bit words must follow frames that k_compact moved)
     if ((type == 1 || type == 8) && fmask == 0u && !moved) {
-      w = sched_resolve(a, kpend, lane, chunks, a.csched);
+      w = next_chunk();
       continue;
     }
     __syncwarp();
@@ -748,7 +868,7 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
 #define BPDEC_TYPED(NH_, ND_)                                                                       \
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
-      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= 4), kRing, LW>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], \
+      check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= kSplitMaxD), kRing, LW>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], \
                                              lane, act, first, amask, fmask, &synw, &d1w);          \
     else                                                                                            \
       typed = false;                                                                                \
@@ -792,12 +912,12 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
       }
     }
     if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = synw;
-    w = sched_resolve(a, kpend, lane, chunks, a.csched);
+    w = next_chunk();
   }
 }
 
 template <int MAXD, bool WANT_POST>
-__global__ void __launch_bounds__(kCheckThreads, 5) k_check(const Args a) {  // 5 blocks/SM, 96 regs: measured best
+__global__ void __launch_bounds__(kCheckThreads, kCheckMinBlocks) k_check(const Args a) {  // 5 blocks/SM, 96 regs: measured best
   pdl_begin();
   __shared__ CheckSmem<MAXD> sm;
   if (blockIdx.x == 0) {

@@ -38,14 +38,14 @@ def met2(N, R, f1, d1, p1, k2, seed):
 designs = [
     # name, f1, d1 degrees, probs, k2
     ("A_f.85_k3", 0.85, [2, 3], [0.5, 0.5], 3),
-    ("B_f.8375_k3", 0.8375, [2, 3], [0.5, 0.5], 3),
-    ("C_f.875_k3", 0.875, [2, 3], [0.6, 0.4], 3),
-    ("D_f.85_k2", 0.85, [2, 3], [0.5, 0.5], 2),
-    ("E_f.8_k3", 0.8, [3], [1.0], 3),
+    ("G_f.733_k3", 0.7333, [2, 3], [0.5, 0.5], 3),
+    ("H_f.75_d2_k3", 0.75, [2], [1.0], 3),
+    ("I_f.70_k2", 0.70, [2, 3], [0.5, 0.5], 2),
+    ("J_f.80_k3_d2", 0.80, [2], [1.0], 3),
 ]
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 16
 F = 64
-betas = [0.5, 0.6, 0.7, 0.75, 0.8, 0.85, 0.9, 0.93, 0.96]
+betas = [0.6, 0.7, 0.75, 0.8, 0.85, 0.9]
 for name, f1, d1, p1, k2 in designs:
     code = met2(N, 0.1, f1, d1, p1, k2, 7)
     dec = P.BatchDecoder(code, max_slots=64)
