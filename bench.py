@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=None)
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period during the timed region")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
-    ap.add_argument("--mode", choices=["stream", "batch"], default="batch",
+    ap.add_argument("--mode", choices=["stream", "batch"], default="stream",
                     help="stream: the K batches go through bpdec_stream_* back to back (a batch's tail lanes are "
                          "refilled with the next batch's frames); batch: one blocking bpdec_decode_batch per step")
     ap.add_argument("--multi", action="store_true",
@@ -425,7 +425,8 @@ def traffic_probe(args):
     w = P.WORKLOADS[args.workload]
     code = w.make_code()
     F = args.frames or FRAMES[args.workload]
-    dec = P.BatchDecoder(code, device=0, max_slots=args.slots or min(F, 512))
+    dec = P.BatchDecoder(code, device=0, max_slots=args.slots or
+                         (min(4 * F, 1024) if args.mode == "stream" else min(F, 512)))
     d_llr, d_syn, _ = make_frames(P, dec, code, args, F, 0, 0)
     torch.cuda.synchronize()
     cfg = P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS)
@@ -436,7 +437,7 @@ def traffic_probe(args):
         outs = [{"iterations": torch.zeros(F, dtype=torch.int32, device="cuda"),
                  "reasons": torch.zeros(F, dtype=torch.uint8, device="cuda"),
                  "bits": torch.zeros((F, (code.n_vars + 31) // 32), dtype=torch.int32, device="cuda")}
-                for _ in range(2)]
+                for _ in range(8)]  # enough batches for the stream's steady state
         for t in [dec.stream_submit(d_llr, d_syn, out=o) for o in outs]:
             dec.stream_wait(t)
         dec.stream_close()
@@ -505,7 +506,9 @@ def run_ours(args):
     w = P.WORKLOADS[args.workload]
     code = w.make_code()
     F = args.frames or FRAMES[args.workload]
-    slots = args.slots or min(F, 512)
+    # stream mode keeps four batches' worth of slots in flight: a batch's
+    # tail shares the steps with the next batches' frames
+    slots = args.slots or (min(4 * F, 1024) if args.mode == "stream" else min(F, 512))
     beta, brange = workload_beta(args)
     dec = P.BatchDecoder(code, device=local, max_slots=slots)
     # weak scaling: rank r owns global frames [r*F, (r+1)*F)
@@ -549,7 +552,7 @@ def run_ours(args):
     t_warm = time.perf_counter()
     n_warm = 0
     if use_stream:
-        dec.stream_open(cfg, packed=True, ring_frames=4 * max(F, dec.slots))
+        dec.stream_open(cfg, packed=True, ring_frames=2 * max(F, dec.slots))
         while n_warm < args.warmup or time.perf_counter() - t_warm < 1.5:
             stream_run(args.warmup, lambda k: d_llr, lambda k: d_syn, souts)
             n_warm += args.warmup
@@ -593,7 +596,7 @@ def run_ours(args):
     # host work per launch)
     if use_stream:
         dec.stream_close()
-        dec.stream_open(cfg, packed=True, ring_frames=4 * max(F, dec.slots))  # frame-iteration counter from 0
+        dec.stream_open(cfg, packed=True, ring_frames=2 * max(F, dec.slots))  # frame-iteration counter from 0
     dec.reset_profile()
     dec.set_profiling(True)
     if use_stream:
@@ -656,7 +659,7 @@ def run_ours(args):
     pipelining = None
     if use_stream:
         h_outs = [host_out() for _ in range(K)]
-        dec.stream_open(cfg, packed=True, ring_frames=4 * max(F, dec.slots))
+        dec.stream_open(cfg, packed=True, ring_frames=2 * max(F, dec.slots))
         stream_run(min(K, 4), lambda k: h_llr[k % 2], lambda k: h_syn[k % 2], h_outs)  # warm
         for _rep in range(3):
             barrier(dist)
@@ -717,7 +720,7 @@ def run_ours(args):
                  "value": sum_over_ranks(float(bi), dist) * code.n_edges / tb, "ms_per_step": 1e3 * tb / K}
     else:
         souts = [dev_out() for _ in range(K)]
-        dec.stream_open(cfg, packed=True, ring_frames=4 * max(F, dec.slots))
+        dec.stream_open(cfg, packed=True, ring_frames=2 * max(F, dec.slots))
         stream_run(min(K, 4), lambda k: d_llr, lambda k: d_syn, souts)
         dec.stream_timer_reset()
         si = stream_run(K, lambda k: d_llr, lambda k: d_syn, souts)

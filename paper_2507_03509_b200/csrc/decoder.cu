@@ -153,6 +153,8 @@ struct Args {
   int32_t batch, d_max, use_pce, use_vnr, q_mode;
   float clamp;
   int32_t narrow_ok;          // the tail group may be re-laid out narrow (check degree <= 4, G >= 2)
+  int32_t group_refill;       // stream mode: refill only groups that are entirely free (dense loads)
+                              // and compact while frames are queued, so no step refills single lanes
   // inputs / outputs (device)
   const float* in_llr;        // [batch][N]
   const uint32_t* in_syn;     // [batch][MW] or null
@@ -1628,8 +1630,12 @@ __device__ __forceinline__ void decide_group(const Args& a, int g, int lane) {
     atomicSub(&a.counters[3], nstop);
   }
   // refill: every lane that is not active (this step's stops and lanes left
-  // free earlier) takes the next available queued frame, in lane order
-  const uint32_t load = refill_lanes(a, g, ~(amask & ~stop), lane);
+  // free earlier) takes the next available queued frame, in lane order --
+  // or, with group_refill, only a group whose every lane is free (a refill
+  // rewrites every row of the group: one dense load of up to 32 frames
+  // instead of a partial-line pass per few frames; k_compact frees groups)
+  const uint32_t left = amask & ~stop;
+  const uint32_t load = refill_lanes(a, g, (a.group_refill && left != 0u) ? 0u : ~left, lane);
   if (lane == 0) {
     a.stopped[g] = stop;
     a.load_mask[g] = load;
@@ -2077,8 +2083,11 @@ __device__ void compact_plan(const Args& a, CompactPlan& pl, int* cnt) {
   const int G = a.G;
   if (G > kMaxCompactGroups || G < 2) return;
   // frames still queued: freed slots get refilled instead (stream mode: the
-  // frames submitted so far)
-  if (a.counters[0] < (a.ring_cap ? *reinterpret_cast<volatile int32_t*>(&a.counters[9]) : a.batch)) return;
+  // frames submitted so far) -- except with group_refill, where compaction
+  // is what frees whole groups for the queued frames
+  if (!a.group_refill &&
+      a.counters[0] < (a.ring_cap ? *reinterpret_cast<volatile int32_t*>(&a.counters[9]) : a.batch))
+    return;
   int total = 0, alive = 0;
   for (int g = 0; g < G; ++g) {
     cnt[g] = __popc(a.group_active[g]);
@@ -3390,6 +3399,7 @@ void GpuDecoder::stream_open(const DecodeParams& p, bool packed, bool want_bits,
   a.q_mode = p.q_mode;
   a.clamp = p.msg_clamp;
   a.narrow_ok = 0;  // a narrow tail group cannot take refills
+  a.group_refill = (G >= 2 && std::getenv("BPDEC_LANE_REFILL") == nullptr) ? 1 : 0;
   a.in_llr = z.r_llr;
   a.in_syn = z.r_syn;
   a.out_bits_u8 = (want_bits && !packed) ? static_cast<uint8_t*>(z.r_bits) : nullptr;

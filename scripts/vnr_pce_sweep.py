@@ -25,6 +25,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2507_03509_b200 as P  # noqa: E402
+from paper_2507_03509_b200 import qkd  # noqa: E402
 from paper_2507_03509_b200.decoder import Q_ABS  # noqa: E402
 
 BETAS = [0.10, 0.20, 0.30, 0.40, 0.50, 0.70, 0.80, 0.90, 0.92, 0.94, 0.96, 0.98, 0.99]
@@ -141,6 +142,19 @@ def main():
             if name.startswith("pce") and row[name]["fer"] < 1.0:
                 row[f"k_vnr_over_k_{name}"] = (row[name]["d_bar"] / row["vnr"]["d_bar"]) * \
                     (1.0 - row["vnr"]["fer"]) / (1.0 - row[name]["fer"])
+        # Eq. (1)-(3) at the paper's operating point (V_A such that I_AB =
+        # R / beta; 80 km, eta 0.4, nu_el 0.01, xi 0.001, heterodyne,
+        # N_privacy 1e8): SKR per pulse, K and SKR_dec per iteration latency,
+        # and SKR_dec in bits/s with the measured decode time
+        if brange is None:
+            for name, _ in pols:
+                r = row[name]
+                b = qkd.evaluate(code.rate(), beta, r["fer"], N, max(r["d_bar"], 1.0))
+                r["skr_bits_per_pulse"] = b.skr
+                r["k_eq2"] = b.k_throughput
+                r["skr_dec_eq3"] = b.skr_dec
+                r["skr_dec_bits_per_s"] = b.skr * (r["frames"] * N / 2.0) / r["seconds"]
+                r["skr_negative"] = b.negative
         rows.append(row)
         print(json.dumps({"point": beta if brange is None else list(brange),
                           **{f"d_{k}": row[k]["d_bar"] for k, _ in pols},
@@ -149,7 +163,16 @@ def main():
                           **{k: v for k, v in row.items() if k.startswith("k_vnr")},
                           "gain_it": row["iteration_gain"], "gain_frames": row["frame_throughput_gain"]}),
               flush=True)
-    res = {"workload": w.name, "code": {"N": N, "M": M, "E": E, "rate": code.rate()}, "d_max": w.d_max,
+    beta_opt = {}
+    if not mixed:
+        for name, _ in pols:
+            recs = [qkd.SweepRecord(r["beta"], r[name]["skr_bits_per_pulse"], r[name]["skr_dec_eq3"]) for r in rows]
+            bs, bd = qkd.optimize_beta(recs)
+            beta_opt[name] = {"skr": bs, "skr_dec": bd}
+        print(json.dumps({"beta_opt": beta_opt}), flush=True)
+    res = {"workload": w.name, "beta_opt": beta_opt,
+           "qkd_params": "paper simulation point: 80 km, 0.2 dB/km, eta 0.4, nu_el 0.01, xi 0.001, heterodyne, "
+                         "N_privacy 1e8, V_A such that I_AB = R / beta (paper_2507_03509_b200/qkd.py)", "code": {"N": N, "M": M, "E": E, "rate": code.rate()}, "d_max": w.d_max,
            "q_mode": "abs", "data": "synthetic (seeded generator, device-generated syndrome-mode frames)",
            "gpu": torch.cuda.get_device_name(0), "rows": rows}
     with open(out_path, "w") as f:

@@ -162,3 +162,53 @@ def test_syndrome_packing(cfg1_code):
         bad[0] ^= 1
         assert not P.syndrome_check(cfg1_code, x[f], bad)
     assert np.array_equal(P.unpack_bits(P.pack_bits(x), cfg1_code.n_vars), x)
+
+
+@pytest.mark.parametrize("n,rate,f1,degs,probs,k2", [
+    (8192, 0.1, 0.70, (2, 3), (0.5, 0.5), 2),
+    (8192, 0.1, 0.85, (2, 3), (0.5, 0.5), 3),
+    (20000, 0.02, 0.90, (3,), (1.0,), 3),
+])
+def test_met_core_generator_structure(n, rate, f1, degs, probs, k2):
+    """generate_met_core (csrc/code.cpp): degree-1 variables nc.. on the
+    extension checks (one each, identity), every extension check holds
+    exactly k2 core variables, core checks hold only core variables, core
+    type-1 degree classes in proportion, type-2 degrees within 1 of each
+    other, no duplicate edges, deterministic for a seed."""
+    m = int(n * (1 - rate) + 0.5)
+    n1 = int(f1 * n + 0.5)
+    nc, mc = n - n1, m - n1
+    code = P.generate_met_core(n, m, n1, degs, probs, k2, 99)
+    ptr, var = code.csr()
+    assert (code.n_vars, code.n_checks) == (n, m)
+    vdeg = code.var_degrees()
+    assert np.all(vdeg[nc:] == 1)
+    t1 = np.zeros(nc, dtype=np.int64)
+    t2 = np.zeros(nc, dtype=np.int64)
+    for c in range(m):
+        vs = var[ptr[c]:ptr[c + 1]]
+        assert len(set(vs.tolist())) == len(vs)
+        if c < mc:
+            assert np.all(vs < nc)
+            np.add.at(t1, vs, 1)
+        else:
+            core = vs[vs < nc]
+            assert len(core) == k2 and vs[-1] == nc + (c - mc) and len(vs) == k2 + 1
+            np.add.at(t2, core, 1)
+    counts = np.bincount(t1, minlength=max(degs) + 1)
+    for d, p in zip(degs[:-1], probs[:-1]):
+        assert counts[d] == int(np.floor(nc * p + 0.5))
+    assert t2.max() - t2.min() <= 1
+    again = P.generate_met_core(n, m, n1, degs, probs, k2, 99)
+    assert np.array_equal(again.csr()[1], var) and np.array_equal(again.csr()[0], ptr)
+    other = P.generate_met_core(n, m, n1, degs, probs, k2, 100)
+    assert not np.array_equal(other.csr()[1], var)
+
+
+def test_met_core_generator_errors():
+    with pytest.raises(P.ValidationError):
+        P.generate_met_core(100, 90, 95, (2,), (1.0,), 2, 1)     # n_deg1 >= n_checks
+    with pytest.raises(P.ValidationError):
+        P.generate_met_core(100, 90, 50, (2, 3), (1.0,), 2, 1)   # misaligned classes
+    with pytest.raises(P.ValidationError):
+        P.generate_met_core(100, 90, 50, (2,), (1.0,), 0, 1)     # ext_degree 0
