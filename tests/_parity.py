@@ -64,11 +64,15 @@ def _q_gap_ties(a, kw):
     return tie
 
 
-def ref_ties(refc, llr32, **kw):
+def ref_ties(refc, llr32, chaotic_is_tie=True, **kw):
     """Runs the reference on the inputs and on their +-1 ulp neighbours.
     Returns (reference outputs with 'drift' per frame, tie mask).  Frames
     already tied by the q-gap rule skip the perturbed runs (their verdict
-    cannot change), which keeps full-size VNR configurations affordable."""
+    cannot change), which keeps full-size VNR configurations affordable.
+    chaotic_is_tie=False keeps rule-3 frames (outcome stable under the
+    perturbations, posteriors not) in the comparison: their bits,
+    iterations and reason are compared exactly and their posteriors at
+    DRIFT_FACTOR x the measured drift (compare with strict=False)."""
     a = refc.decode_batch(llr32.astype(np.float64), want_posteriors=True, **kw)
     B = len(a["iterations"])
     tie = _q_gap_ties(a, kw)
@@ -87,7 +91,7 @@ def ref_ties(refc, llr32, **kw):
                           a["reasons"][f] != o["reasons"][j])
             if not t:
                 drift[f] = _norm_err(b["posteriors"][j], a["posteriors"][f])
-                t = drift[f] > 1.0  # chaotic frame (rule 3)
+                t = chaotic_is_tie and drift[f] > 1.0  # chaotic frame (rule 3)
             tie[f] = t
     a["drift"] = drift
     return a, tie
