@@ -420,12 +420,16 @@ __device__ __forceinline__ void check_magnitudes_d1(const float (&m)[NH + 1], fl
 // o.  Same decision as (l + o < 0) except where |o| and |l| agree to float
 // rounding (a posterior at zero: a tie).
 __device__ __forceinline__ uint32_t d1_bit_phi(uint32_t sl, uint32_t so, float s_hi, float phd, float phc) {
+  // branch-free (selects only: the branchy form compiled to divergent
+  // branches and a convergence check before every ballot)
   const float kInf = __int_as_float(0x7f800000);
-  if (sl == so) return (phd == kInf && s_hi == kInf) ? 0u : sl;  // same signs: l's sign (0 + 0: +0 or -0, not < 0)
-  const bool l_small = phd > phc;                                 // |l| < clamp
-  if (l_small && s_hi < phd) return so;                           // |o| > |l|
-  if (!l_small || s_hi > phd) return sl;                          // |l| > |o|
-  return 0u;                                                      // |o| == |l|: post = +0
+  const bool zero = (phd == kInf) & (s_hi == kInf);  // l = 0 and o = 0: +0 or -0, not < 0
+  const bool l_small = phd > phc;                    // |l| < clamp
+  const bool o_big = l_small & (s_hi < phd);         // |o| > |l|
+  const bool l_big = !l_small | (s_hi > phd);        // |l| > |o|  (neither: equal, post = +0)
+  const uint32_t diff = o_big ? so : (l_big ? sl : 0u);
+  const uint32_t same = zero ? 0u : sl;
+  return sl == so ? same : diff;
 }
 
 template <int MAXD, bool WANT_POST>
