@@ -83,13 +83,14 @@ enum KernelId { kCheck = 0, kVar = 1, kSyn = 2, kTerm = 3, kTurnover = 4, kCompa
 #define BPDEC_CHECK_MINB 5
 #endif
 #ifndef BPDEC_SPLIT_MAXD
-#define BPDEC_SPLIT_MAXD 4
+#define BPDEC_SPLIT_MAXD 6
 #endif
 constexpr int kCheckMinBlocks = BPDEC_CHECK_MINB;  // k_check blocks per SM (register budget)
 // k_check kernels (by maximum check degree) with a separate steady-state
 // copy of every typed chunk loop, which also uses the phi-domain degree-1
 // edge (kPhiD in check_batch_compute); wider kernels keep one copy
-// (instruction cache; splitting k_check<8> measured -2% on a (3,1) code)
+// (instruction cache; splitting k_check<8> measured -2% on a (3,1) code,
+// splitting k_check<6> +6.7% on the rate-0.1 QC lift of scripts/qc_probe.py)
 constexpr int kSplitMaxD = BPDEC_SPLIT_MAXD;
 constexpr int kCheckGrab = 1;     // k_check chunks per scheduler atomic (2: -9% on cfg2, the two
                                   // chunks of a grab run back to back on one warp instead of side by side)
@@ -899,12 +900,15 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
     if (typed) {
       if ((type & 7) != 0) a.d1bits[static_cast<size_t>(g) * a.N1 + db0 + lane] = d1w;
     } else {
-      for (int j = 0; j < nc; j += 2) {
+      // two checks in flight per step in k_check<3>; one in the wider
+      // kernels (two states of MAXD >= 4 messages spill)
+      constexpr int kGenPair = MAXD <= 3 ? 2 : 1;
+      for (int j = 0; j < nc; j += kGenPair) {
         CheckState<MAXD> A, B;
         const int4 dA = s_desc[wi][j];
         check_load<MAXD>(a, A, g, dA, s_syn[wi][j], kStage ? &s_hh[wi][dA.x - hb0] : &a.chk_hi_h[dA.x], lane, act,
                          first, LW);
-        const bool hasB = j + 1 < nc;
+        const bool hasB = kGenPair == 2 && j + 1 < nc;
         if (hasB) {
           const int4 dB = s_desc[wi][j + 1];
           check_load<MAXD>(a, B, g, dB, s_syn[wi][j + 1], kStage ? &s_hh[wi][dB.x - hb0] : &a.chk_hi_h[dB.x], lane,
@@ -924,7 +928,8 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
 }
 
 template <int MAXD, bool WANT_POST>
-__global__ void __launch_bounds__(kCheckThreads, kCheckMinBlocks) k_check(const Args a) {  // 5 blocks/SM, 96 regs: measured best
+__global__ void __launch_bounds__(kCheckThreads, MAXD >= 16 ? kCheckMinBlocks - 1 : kCheckMinBlocks)
+    k_check(const Args a) {  // the degree-16 / generic kernels: 4 blocks (128 registers, no spills)  // 5 blocks/SM, 96 regs: measured best
   pdl_begin();
   __shared__ CheckSmem<MAXD> sm;
   if (blockIdx.x == 0) {
