@@ -2,9 +2,9 @@
 """Summarise an ncu report (and optional launch-list CSV) into profiles/.
 
 Usage: python scripts/ncu_summary.py <prof.ncu-rep> <tag> [launches.csv]
-Writes profiles/<tag>_ncu.md, profiles/<tag>_ncu.json and, for the check
-kernel, profiles/check_kernel_dram_bytes.json (read by bench.py as the
-roofline `traffic`).  Run here (no GPU needed): ncu -i reads the report.
+Writes profiles/<tag>_ncu.md and profiles/<tag>_ncu.json (tag may contain a
+directory, e.g. r2/cfg2_stream).  Run here (no GPU needed): ncu -i reads the
+report.  bench.py measures the check kernel's traffic itself (live ncu probe).
 """
 import csv
 import io
@@ -57,7 +57,7 @@ def main():
     rep, tag = sys.argv[1], sys.argv[2]
     launches = sys.argv[3] if len(sys.argv) > 3 else None
     res = raw(rep)
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    os.makedirs(os.path.dirname(os.path.join(ROOT, "profiles", f"{tag}_ncu.json")), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu.json"), "w") as f:
         json.dump(res, f, indent=1)
     lines = [f"# ncu summary `{tag}`", "", f"source report: `{os.path.basename(rep)}` (ncu --set full --clock-control none)", ""]
@@ -75,11 +75,6 @@ def main():
                      f"{d.get('lts__t_sector_hit_rate.pct', {}).get('value')} | "
                      f"{d.get('launch__registers_per_thread', {}).get('value')} | "
                      f"{', '.join(f'{n} {v}' for n, v in d['top_stalls'][:3])} |")
-        if "k_check" in k:
-            with open(os.path.join(ROOT, "profiles", "check_kernel_dram_bytes.json"), "w") as f:
-                json.dump({"workload": "cfg2_r0.1_n2^20", "frames": 64, "tag": tag,
-                           "dram_bytes_per_launch": rb, "kernel": k,
-                           "note": "one k_check launch = one iteration of 64 frames (ncu --set full)"}, f, indent=1)
     if launches and os.path.exists(launches):
         lines += ["", "## launch list (`--metrics gpu__time_duration.sum`, cold-cache, serialised)", ""]
         with open(launches) as f:
