@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <deque>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -94,51 +96,94 @@ TrialStats run_trials(GpuDecoder* dec, int32_t n_vars, int32_t n_checks, double 
   HCUDA_OK(dg.status());
   const int32_t nw = (n_vars + 31) / 32;
   const size_t B = static_cast<size_t>(block);
-  DevBuf<float> d_llr(B * n_vars);
-  DevBuf<uint32_t> d_bits(B * nw);
-  DevBuf<int32_t> d_iters(B);
-  DevBuf<uint8_t> d_reasons(B);
+  // Pipelined: up to kDepth blocks in flight through the decoder's stream
+  // mode (generation + puncturing of block k+1 on a side stream while block
+  // k decodes; a block's slow frames share their steps with the next
+  // block's), folded strictly in trial order on the host.
+  constexpr int kDepth = 3;
+  struct Slot {
+    DevBuf<float> llr;
+    DevBuf<uint32_t> bits;
+    DevBuf<int32_t> iters;
+    DevBuf<uint8_t> reasons;
+    explicit Slot(size_t b, int32_t n, int32_t w) : llr(b * n), bits(b * w), iters(b), reasons(b) {}
+  };
+  std::vector<std::unique_ptr<Slot>> slots;
+  for (int k = 0; k < kDepth; ++k) slots.emplace_back(new Slot(B, n_vars, nw));
   DevBuf<uint32_t> d_flag(B);
   DevBuf<int32_t> d_punct(punctured.size());
   if (!punctured.empty()) {
     HCUDA_OK(cudaMemcpy(d_punct.p, punctured.data(), punctured.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
+  cudaStream_t gs = nullptr;
+  HCUDA_OK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+  struct StreamGuard {  // closes the decoder's stream (and the side stream) on every exit
+    GpuDecoder* dec;
+    cudaStream_t gs;
+    bool open = false;
+    ~StreamGuard() {
+      if (open) {
+        try {
+          gpu_stream_close(dec);
+        } catch (...) {
+        }
+      }
+      cudaStreamDestroy(gs);
+    }
+  } guard{dec, gs};
+  gpu_stream_open(dec, p, /*packed=*/true, /*want_bits=*/true, /*want_post=*/false, /*want_q=*/false,
+                  static_cast<int32_t>(kDepth * B));
+  guard.open = true;
   std::vector<int32_t> it(B);
   std::vector<uint8_t> rs(B);
   std::vector<uint32_t> nz(B);
 
   TrialStats st;
   st.histogram.assign(static_cast<size_t>(p.d_max) + 1, 0);
-  int64_t next = 0;
-  bool done = false;
-  while (!done) {
+  struct InFlight {
+    int64_t ticket;
+    int32_t nb;
+    int slot;
+  };
+  std::deque<InFlight> inflight;
+  int64_t next = 0, folded = 0;
+  bool exhausted = false, done = false;
+  auto submit = [&](int slot) {
     int64_t bs = block;
     if (max_frames > 0) bs = std::min<int64_t>(bs, max_frames - next);
     if (bs <= 0) {
-      st.hit_max_frames = true;
-      break;
+      exhausted = true;
+      return;
     }
     const int32_t nb = static_cast<int32_t>(bs);
-    gpu_sample_frames_device(dec, snr, 0.0, 0.0, 0.0, seed, next, nb, /*all_zero=*/true, d_llr.p, nullptr, nullptr,
-                             nullptr);
+    Slot& sl = *slots[slot];
+    gpu_sample_frames_device(dec, snr, 0.0, 0.0, 0.0, seed, next, nb, /*all_zero=*/true, sl.llr.p, nullptr, nullptr,
+                             gs);
     if (!punctured.empty()) {
-      k_puncture<<<256, 256>>>(d_llr.p, n_vars, nb, d_punct.p, static_cast<int32_t>(punctured.size()));
+      k_puncture<<<256, 256, 0, gs>>>(sl.llr.p, n_vars, nb, d_punct.p, static_cast<int32_t>(punctured.size()));
       HCUDA_OK(cudaGetLastError());
-      HCUDA_OK(cudaDeviceSynchronize());
+      HCUDA_OK(cudaStreamSynchronize(gs));
     }
-    DecodeBuffers b;
-    b.batch = nb;
-    b.llr = d_llr.p;
-    b.bits_packed = true;
-    b.bits = d_bits.p;
-    b.iterations = d_iters.p;
-    b.reasons = d_reasons.p;
-    gpu_decode_batch(dec, p, b, nullptr);
-    k_any_bit<<<nb, 256>>>(d_bits.p, nw, nb, d_flag.p);
+    StreamOutputs o;
+    o.bits = sl.bits.p;
+    o.iterations = sl.iters.p;
+    o.reasons = sl.reasons.p;
+    inflight.push_back({gpu_stream_submit(dec, nb, sl.llr.p, nullptr, o), nb, slot});
+    next += nb;
+  };
+  for (int k = 0; k < kDepth && !exhausted; ++k) submit(k);
+  while (!inflight.empty() && !done) {
+    const InFlight f = inflight.front();
+    inflight.pop_front();
+    gpu_stream_wait(dec, f.ticket);
+    const Slot& sl = *slots[f.slot];
+    const int32_t nb = f.nb;
+    k_any_bit<<<nb, 256, 0, gs>>>(sl.bits.p, nw, nb, d_flag.p);
     HCUDA_OK(cudaGetLastError());
-    HCUDA_OK(cudaMemcpy(it.data(), d_iters.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    HCUDA_OK(cudaMemcpy(rs.data(), d_reasons.p, nb, cudaMemcpyDeviceToHost));
-    HCUDA_OK(cudaMemcpy(nz.data(), d_flag.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    HCUDA_OK(cudaMemcpyAsync(it.data(), sl.iters.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, gs));
+    HCUDA_OK(cudaMemcpyAsync(rs.data(), sl.reasons.p, nb, cudaMemcpyDeviceToHost, gs));
+    HCUDA_OK(cudaMemcpyAsync(nz.data(), d_flag.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, gs));
+    HCUDA_OK(cudaStreamSynchronize(gs));
     // fold in trial order; the error target truncates exactly where a serial
     // run would have stopped (channel.cpp:133-147)
     for (int32_t t = 0; t < nb; ++t) {
@@ -156,12 +201,17 @@ TrialStats run_trials(GpuDecoder* dec, int32_t n_vars, int32_t n_checks, double 
         break;
       }
     }
-    next += nb;
-    if (!done && max_frames > 0 && next >= max_frames) {
+    folded += nb;
+    if (!done && max_frames > 0 && folded >= max_frames) {
       st.hit_max_frames = true;
       done = true;
     }
+    if (!done && !exhausted) submit(f.slot);  // the folded block's buffers take the next block
   }
+  // blocks still in flight past the stop are discarded (gpu_stream_close
+  // waits for them)
+  guard.open = false;
+  gpu_stream_close(dec);
   st.fer = static_cast<double>(st.frame_errors) / static_cast<double>(st.frames);
   const auto ci = wilson_interval(st.frame_errors, st.frames);
   st.fer_ci_low = ci.first;

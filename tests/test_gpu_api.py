@@ -68,6 +68,31 @@ def test_stream_batches_equal_blocking_decode(P, cfg1_code):
     _same(whole, dec.decode_batch(llr[:20], cfg, syndrome=s[:20], want_posteriors=True, want_q_trace=True), 0, 20)
 
 
+def test_stream_group_refill_equals_lane_refill(P, cfg1_code, monkeypatch):
+    """Stream mode refills whole groups and compacts while frames are queued
+    (default) or refills single lanes (BPDEC_LANE_REFILL=1): 600 frames in
+    batches of 40 through 256 slots (8 groups) give, per frame, exactly the
+    blocking decode's outputs either way (frames move between groups many
+    times)."""
+    code = cfg1_code
+    llr, x, s = _frames(P, code, 0.95, 600, seed=21)
+    cfg = P.DecodeConfig(d_max=200, use_pce=True, use_vnr=True, q_mode=P.decoder.Q_ABS)
+    dec = P.BatchDecoder(code, max_slots=256)
+    whole = dec.decode_batch(llr, cfg, syndrome=s, want_posteriors=True, want_q_trace=True)
+    for lane_refill in (False, True):
+        if lane_refill:
+            monkeypatch.setenv("BPDEC_LANE_REFILL", "1")
+        else:
+            monkeypatch.delenv("BPDEC_LANE_REFILL", raising=False)
+        dec.stream_open(cfg, want_posteriors=True, want_q_trace=True, ring_frames=512)
+        try:
+            tickets = [(lo, dec.stream_submit(llr[lo:lo + 40], s[lo:lo + 40])) for lo in range(0, 600, 40)]
+            for lo, t in tickets:
+                _same(whole, dec.stream_wait(t), lo, lo + 40)
+        finally:
+            dec.stream_close()
+
+
 def test_stream_device_inputs_packed_and_error_isolation(P, cfg1_code):
     """Device-resident inputs / outputs, packed bits, all-zero syndrome
     (None); a batch with a non-finite LLR fails alone (ValidationError on its
