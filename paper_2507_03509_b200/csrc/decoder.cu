@@ -696,12 +696,14 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
       if (WANT_POST) st_pred(dq + static_cast<size_t>(i0 + kb) * LW, pd, on);
     }
     if constexpr (LW == 32) {
+      // the syndrome word is the target word xor the degree-1 word (a
+      // ballot is linear over xor): one ballot per check, not two
+      uint32_t dw = 0u;
       if (ND) {
-        const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
+        dw = __ballot_sync(0xffffffffu, dbit);
         if (lane == ci) *d1w = dw;
       }
-      const uint32_t sw = __ballot_sync(0xffffffffu, sbit ^ dbit);
-      if (lane == ci) *synw = sw;
+      if (lane == ci) *synw = ssyn[ci] ^ dw;
     } else {
       constexpr uint32_t kMask = (1u << LW) - 1u;
       const uint32_t bd = ND ? __ballot_sync(0xffffffffu, dbit) : 0u;
