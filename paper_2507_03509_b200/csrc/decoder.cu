@@ -845,13 +845,18 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
     const int g = static_cast<int>(w / chunks);
     const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
     const int c0 = ch * 32;
-    const uint32_t amask = a.group_active[g];
     const int nc = min(32, a.M - c0);
+    // the chunk's independent setup loads first (one round trip instead of
+    // a chain: the slot iteration is loaded for every lane and masked, the
+    // target syndrome word before the skip test)
+    const int4 cdk = __ldg(&a.ctype[ch]);
+    const uint32_t amask = a.group_active[g];
+    const int it_raw = a.slot_iter[g * kLanes + lane];
+    const uint32_t sy = lane < nc ? a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane] : 0u;
     const bool act = (amask >> lane) & 1u;
-    const int it = act ? a.slot_iter[g * kLanes + lane] : 0;
+    const int it = act ? it_raw : 0;
     const bool first = (it == 1);
     const uint32_t fmask = __ballot_sync(0xffffffffu, act && first);
-    const int4 cdk = __ldg(&a.ctype[ch]);
     const int type = kStage ? cdk.x : -1;
     // degree-1 checks only change in a frame's first iteration (and their
     // bit words must follow frames that k_compact moved)
@@ -860,8 +865,8 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
       continue;
     }
     __syncwarp();
-    if (lane < nc) s_syn[wi][lane] = a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane];
-    int hb0 = cdk.y;
+    if (lane < nc) s_syn[wi][lane] = sy;
+    int hb0 = cdk.y;  // = the first check's descriptor .x for generic chunks too
     if (type < 0) {  // generic chunk: per-check descriptors
       if (lane < nc) s_desc[wi][lane] = __ldg(&a.cdesc[c0 + lane]);
       __syncwarp();
