@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--multi", action="store_true",
                     help="strong scaling in ONE process: the K x F frames of the run split over --gpus devices "
                          "by bpdec_multi_decode_batch (dynamic chunk queue, host gather)")
+    ap.add_argument("--multi-devices", default=None,
+                    help="--multi: comma-separated device list (a device may repeat; default 0..gpus-1)")
     ap.add_argument("--no-traffic", action="store_true", help="skip the live ncu DRAM-traffic probe of k_check")
     ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--ref-inputs", default=None, help=argparse.SUPPRESS)
@@ -840,9 +842,11 @@ def run_multi(args):
     import torch
     import paper_2507_03509_b200 as P
     from paper_2507_03509_b200.decoder import Q_ABS
-    ng = args.gpus
-    if torch.cuda.device_count() < ng:
-        raise SystemExit(f"bench --multi: {ng} GPUs requested, {torch.cuda.device_count()} visible")
+    devices = ([int(x) for x in args.multi_devices.split(",")] if args.multi_devices
+               else list(range(args.gpus)))
+    ng = len(devices)
+    if torch.cuda.device_count() <= max(devices):
+        raise SystemExit(f"bench --multi: devices {devices} requested, {torch.cuda.device_count()} visible")
     w = P.WORKLOADS[args.workload]
     code = w.make_code()
     F = args.frames or FRAMES[args.workload]
@@ -864,7 +868,7 @@ def run_multi(args):
     del gen
     torch.cuda.empty_cache()
     cfg = P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS)
-    m = P.MultiDecoder(code, list(range(ng)), slots_per_decoder=slots)
+    m = P.MultiDecoder(code, devices, slots_per_decoder=slots)
     h_out = {"iterations": torch.zeros(total, dtype=torch.int32, pin_memory=True),
              "reasons": torch.zeros(total, dtype=torch.uint8, pin_memory=True),
              "bits": torch.zeros((total, NW), dtype=torch.int32, pin_memory=True)}
@@ -877,12 +881,13 @@ def run_multi(args):
     T = float(np.median(runs))
     it = float(h_out["iterations"].numpy().sum())
     value = it * code.n_edges / T
-    emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ng, "steps": args.steps, "warmup": 1,
+    emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": len(set(devices)), "steps": args.steps,
+          "warmup": 1, "devices": devices,
           "ms_per_step": 1e3 * T / max(1, args.steps), "higher_is_better": True, "scaling": "strong",
           "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded BASELINE generator)",
           "config": {"workload": w.name, "frames_total": total, "slots_per_gpu": slots,
                      "beta": beta if brange is None else list(brange), "d_max": w.d_max, "et": "vnr+pce",
-                     "parallelism": f"bpdec_multi x{ng} (dynamic chunk queue, host gather)"},
+                     "parallelism": f"bpdec_multi x{ng} on devices {devices} (dynamic chunk queue, host gather)"},
           "frames_per_decoder": m.last_frames_per_decoder.tolist(), "d_bar_vnr": it / total,
           "runs_s": runs, "timing_note": "median of 3 calls after a full-size warm-up call",
           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": F * (N + MW) * 4,
