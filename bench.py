@@ -36,6 +36,8 @@ E_BYTES_MODEL_A = None  # filled per code: 16E + 4N + (N+M)/8 per frame-iteratio
 
 # frames per GPU per step for each BASELINE workload (cfg4/cfg5 are the
 # 8-GPU streams 512..4096 / 8192 frames; per GPU at N=1 the first shard)
+E2E_RUNS = 5  # e2e: median of this many timed runs (>= 5)
+
 FRAMES = {"cfg1": 16, "cfg2": 64, "cfg3": 32, "cfg4": 512, "cfg5": 1024, "met": 64, "met_s": 16}
 
 
@@ -663,7 +665,7 @@ def run_ours(args):
         h_outs = [host_out() for _ in range(K)]
         dec.stream_open(cfg, packed=True, ring_frames=2 * max(F, dec.slots))
         stream_run(min(K, 4), lambda k: h_llr[k % 2], lambda k: h_syn[k % 2], h_outs)  # warm
-        for _rep in range(3):
+        for _rep in range(E2E_RUNS):
             barrier(dist)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -682,7 +684,7 @@ def run_ours(args):
             if staged:
                 dec.stage_inputs(h_llr[i], h_syn[i])
             dec.decode_batch(h_llr[i], cfg, syndrome=h_syn[i], packed=True, out=h_o, stream=sptr)
-        for _rep in range(3):
+        for _rep in range(E2E_RUNS):
             barrier(dist)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -823,7 +825,8 @@ def run_ours(args):
                          "frame_iterations": fi},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "runs": e2e_runs, "note": f"median of 3 timed runs of {K} steps", "pipelining": pipelining},
+                    "runs": e2e_runs, "note": f"median of {E2E_RUNS} timed runs of {K} steps",
+                    "pipelining": pipelining},
             "gpu_launches": launches,
             "clocks": clock,
         })
