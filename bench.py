@@ -892,7 +892,7 @@ def run_multi(args):
                      "beta": beta if brange is None else list(brange), "d_max": w.d_max, "et": "vnr+pce",
                      "parallelism": f"bpdec_multi x{ng} on devices {devices} (dynamic chunk queue, host gather)"},
           "frames_per_decoder": m.last_frames_per_decoder.tolist(), "d_bar_vnr": it / total,
-          "runs_s": runs, "timing_note": "median of 3 calls after a full-size warm-up call",
+          "runs_s": runs, "timing_note": f"median of {E2E_RUNS} calls after a full-size warm-up call",
           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": F * (N + MW) * 4,
                   "d2h_bytes_per_step": F * (NW * 4 + 5)},
           "timing": "host clock around bpdec_multi_decode_batch (host buffers in and out)"})
