@@ -877,7 +877,7 @@ def run_multi(args):
              "bits": torch.zeros((total, NW), dtype=torch.int32, pin_memory=True)}
     m.decode_batch(h_llr, cfg, syndrome=h_syn, packed=True, out=h_out)  # warm-up: the full batch once
     runs = []
-    for _rep in range(3):
+    for _rep in range(E2E_RUNS):
         t0 = time.perf_counter()
         m.decode_batch(h_llr, cfg, syndrome=h_syn, packed=True, out=h_out)
         runs.append(time.perf_counter() - t0)
