@@ -295,6 +295,9 @@ class BpDecoder {
     return o;
   }
 
+  bpdec_decoder* handle() const { return dec_.get(); }
+  const ParityCheckMatrix& code() const { return code_; }
+
   // Batched, syndrome-aware decode of `batch` frames ([batch][N] float LLRs,
   // [batch][ceil(M/32)] packed syndromes or null).
   std::vector<DecodeOutcome> decode_batch(int batch, const float* llr, const std::uint32_t* syndrome,
@@ -338,6 +341,116 @@ class BpDecoder {
   ActiveVarSet active_;
   bool active_valid_ = false;
 };
+
+// Per-frame results of a batch in packed form (stream / multi-decoder calls).
+struct BatchOutcome {
+  std::vector<std::uint32_t> bits_packed;  // [batch][ceil(N/32)], bit v of frame b = hard decision of v
+  std::vector<int32_t> iterations;
+  std::vector<std::uint8_t> reasons;       // StopReason values
+  int words_per_frame = 0;
+  std::uint8_t bit(int b, int v) const {
+    return static_cast<std::uint8_t>((bits_packed[static_cast<size_t>(b) * words_per_frame + (v >> 5)] >> (v & 31)) & 1u);
+  }
+};
+
+// Stream mode (bpdec_stream_*; no reference counterpart — it replaces the
+// per-block loop of run_trials, channel.cpp:90-148): batches submitted back
+// to back decode as one continuous frame stream through the decoder's slots.
+// The caller's LLR / syndrome arrays must stay valid until the batch is
+// waited for.  Closing (destructor) waits for every submitted batch.
+class FrameStream {
+ public:
+  FrameStream(BpDecoder& dec, const DecodeConfig& cfg, int ring_frames = 0)
+      : dec_(dec), n_(dec.code().n_vars()), nw_((dec.code().n_vars() + 31) / 32) {
+    bpdec_config c{cfg.d_max, cfg.use_pce ? 1 : 0, cfg.use_vnr ? 1 : 0, cfg.q_mode, cfg.msg_clamp};
+    check_status(bpdec_stream_open(dec_.handle(), &c, BPDEC_BITS_PACKED, ring_frames, 1, 0, 0));
+    open_ = true;
+  }
+  FrameStream(const FrameStream&) = delete;
+  FrameStream& operator=(const FrameStream&) = delete;
+  ~FrameStream() {
+    if (open_) bpdec_stream_close(dec_.handle());
+  }
+  std::int64_t submit(int batch, const float* llr, const std::uint32_t* syndrome = nullptr) {
+    BatchOutcome o;
+    o.words_per_frame = nw_;
+    o.bits_packed.assign(static_cast<size_t>(batch) * nw_, 0u);
+    o.iterations.assign(batch, 0);
+    o.reasons.assign(batch, 0);
+    std::int64_t t = -1;
+    check_status(bpdec_stream_submit(dec_.handle(), batch, llr, syndrome, o.bits_packed.data(), o.iterations.data(),
+                                     o.reasons.data(), nullptr, nullptr, &t));
+    pending_.emplace(t, std::move(o));  // vectors keep their buffers when moved
+    return t;
+  }
+  BatchOutcome wait(std::int64_t ticket) {
+    check_status(bpdec_stream_wait(dec_.handle(), ticket));
+    auto it = pending_.find(ticket);
+    if (it == pending_.end()) throw ValidationError("stream: unknown or already collected ticket");
+    BatchOutcome o = std::move(it->second);
+    pending_.erase(it);
+    return o;
+  }
+  void close() {
+    if (open_) {
+      open_ = false;
+      check_status(bpdec_stream_close(dec_.handle()));
+    }
+  }
+
+ private:
+  BpDecoder& dec_;
+  int n_, nw_;
+  bool open_ = false;
+  std::map<std::int64_t, BatchOutcome> pending_;
+};
+
+// Several GPUs of one host (bpdec_multi_*; the strided worker pool of
+// run_trials, channel.cpp:98-122): one decoder and host thread per entry of
+// `devices` (a device may repeat), frames dealt from a dynamic chunk queue,
+// per-frame outputs at their frame index — identical for any device list.
+class MultiDecoder {
+ public:
+  MultiDecoder(const ParityCheckMatrix& code, const std::vector<int>& devices, int slots_per_decoder = 64)
+      : code_(code) {
+    std::vector<int32_t> dv(devices.begin(), devices.end());
+    bpdec_multi* m = nullptr;
+    check_status(bpdec_multi_create(code.handle(), dv.data(), static_cast<int32_t>(dv.size()), slots_per_decoder, &m));
+    m_.reset(m);
+  }
+  BatchOutcome decode_batch(int batch, const float* llr, const std::uint32_t* syndrome, const DecodeConfig& cfg,
+                            int chunk_frames = 0) {
+    const int nw = (code_.n_vars() + 31) / 32;
+    BatchOutcome o;
+    o.words_per_frame = nw;
+    o.bits_packed.assign(static_cast<size_t>(batch) * nw, 0u);
+    o.iterations.assign(batch, 0);
+    o.reasons.assign(batch, 0);
+    bpdec_config c{cfg.d_max, cfg.use_pce ? 1 : 0, cfg.use_vnr ? 1 : 0, cfg.q_mode, cfg.msg_clamp};
+    check_status(bpdec_multi_decode_batch(m_.get(), batch, llr, syndrome, &c, BPDEC_BITS_PACKED, o.bits_packed.data(),
+                                          o.iterations.data(), o.reasons.data(), nullptr, nullptr, chunk_frames,
+                                          nullptr));
+    return o;
+  }
+
+ private:
+  struct Del {
+    void operator()(bpdec_multi* m) const { bpdec_multi_destroy(m); }
+  };
+  ParityCheckMatrix code_;
+  std::unique_ptr<bpdec_multi, Del> m_;
+};
+
+// Two-edge-type low-rate construction with a core code (FER < 1 family;
+// bpdec_code_generate_met_core).
+inline ParityCheckMatrix generate_met_core(int n_vars, int n_checks, int n_deg1, const std::vector<int>& core_degrees,
+                                           const std::vector<double>& core_probs, int ext_degree, std::uint64_t seed) {
+  std::vector<int32_t> d(core_degrees.begin(), core_degrees.end());
+  bpdec_code* c = nullptr;
+  check_status(bpdec_code_generate_met_core(n_vars, n_checks, n_deg1, static_cast<int32_t>(d.size()), d.data(),
+                                            core_probs.data(), ext_degree, seed, &c));
+  return ParityCheckMatrix::adopt(c);
+}
 
 // ≙ etdec::run_trials (channel.hpp:72-74) on the GPU: trials are decoded in
 // device-resident blocks instead of by `workers` threads; the stop rule is

@@ -46,6 +46,9 @@ int main(int argc, char** argv) {
   const auto pm = ed::apply_puncture(lift, 0.6, 3);
   CHECK(pm.punctured.size() == static_cast<size_t>(std::lround(2048 - 1024 / 0.6)));
   CHECK(ed::no_puncture(lift).empty() && std::fabs(ed::no_puncture(lift).effective_rate - 0.5) < 1e-15);
+  // FER < 1 family generator
+  const auto met = ed::generate_met_core(8192, 7373, 5734, {2, 3}, {0.5, 0.5}, 2, 1);
+  CHECK(met.n_vars() == 8192 && met.n_checks() == 7373);
 
   if (!gpu) {
     bool dev_err = false;
@@ -93,6 +96,44 @@ int main(int argc, char** argv) {
   for (const auto& kv : t1.iteration_histogram) hsum += kv.second;
   CHECK(hsum == t1.frames && t1.stops_syndrome + t1.stops_vnr + t1.stops_max_iter == t1.frames);
   CHECK(t1.fer >= 0.0 && t1.fer <= 1.0 && t1.fer_ci_low <= t1.fer && t1.fer <= t1.fer_ci_high);
+  // stream mode and the multi-decoder give, per frame, the blocking decode's
+  // result (frames of the (3,6) lift with seeded Gaussian LLRs)
+  {
+    const int B = 96, n = lift.n_vars();
+    std::vector<float> llrs(static_cast<size_t>(B) * n);
+    std::uint64_t st = 0x9e3779b97f4a7c15ull;
+    for (auto& v : llrs) {  // Irwin-Hall approximation of N(0.9, 1.3^2), reproducible without <random>
+      double acc = 0.0;
+      for (int k = 0; k < 4; ++k) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        acc += static_cast<double>(st >> 11) * (1.0 / 9007199254740992.0);
+      }
+      v = static_cast<float>(0.9 + 1.3 * (acc - 2.0) * std::sqrt(3.0));
+    }
+    ed::DecodeConfig sc;
+    sc.d_max = 80;
+    sc.use_vnr = true;
+    ed::BpDecoder sd(lift, 0, 64);
+    const auto want = sd.decode_batch(B, llrs.data(), nullptr, sc);
+    std::vector<ed::BatchOutcome> got;
+    {
+      ed::FrameStream fs(sd, sc);
+      std::vector<std::int64_t> tickets;
+      for (int b0 = 0; b0 < B; b0 += 32) tickets.push_back(fs.submit(32, llrs.data() + static_cast<size_t>(b0) * n));
+      for (auto t : tickets) got.push_back(fs.wait(t));
+    }
+    for (int b = 0; b < B; ++b) {
+      const auto& g = got[b / 32];
+      CHECK(g.iterations[b % 32] == want[b].iterations && g.reasons[b % 32] == static_cast<int>(want[b].reason));
+      for (int v = 0; v < n; ++v) CHECK(g.bit(b % 32, v) == want[b].bits[v]);
+    }
+    ed::MultiDecoder md(lift, {0, 0}, 32);
+    const auto mo = md.decode_batch(B, llrs.data(), nullptr, sc, 20);
+    for (int b = 0; b < B; ++b) {
+      CHECK(mo.iterations[b] == want[b].iterations && mo.reasons[b] == static_cast<int>(want[b].reason));
+      for (int v = 0; v < n; ++v) CHECK(mo.bit(b, v) == want[b].bits[v]);
+    }
+  }
   std::printf("compat_test (gpu) OK\n");
   return 0;
 }
