@@ -430,7 +430,7 @@ def traffic_probe(args):
     code = w.make_code()
     F = args.frames or FRAMES[args.workload]
     dec = P.BatchDecoder(code, device=0, max_slots=args.slots or
-                         (min(4 * F, 1024) if args.mode == "stream" else min(F, 512)))
+                         (min(6 * F, 1024) if args.mode == "stream" else min(F, 512)))
     d_llr, d_syn, _ = make_frames(P, dec, code, args, F, 0, 0)
     torch.cuda.synchronize()
     cfg = P.DecodeConfig(d_max=w.d_max, use_pce=True, use_vnr=True, q_mode=Q_ABS)
@@ -510,9 +510,9 @@ def run_ours(args):
     w = P.WORKLOADS[args.workload]
     code = w.make_code()
     F = args.frames or FRAMES[args.workload]
-    # stream mode keeps four batches' worth of slots in flight: a batch's
+    # stream mode keeps six batches' worth of slots in flight: a batch's
     # tail shares the steps with the next batches' frames
-    slots = args.slots or (min(4 * F, 1024) if args.mode == "stream" else min(F, 512))
+    slots = args.slots or (min(6 * F, 1024) if args.mode == "stream" else min(F, 512))
     beta, brange = workload_beta(args)
     dec = P.BatchDecoder(code, device=local, max_slots=slots)
     # weak scaling: rank r owns global frames [r*F, (r+1)*F)
