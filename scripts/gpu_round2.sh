@@ -26,4 +26,6 @@ st ncu_full $?
 timeout 1200 python scripts/vnr_pce_sweep.py gpurun_out/et_sweep_cfg2.json > gpurun_out/sweep2.log 2>&1; st sweep2 $?
 timeout 900 python scripts/vnr_pce_sweep.py gpurun_out/et_sweep_cfg5.json --workload cfg5 --no-none > gpurun_out/sweep5.log 2>&1; st sweep5 $?
 timeout 900 python scripts/qc_probe.py > gpurun_out/qc.log 2>&1; st qc $?
+timeout 1800 python scripts/vnr_pce_sweep.py gpurun_out/et_sweep_met.json --workload met --betas 0.84 0.85 0.86 0.865 0.87 0.875 0.88 0.9 --batches 8 --dmax 250 1000 --no-none > gpurun_out/sweep_met.log 2>&1; st sweep_met $?
+timeout 900 python bench.py --multi --gpus 1 --workload cfg5 --frames 8192 --steps 1 --no-traffic > gpurun_out/bench_cfg5_stream8192.log 2>&1; st bench_cfg5_8192 $?
 cat gpurun_out/status.txt
