@@ -20,7 +20,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REF_LIB = os.path.join(HERE, "_ref", "libetdec_ref.so")
 ORC_LIB = os.path.join(HERE, "_build", "liboracle.so")
 
-ORC_REF_DOUBLE, ORC_PHI_FLOAT = 0, 1
+ORC_REF_DOUBLE, ORC_PHI_FLOAT, ORC_T_FLOAT = 0, 1, 2
+# the float32 variant of the shipped CUDA kernels (phi.cuh: t domain)
+ORC_GPU_FLOAT = ORC_T_FLOAT
 
 
 def _p(a, t):

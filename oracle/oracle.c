@@ -18,6 +18,11 @@
  *                   clamp(llr), per-check order "edges to degree>=2 variables
  *                   first, then degree-1 edges", phi evaluated in double and
  *                   rounded — the GPU algorithm with ideal phi.
+ *   ORC_T_FLOAT     the same float32 algorithm in the t domain of the CUDA
+ *                   kernels (phi.cuh): t = e^-|m| (double exp, rounded),
+ *                   outputs -ln of the float fraction n/d of the prefix /
+ *                   suffix (+)-sums, a (+) b = (a + b) / (1 + ab) — the
+ *                   shipped GPU algorithm with ideal exp / ln.
  * Build with -ffp-contract=off (no FMA contraction; the reference's Release
  * build on x86-64 has none either).
  */
@@ -142,8 +147,15 @@ static int decode_ref_double(int n, int m, const int* cp, const int* cv, const d
 /* phi(x) = -ln tanh(x/2) = log1p(2/expm1(x)); phi(0) = inf, phi(inf) = 0 */
 static float phi_ideal(float x) { return (float)log1p(2.0 / expm1((double)x)); }
 
+/* t domain: fraction (n, d) (+) t and fraction (+) fraction (float) */
+static void tf_add(float* n, float* d, float t) {
+  const float nn = *n + t * *d, dd = *d + t * *n;
+  *n = nn;
+  *d = dd;
+}
+
 static int decode_phi_float(int n, int m, const int* cp, const int* cv, const double* llr_d,
-                            const uint32_t* syn, const orc_config* cfg, uint8_t* bits, int32_t* iters,
+                            const uint32_t* syn, const orc_config* cfg, int tdom, uint8_t* bits, int32_t* iters,
                             int32_t* reason, double* post_out, double* q_trace) {
   const int E = cp[m];
   int *vp, *ve, *deg, *ord;
@@ -209,6 +221,20 @@ static int decode_phi_float(int n, int m, const int* cp, const int* cv, const do
       } else if (d == 2) {
         out[0] = fminf(fabsf(msg[1]), clamp);
         out[1] = fminf(fabsf(msg[0]), clamp);
+      } else if (tdom) {
+        /* ph = t, pre = prefix fraction numerators, lv-free scratch in out */
+        float pn = 0.0f, pd = 1.0f, sn = 0.0f, sd = 1.0f;
+        for (j = 0; j < d; ++j) ph[j] = (float)exp(-(double)fabsf(msg[j]));
+        for (j = 0; j < d; ++j) { /* out[j] <- prefix over 0..j-1, kept as (pre, out) = (n, d) */
+          pre[j] = pn;
+          out[j] = pd;
+          tf_add(&pn, &pd, ph[j]);
+        }
+        for (j = d - 1; j >= 0; --j) {
+          const float nn = pre[j] * sd + out[j] * sn, dd = out[j] * sd + pre[j] * sn;
+          out[j] = nn == dd ? 0.0f : fminf(fabsf((float)log((double)dd / (double)nn)), clamp);
+          tf_add(&sn, &sd, ph[j]);
+        }
       } else {
         for (j = 0; j < d; ++j) {
           ph[j] = phi_ideal(fabsf(msg[j]));
@@ -284,9 +310,9 @@ int orc_decode(int n_vars, int n_checks, const int* check_ptr, const int* check_
   if (variant == ORC_REF_DOUBLE)
     return decode_ref_double(n_vars, n_checks, check_ptr, check_vars, llr, syndrome, cfg, bits, iterations, reason,
                              posteriors, q_trace);
-  if (variant == ORC_PHI_FLOAT)
-    return decode_phi_float(n_vars, n_checks, check_ptr, check_vars, llr, syndrome, cfg, bits, iterations, reason,
-                            posteriors, q_trace);
+  if (variant == ORC_PHI_FLOAT || variant == ORC_T_FLOAT)
+    return decode_phi_float(n_vars, n_checks, check_ptr, check_vars, llr, syndrome, cfg, variant == ORC_T_FLOAT,
+                            bits, iterations, reason, posteriors, q_trace);
   return 1;
 }
 

@@ -8,7 +8,7 @@
 extern "C" {
 #endif
 
-enum { ORC_REF_DOUBLE = 0, ORC_PHI_FLOAT = 1 };
+enum { ORC_REF_DOUBLE = 0, ORC_PHI_FLOAT = 1, ORC_T_FLOAT = 2 };
 enum { ORC_Q_RAW = 0, ORC_Q_ABS = 1 };
 
 typedef struct {

@@ -356,10 +356,59 @@ __device__ __forceinline__ void check_load(const Args& a, CheckState<MAXD>& s, i
   }
 }
 
-// Magnitudes of the outgoing messages from the incoming ones (phi domain;
-// prefix/suffix sums, no subtraction).  deg 1: empty product -> clamp;
-// deg 2: phi(phi(x)) = x, passed through.
+#ifndef BPDEC_PHI_DOMAIN
+#define BPDEC_PHI_DOMAIN 0  // 0: t domain (phi.cuh, the shipped form); 1: phi domain (A/B builds)
+#endif
+
+// Magnitudes of the outgoing messages from the incoming ones; deg 1: empty
+// product -> clamp; deg 2: phi(phi(x)) = x, passed through.
 // `m` are magnitudes (already clamped to <= msg_clamp except in iteration 1).
+//
+// t domain (phi.cuh): t_i = e^-m_i, prefix / suffix (+)-sums, out_j =
+// -ln(pre_j (+) suf_j+1).  Raw operands stay raw where the structure allows
+// (pre_1, suf_D-1), so a degree-3 or degree-4 check needs no fraction (+)
+// fraction.  phi domain: prefix / suffix sums of phi without the additions
+// of 0 (phi >= 0, so bit-identical to starting both sums at 0).
+//
+// DSum: the hi-edge sum a degree-1 decision reads (check_magnitudes_d1):
+// a float phi sum or a t-domain fraction.
+#if BPDEC_PHI_DOMAIN
+using DSum = float;
+__device__ __forceinline__ float d1_stat(float x) { return dev::phi(x); }
+__device__ __forceinline__ float d1_out(float s, float clamp) { return fminf(dev::phi(s), clamp); }
+#else
+using DSum = dev::TF;
+__device__ __forceinline__ float d1_stat(float x) { return dev::tdom(x); }
+__device__ __forceinline__ float d1_out(dev::TF s, float clamp) { return dev::tmag(s, clamp); }
+
+// t-domain outputs of a check of degree D (>= 3) whose inputs are t[0..D-1];
+// out[j] for j < NOUT (NOUT = D: all; D - 1: all but the last edge).
+// Returns the prefix sum over t[0..D-2] (the hi sum of a d1 check).
+template <int D, int NOUT>
+__device__ __forceinline__ dev::TF t_outputs(const float (&t)[D], float (&out)[D], float clamp) {
+  using dev::TF;
+  TF pre[D];  // pre[j] = t[0] (+) ... (+) t[j-1], j >= 2 (pre[1] = t[0], raw)
+  pre[2] = dev::tf_pair(t[0], t[1]);
+#pragma unroll
+  for (int j = 3; j < D; ++j) pre[j] = dev::tf_add(pre[j - 1], t[j - 1]);
+  if (NOUT == D) out[D - 1] = dev::tmag(pre[D - 1], clamp);
+  // suffix: suf = t[j+1] (+) ... (+) t[D-1], raw while it holds one term
+  TF suf = dev::tf_pair(t[D - 2], t[D - 1]);  // j = D - 3
+#pragma unroll
+  for (int j = D - 2; j >= 0; --j) {
+    TF o;
+    if (j == D - 2) {
+      o = j == 0 ? TF{t[D - 1], 1.0f} : (j == 1 ? dev::tf_pair(t[0], t[D - 1]) : dev::tf_add(pre[j], t[D - 1]));
+    } else {
+      if (j < D - 3) suf = dev::tf_add(suf, t[j + 1]);
+      o = j == 0 ? suf : (j == 1 ? dev::tf_add(suf, t[0]) : dev::tf_join(pre[j], suf));
+    }
+    out[j] = dev::tmag(o, clamp);
+  }
+  return pre[D - 1];
+}
+#endif
+
 template <int D>
 __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&out)[D], float clamp) {
   if (D == 1) {
@@ -368,8 +417,7 @@ __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&ou
     out[0] = fminf(m[1], clamp);
     out[1] = fminf(m[D > 1 ? 0 : 0], clamp);
   } else {
-    // prefix / suffix sums without the additions of 0 (phi >= 0, so the
-    // results are bit-identical to starting both sums at 0)
+#if BPDEC_PHI_DOMAIN
     float ph[D];
     float pre[D];
 #pragma unroll
@@ -385,18 +433,26 @@ __device__ __forceinline__ void check_magnitudes(const float (&m)[D], float (&ou
       suf += ph[j];
     }
     out[0] = fminf(dev::phi(suf), clamp);
+#else
+    float t[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t[j] = dev::tdom(m[j]);
+    t_outputs<D, D>(t, out, clamp);
+#endif
   }
 }
 
 // Check with NH edges to degree>=2 variables and one degree-1 edge whose
-// phi value phd is given: outputs of the NH hi edges (same prefix / suffix
-// order as check_magnitudes<NH+1>, so bit-identical to it when phd =
-// phi(m[NH])) and s_hi = sum of the hi edges' phi (the degree-1 edge's
-// output is phi(s_hi), not formed here).
+// domain value phd (phi or t of its clamped magnitude, d1_stat) is given:
+// outputs of the NH hi edges (same prefix / suffix order as
+// check_magnitudes<NH+1>, so bit-identical to it when phd =
+// d1_stat(m[NH])) and s_hi = the hi edges' sum (the degree-1 edge's output
+// is d1_out(s_hi), not formed here).
 template <int NH>
 __device__ __forceinline__ void check_magnitudes_d1(const float (&m)[NH + 1], float phd, float (&out)[NH + 1],
-                                                    float clamp, float& s_hi) {
+                                                    float clamp, DSum& s_hi) {
   constexpr int D = NH + 1;
+#if BPDEC_PHI_DOMAIN
   float ph[D];
   float pre[D];
 #pragma unroll
@@ -413,22 +469,40 @@ __device__ __forceinline__ void check_magnitudes_d1(const float (&m)[NH + 1], fl
     suf += ph[j];
   }
   out[0] = fminf(dev::phi(suf), clamp);
+#else
+  float t[D];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) t[j] = dev::tdom(m[j]);
+  t[NH] = phd;
+  s_hi = t_outputs<D, D - 1>(t, out, clamp);
+#endif
 }
 
 // Hard decision of a degree-1 variable, post = l + o (o its check's output
-// to it), decided in the phi domain without forming o: |o| = min(phi(s_hi),
-// clamp) against |l| through phd = phi(min(|l|, clamp)) (phi decreasing;
-// phd <= phc = phi(clamp) means |l| >= clamp).  sl / so: sign bits of l and
-// o.  Same decision as (l + o < 0) except where |o| and |l| agree to float
-// rounding (a posterior at zero: a tie).
-__device__ __forceinline__ uint32_t d1_bit_phi(uint32_t sl, uint32_t so, float s_hi, float phd, float phc) {
+// to it), decided without forming o: |o| = min(-ln T_hi, clamp) (t domain;
+// phi domain: min(phi(s_hi), clamp)) against |l| through phd = d1_stat(
+// min(|l|, clamp)) (both maps decreasing; phd <= phc = d1_stat(clamp) means
+// |l| >= clamp).  sl / so: sign bits of l and o.  Same decision as (l + o <
+// 0) except where |o| and |l| agree to float rounding (a posterior at zero:
+// a tie).
+__device__ __forceinline__ uint32_t d1_bit_phi(uint32_t sl, uint32_t so, DSum s_hi, float phd, float phc) {
   // branch-free (selects only: the branchy form compiled to divergent
   // branches and a convergence check before every ballot)
+#if BPDEC_PHI_DOMAIN
   const float kInf = __int_as_float(0x7f800000);
   const bool zero = (phd == kInf) & (s_hi == kInf);  // l = 0 and o = 0: +0 or -0, not < 0
-  const bool l_small = phd > phc;                    // |l| < clamp
-  const bool o_big = l_small & (s_hi < phd);         // |o| > |l|
-  const bool l_big = !l_small | (s_hi > phd);        // |l| > |o|  (neither: equal, post = +0)
+  const bool o_lt = s_hi < phd;                      // phi(|o|) < phi(|l|)
+  const bool o_gt = s_hi > phd;
+#else
+  // l = 0 (t = 1) and o = 0 (T_hi = 1, n == d exactly)
+  const bool zero = (phd == 1.0f) & (s_hi.n == s_hi.d);
+  const float r = phd * s_hi.d;  // T_hi = n / d against t(|l|): n against t*d
+  const bool o_lt = s_hi.n < r;
+  const bool o_gt = s_hi.n > r;
+#endif
+  const bool l_small = phd > phc;       // |l| < clamp
+  const bool o_big = l_small & o_lt;    // |o| > |l|
+  const bool l_big = !l_small | o_gt;   // |l| > |o|  (neither: equal, post = +0)
   const uint32_t diff = o_big ? so : (l_big ? sl : 0u);
   const uint32_t same = zero ? 0u : sl;
   return sl == so ? same : diff;
@@ -663,16 +737,16 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
       float phd = fabsf(l);
       float phf = 0.0f;
       if (FM) {
-        phf = dev::phi(m[NH]);  // unclamped in the first iteration (cl = inf)
+        phf = d1_stat(m[NH]);  // unclamped in the first iteration (cl = inf)
         if (first) phd = phf;
       }
-      float s_hi;
+      DSum s_hi;
       check_magnitudes_d1<NH>(m, phd, out, clamp, s_hi);
       const uint32_t so = (par ^ sm[NH]) >> 31, sl = sm[NH] >> 31;
       if (FM) {
         // first lanes: the plain decision on the LLR, and the phi of the
         // clamped magnitude written back for the steady state
-        const float o = __uint_as_float(__float_as_uint(fminf(dev::phi(s_hi), clamp)) | (par ^ sm[NH]));
+        const float o = __uint_as_float(__float_as_uint(d1_out(s_hi, clamp)) | (par ^ sm[NH]));
         const uint32_t fb = (l + o < 0.0f) ? 1u : 0u;
         dbit = first ? fb : d1_bit_phi(sl, so, s_hi, phd, phc);
         const float stored = __uint_as_float(__float_as_uint(fabsf(l) > clamp ? phc : phf) | sm[NH]);
@@ -737,7 +811,7 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
   float* llrg = a.llr_d + rix(g, a.N1, db, LW) + f;
   const float clamp = a.clamp;
   const float cl = first ? __int_as_float(0x7f800000) : clamp;
-  const float phc = dev::phi(clamp);
+  const float phc = d1_stat(clamp);
   // this lane's 16-byte piece: frames lcol .. lcol+3 of row lrow of a row group
   constexpr int QPR = LW / 4;  // 16-byte pieces per row
   const int lrow = lane / QPR;

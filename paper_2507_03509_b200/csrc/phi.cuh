@@ -53,3 +53,52 @@ __device__ __forceinline__ float phi(float x) {
 
 }  // namespace dev
 }  // namespace bpdec
+
+// ---------------------------------------------------------------------------
+// The same check update in the "t domain": t(x) = e^-x, the ratio
+// (1 - tanh(x/2)) / (1 + tanh(x/2)).  A product of tanh factors is, in t,
+// the relativistic-velocity sum  a (+) b = (a + b) / (1 + a b)  (associative,
+// commutative, 0 neutral, 1 absorbing), so
+//     |c2v_j| = -ln( (+)_{i != j} t(|v2c_i|) ),
+// the reference's 2*atanh(prod tanh(m/2)) without ever forming tanh: t keeps
+// full relative precision where tanh rounds to 1 (large |m|, the saturation
+// that rules out the float tanh form), and -ln T of a tiny T is as exact as
+// phi of a small sum.  Only weak outputs (T near 1) lose relative precision:
+// their absolute error stays ~1e-7, far below the float posterior rounding.
+//
+// Sums are kept as fractions n / d of non-negative terms (no cancellation,
+// d >= 1, one MUFU.LG2 pair per output instead of two phi evaluations per
+// edge):  inputs 1 MUFU (EX2) + 1 FMUL, each (+) 2 ops, outputs
+// ln2 * |lg2 d - lg2 n| (2 MUFU + 2 ops) min clamp.
+//
+// Exact zeros: a zero input (t = 1) makes every other output exactly 0, as
+// in the reference (tanh 0 = 0): every (+) below keeps n == d bitwise once
+// one operand has n == d (fma / add commute), and lg2 d - lg2 n is then 0.
+// An underflowed t (|m| >= ~87) is 0: the outputs of the others are their
+// own -ln t, and an all-underflow sum gives n = 0 -> +inf -> clamp, the
+// reference's atanh(1) = inf -> clamp.
+namespace bpdec {
+namespace dev {
+
+struct TF {
+  float n, d;  // T = n / d, 0 <= n <= d (up to rounding), d >= 1
+};
+
+__device__ __forceinline__ float tdom(float x) { return ex2_approx(x * -1.4426950408889634f); }
+
+// raw (+) raw
+__device__ __forceinline__ TF tf_pair(float a, float b) { return {a + b, fmaf(a, b, 1.0f)}; }
+// fraction (+) raw
+__device__ __forceinline__ TF tf_add(TF f, float t) { return {fmaf(t, f.d, f.n), fmaf(t, f.n, f.d)}; }
+// fraction (+) fraction, rounded products then a commuting add (symmetric:
+// n == d on either side gives n == d)
+__device__ __forceinline__ TF tf_join(TF a, TF b) {
+  return {__fadd_rn(__fmul_rn(a.n, b.d), __fmul_rn(a.d, b.n)), __fadd_rn(__fmul_rn(a.d, b.d), __fmul_rn(a.n, b.n))};
+}
+// |c2v| = min(-ln(n / d), clamp); |.| absorbs a rounding of n above d
+__device__ __forceinline__ float tmag(TF f, float clamp) {
+  return fminf(fabsf((lg2_approx(f.d) - lg2_approx(f.n)) * 0.6931471805599453f), clamp);
+}
+
+}  // namespace dev
+}  // namespace bpdec

@@ -7,7 +7,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle import ORC_PHI_FLOAT
+from oracle import ORC_GPU_FLOAT
 from _parity import DRIFT_FACTOR, _norm_err, ref_ties, ulp_up
 
 pytestmark = pytest.mark.gpu
@@ -189,10 +189,11 @@ def test_observer_matches_reference(P, ref, orc, cfg1_code, lift36, codename, pc
         assert r["calls"] == len(calls) == out.iterations == r["iterations"]
         assert [c[0] for c in calls] == list(range(1, r["iterations"] + 1))
         # and the float32-arithmetic trajectory itself: the plain-C float
-        # restatement (ideal phi) drifts from the double reference by up to
-        # ~0.5% in q on frames converging slowly near d_max (lift36, beta 0.7)
+        # restatement of the GPU algorithm (t domain, ideal exp / ln; the phi
+        # form drifts as much) moves from the double reference by up to ~1%
+        # in q on frames converging slowly near d_max (lift36, beta 0.7)
         of = orc.decode(code.n_vars, *code.csr(), leq[f].astype(np.float64), d_max=d_max, use_pce=pce,
-                        use_vnr=vnr, variant=ORC_PHI_FLOAT)
+                        use_vnr=vnr, variant=ORC_GPU_FLOAT)
         for k, c in enumerate(calls):
             qtol = 1e-5 * abs(r["q"][k]) + 1e-3
             if codename != "cfg1" and k < ru["calls"]:
@@ -205,10 +206,10 @@ def test_observer_matches_reference(P, ref, orc, cfg1_code, lift36, codename, pc
             if codename != "cfg1" and k < ru["calls"]:
                 bound = max(1.0, DRIFT_FACTOR * _norm_err(ru["posteriors"][k], r["posteriors"][k]))
             if codename != "cfg1" and err > bound:
-                # the float32 trajectory (restatement, ideal phi) at iteration
+                # the float32 trajectory (restatement, ideal exp / ln) at iteration
                 # k+1: ET does not change a trajectory before its stop
                 ofk = orc.decode(code.n_vars, *code.csr(), leq[f].astype(np.float64), d_max=k + 1, use_pce=False,
-                                 use_vnr=False, variant=ORC_PHI_FLOAT)
+                                 use_vnr=False, variant=ORC_GPU_FLOAT)
                 bound = max(bound, 4.0 * _norm_err(ofk["posteriors"], r["posteriors"][k]))
             assert err <= bound, (f, k, float(err), float(bound))
             if int(c[2]) != int(r["syndrome_ok"][k]):

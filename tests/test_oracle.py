@@ -125,9 +125,11 @@ def test_restatement_matches_golden_fixtures(orc):
                 assert np.array_equal(o["posteriors"].astype(np.float32), z[f"{mode}_posteriors"][b])
 
 
-def test_phi_float_variant_tracks_reference(P, ref, orc, cfg1_code):
-    """The GPU algorithm (float, phi domain) restated on the CPU stays within
-    the parity tolerance of the reference on config-1 frames."""
+@pytest.mark.parametrize("variant", [oracle.ORC_PHI_FLOAT, oracle.ORC_T_FLOAT])
+def test_phi_float_variant_tracks_reference(P, ref, orc, cfg1_code, variant):
+    """The GPU algorithm (float; phi domain, and the shipped t domain)
+    restated on the CPU stays within the parity tolerance of the reference on
+    config-1 frames."""
     ptr, var = cfg1_code.csr()
     snr = P.snr_for_beta(0.95, cfg1_code.rate())
     llr, x, s = P.sample_frames(cfg1_code, snr, 5, 0, 2)
@@ -136,7 +138,7 @@ def test_phi_float_variant_tracks_reference(P, ref, orc, cfg1_code):
     r = rc.decode_batch(leq, d_max=200, use_pce=True, use_vnr=True, threads=2)
     for b in range(2):
         o = orc.decode(cfg1_code.n_vars, ptr, var, leq[b], d_max=200, use_pce=True, use_vnr=True,
-                       variant=oracle.ORC_PHI_FLOAT)
+                       variant=variant)
         assert o["iterations"] == r["iterations"][b]
         assert np.array_equal(o["bits"], r["bits"][b])
         np.testing.assert_allclose(o["posteriors"], r["posteriors"][b], rtol=1e-4, atol=1e-4)
