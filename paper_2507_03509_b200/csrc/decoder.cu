@@ -96,6 +96,20 @@ constexpr int kCheckGrab = 1;     // k_check chunks per scheduler atomic (2: -9%
                                   // chunks of a grab run back to back on one warp instead of side by side)
 constexpr int kTermBlocks = 16;   // k_decide q-reduction blocks per group (q partial tree: fixed by the code)
 
+// L2 residency hints (measured on cfg2, 384-slot stream, A/B of builds on
+// one box): the posterior rows are written once by k_var and gathered ~deg
+// times by the next k_check, between 5 GB of streamed messages per step.
+// evict_last on the gathers (1) and also on k_var's posterior stores (2):
+// +2.3 % / +3.5 % edge-updates/s (the variable pass -10 %: fewer DRAM writes
+// between its gathers); evict_last on the per-edge hard-decision words
+// (ebits, read by k_decide): +0.5 %.  0 = plain accesses (A/B builds).
+#ifndef BPDEC_POST_EVICT_LAST
+#define BPDEC_POST_EVICT_LAST 2
+#endif
+
+#ifndef BPDEC_EBITS_EVL
+#define BPDEC_EBITS_EVL 1  // the per-edge hard-decision words of k_var are stored with an evict_last hint
+#endif
 // ------------------------------------------------------------ arguments --
 struct Args {
   // code
@@ -237,10 +251,29 @@ __device__ __forceinline__ void st_pred(float* p, float v, bool pred) {
                : "memory");
 }
 
+[[maybe_unused]] __device__ __forceinline__ void st_pred_pol(float* p, float v, bool pred, uint64_t pol) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.L2::cache_hint.f32 [%0], %1, %3;\n\t}"
+               :
+               : "l"(p), "f"(v), "r"(static_cast<int>(pred)), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_pred_u32(uint32_t* p, uint32_t v, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}"
                :
                : "l"(p), "r"(v), "r"(static_cast<int>(pred))
+               : "memory");
+}
+
+[[maybe_unused]] __device__ __forceinline__ uint64_t policy_evict_last_nv() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+[[maybe_unused]] __device__ __forceinline__ void st_pred_u32_pol(uint32_t* p, uint32_t v, bool pred, uint64_t pol) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.L2::cache_hint.u32 [%0], %1, %3;\n\t}"
+               :
+               : "l"(p), "r"(v), "r"(static_cast<int>(pred)), "l"(pol)
                : "memory");
 }
 
@@ -621,6 +654,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
 
 // Stage layout for a batch of K checks: [K*NH posterior rows][K*NH c2v rows]
 // [K*ND llr rows], rows of LW floats.  `lrow`/`lcol` = this lane's 16-byte
@@ -638,12 +676,19 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
   constexpr int NPC = K * SH::CR;   // previous-c2v rows (0 without C2V)
   constexpr int NPD = K * ND;       // degree-1 rows
   constexpr int RPI = 128 / LW;  // rows per warp instruction
+#if BPDEC_POST_EVICT_LAST
+  const uint64_t polp = policy_evict_last();
+#endif
 #pragma unroll
   for (int r0 = 0; r0 < NPH; r0 += RPI) {
     const int r = r0 + lrow;
     if (r < NPH) {
       const int h = hh[i0 * NH + r];
+#if BPDEC_POST_EVICT_LAST
+      cp_async16_ef(stage + r * LW + lcol, post0 + static_cast<size_t>(h) * LW + lcol, qact, polp);
+#else
       cp_async16(stage + r * LW + lcol, post0 + static_cast<size_t>(h) * LW + lcol, qact);
+#endif
       if (C2V)
         cp_async16_ef(stage + (NPH + r) * LW + lcol, c2v0 + static_cast<size_t>(i0 * NH + r) * LW + lcol, qc2v, pol);
     }
@@ -1134,7 +1179,13 @@ template <int D, int QMODE, int LW, int FE>
 __device__ __forceinline__ void var_finish(float p, float* postg, uint32_t* ebg, const int32_t* ve, int i0, int nval,
                                            int lane, int q, int f, bool act, double& acc, uint32_t& hw) {
   const bool on = act && i0 + q < nval;
+#if BPDEC_POST_EVICT_LAST >= 2
+  uint64_t polp;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(polp));
+  st_pred_pol(postg + static_cast<size_t>(i0 + q) * LW, p, on, polp);
+#else
   st_pred(postg + static_cast<size_t>(i0 + q) * LW, p, on);
+#endif
   if constexpr (FE == 1) {
     if (on) acc += QMODE == 0 ? static_cast<double>(p) : static_cast<double>(fabsf(p));
   } else {
@@ -1154,7 +1205,11 @@ __device__ __forceinline__ void var_finish(float p, float* postg, uint32_t* ebg,
     for (int j0 = 0; j0 < D; j0 += 32) {
       const int j = j0 + lane;
       const int e = ve[i * D + (j < D ? j : 0)];
+#if BPDEC_EBITS_EVL
+      st_pred_u32_pol(ebg + static_cast<uint32_t>(max(e, 0)), word, j < D && e >= 0, policy_evict_last_nv());
+#else
       st_pred_u32(ebg + static_cast<uint32_t>(max(e, 0)), word, j < D && e >= 0);
+#endif
     }
   }
 }
