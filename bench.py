@@ -810,6 +810,13 @@ def run_ours(args):
                          "traffic_measured": traffic if traffic is not None else traffic_note,
                          "peak_kind": peak_kind,
                          "bytes_model": "model A (BASELINE.md §2): check pass = 8E per frame-iteration",
+                         "note": ("model A counts naive per-edge messages; this layout moves fewer bytes (model_b, "
+                                  "traffic), so a model-A frac above 1 is possible -- dram_frac is the kernel's "
+                                  "measured DRAM bytes over its CUDA-event time, the real utilisation"),
+                         "dram_achieved": (None if traffic is None or t_check <= 0 else
+                                           traffic["bytes_per_frame_iteration"] * fi / t_check / 1e9),
+                         "dram_frac": (None if traffic is None or t_check <= 0 else
+                                       traffic["bytes_per_frame_iteration"] * fi / t_check / 1e9 / peak),
                          "model_b": {"what": "bytes this layout moves per frame-iteration (DESIGN.md §3)",
                                      "check_bytes": lb["check"], "variable_bytes": lb["variable"],
                                      "check_achieved": b_check, "check_frac": b_check / peak,
