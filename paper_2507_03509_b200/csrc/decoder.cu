@@ -92,6 +92,8 @@ constexpr int kCheckMinBlocks = BPDEC_CHECK_MINB;  // k_check blocks per SM (reg
 // (instruction cache; splitting k_check<8> measured -2% on a (3,1) code,
 // splitting k_check<6> +6.7% on the rate-0.1 QC lift of scripts/qc_probe.py)
 constexpr int kSplitMaxD = BPDEC_SPLIT_MAXD;
+constexpr int kCheckGrab = 1;     // k_check chunks per scheduler atomic (2: -9% on cfg2, the two
+                                  // chunks of a grab run back to back on one warp instead of side by side)
 constexpr int kTermBlocks = 16;   // k_decide q-reduction blocks per group (q partial tree: fixed by the code)
 
 // L2 residency hints (measured on cfg2, 384-slot stream, A/B of builds on
@@ -126,8 +128,6 @@ struct Args {
   int32_t ve_stride;        // k_var edge-id buffer size (32 x largest typed tile degree)
   const int32_t* vsched;    // [n_tiles] k_var hand-out order: generic tiles first, then by degree
   const int32_t* csched;    // [ceil(M/32)] k_check hand-out order: generic chunks first
-  const int4* csdesc;       // [ceil(M/32)] ctype in hand-out order, .x = chunk << 8 | (type & 0xff): one
-                            //  load per grab instead of the csched -> ctype chain
   // state
   int32_t G;
   float* llr_h;             // [G][NH][32]
@@ -306,9 +306,13 @@ __device__ __forceinline__ int sched_issue_n(const Args& a, int ctr, int lane, i
   return k;  // valid in lane 0 only
 }
 
-// The gi-th group (ascending) that has active slots, or -1 (gi uniform
-// across the warp).
-__device__ __forceinline__ int sched_group(const Args& a, int gi, int lane) {
+// k uniform across the warp
+__device__ __forceinline__ long long sched_map(const Args& a, int k, int lane, int per_group,
+                                               const int32_t* __restrict__ sched) {
+  const long long total = static_cast<long long>(a.G) * per_group;
+  int gi = k / per_group;
+  if (gi >= a.G) return total;
+  const int t = __ldg(&sched[k - gi * per_group]);
   for (int g0 = 0; g0 < a.G; g0 += 32) {
     const int g = g0 + lane;
     const uint32_t live = __ballot_sync(0xffffffffu, g < a.G && a.group_active[g] != 0u);
@@ -316,22 +320,11 @@ __device__ __forceinline__ int sched_group(const Args& a, int gi, int lane) {
     if (gi < n) {
       uint32_t m = live;
       for (int i = 0; i < gi; ++i) m &= m - 1;
-      return g0 + __ffs(m) - 1;
+      return static_cast<long long>(g0 + __ffs(m) - 1) * per_group + t;
     }
     gi -= n;
   }
-  return -1;
-}
-
-// k uniform across the warp
-__device__ __forceinline__ long long sched_map(const Args& a, int k, int lane, int per_group,
-                                               const int32_t* __restrict__ sched) {
-  const long long total = static_cast<long long>(a.G) * per_group;
-  const int gi = k / per_group;
-  if (gi >= a.G) return total;
-  const int t = __ldg(&sched[k - gi * per_group]);
-  const int g = sched_group(a, gi, lane);
-  return g < 0 ? total : static_cast<long long>(g) * per_group + t;
+  return total;
 }
 
 __device__ __forceinline__ long long sched_resolve(const Args& a, int k, int lane, int per_group,
@@ -525,35 +518,27 @@ __device__ __forceinline__ void check_magnitudes_d1(const float (&m)[NH + 1], fl
 // |l| >= clamp).  sl / so: sign bits of l and o.  Same decision as (l + o <
 // 0) except where |o| and |l| agree to float rounding (a posterior at zero:
 // a tie).
-__device__ __forceinline__ uint32_t d1_bit_phi(uint32_t ml, uint32_t mo, DSum s_hi, float phd, float phc) {
-  // ml / mo: sign masks (bit 31) of l and o.  Branch-free (selects only: the
-  // branchy form compiled to divergent branches and a convergence check
-  // before every ballot)
+__device__ __forceinline__ uint32_t d1_bit_phi(uint32_t sl, uint32_t so, DSum s_hi, float phd, float phc) {
+  // branch-free (selects only: the branchy form compiled to divergent
+  // branches and a convergence check before every ballot)
 #if BPDEC_PHI_DOMAIN
-  const uint32_t sl = ml >> 31, so = mo >> 31;
   const float kInf = __int_as_float(0x7f800000);
   const bool zero = (phd == kInf) & (s_hi == kInf);  // l = 0 and o = 0: +0 or -0, not < 0
   const bool o_lt = s_hi < phd;                      // phi(|o|) < phi(|l|)
   const bool o_gt = s_hi > phd;
+#else
+  // l = 0 (t = 1) and o = 0 (T_hi = 1, n == d exactly)
+  const bool zero = (phd == 1.0f) & (s_hi.n == s_hi.d);
+  const float r = phd * s_hi.d;  // T_hi = n / d against t(|l|): n against t*d
+  const bool o_lt = s_hi.n < r;
+  const bool o_gt = s_hi.n > r;
+#endif
   const bool l_small = phd > phc;       // |l| < clamp
   const bool o_big = l_small & o_lt;    // |o| > |l|
   const bool l_big = !l_small | o_gt;   // |l| > |o|  (neither: equal, post = +0)
   const uint32_t diff = o_big ? so : (l_big ? sl : 0u);
   const uint32_t same = zero ? 0u : sl;
   return sl == so ? same : diff;
-#else
-  // w = T_hi's numerator against t(|l|) * denominator: > 0 where |l| > |o|,
-  // < 0 where |o| > |l|, 0 where they agree (one fma: the sign of the exact
-  // difference).  It decides only where the signs differ and |l| < clamp, or
-  // where o = 0 (n == d: then w = d (1 - t(|l|)) >= 0, and 0 exactly for l =
-  // 0 — the +-0 posterior, not < 0); everywhere else l's sign stands (1.0).
-  // The bit is then sign(l) where w > 0, sign(o) where w < 0, 0 where w = 0:
-  // (w ^ sign(l)) < 0 as a float compare (-0 < 0 is false).
-  const float w = fmaf(-phd, s_hi.d, s_hi.n);
-  const bool decides = ((phd > phc) & (ml != mo)) | (s_hi.n == s_hi.d);
-  const float x = decides ? w : 1.0f;
-  return __uint_as_float(__float_as_uint(x) ^ ml) < 0.0f ? 1u : 0u;
-#endif
 }
 
 template <int MAXD, bool WANT_POST>
@@ -736,7 +721,7 @@ __device__ __forceinline__ void check_batch_issue(float* stage, const float* pos
 // edges are bit-identical to the plain path.
 template <int NH, int ND, bool WANT_POST, bool FM, int LW, bool PHID>
 __device__ __forceinline__ void check_batch_compute(const float* stage, float* c2vg, float* d1p, float* llrg,
-                                                    uint32_t* ssyn, int i0, int lane, bool act, bool first,
+                                                    const uint32_t* ssyn, int i0, int lane, bool act, bool first,
                                                     float cl, float clamp, float phc, uint32_t* synw,
                                                     uint32_t* d1w) {
   constexpr int D = NH + ND;
@@ -763,11 +748,8 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
   const float* sp = stage + f + q * NH * LW;                // posterior rows
   const float* sc = stage + f + (NPH + q * SH::CR) * LW;   // previous c2v rows (none with kConstC)
   const float* sl = stage + f + (NPH + NPC + q) * LW;      // degree-1 llr rows
-  // batch bases: the per-check offsets below are compile-time constants
-  // (immediate offsets of the stores instead of 64-bit adds per check)
-  float* cq = c2vg + q * NH * LW + static_cast<size_t>(i0 * NH) * LW;
-  float* dq = WANT_POST ? d1p + q * LW + static_cast<size_t>(i0) * LW : nullptr;
-  float* lq = llrg + static_cast<size_t>(i0) * LW;
+  float* cq = c2vg + q * NH * LW;
+  float* dq = WANT_POST ? d1p + q * LW : nullptr;
 #pragma unroll
   for (int kb = 0; kb < K; kb += FE) {
     float m[D > 0 ? D : 1];      // |v2c|, clamped (cl = inf in the first iteration)
@@ -775,13 +757,11 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
     float l = 0.0f;
     if (ND) l = sl[kb * LW];
     const int ci = i0 + kb + (qok ? q : 0);  // this lane's check (chunk-local)
-    // the check's target bit of this lane's frame, as a sign mask (one shift:
-    // the mask folds into the first xor)
-    const uint32_t spar = (ssyn[ci] << (31 - f)) & kSign;
+    const uint32_t sbit = (ssyn[ci] >> f) & 1u;
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const float c = kConstC ? __uint_as_float(__float_as_uint(fminf(fabsf(l), clamp)) |
-                                                (spar ^ (__float_as_uint(l) & kSign)))
+                                                ((sbit << 31) ^ (__float_as_uint(l) & kSign)))
                               : sc[(kb * NH + j) * LW];
       const float v = sp[(kb * NH + j) * LW] - (FM && first ? 0.0f : c);
       m[j] = fminf(fabsf(v), FM ? cl : clamp);
@@ -791,7 +771,7 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
       m[NH] = fminf(fabsf(l), FM ? cl : clamp);
       sm[NH] = __float_as_uint(l) & kSign;
     }
-    uint32_t par = spar;  // sign of the product times (1 - 2 s_c)
+    uint32_t par = sbit << 31;  // sign of the product times (1 - 2 s_c)
 #pragma unroll
     for (int j = 0; j < D; ++j) par ^= sm[j];
     float out[D > 0 ? D : 1];
@@ -807,17 +787,17 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
       }
       DSum s_hi;
       check_magnitudes_d1<NH>(m, phd, out, clamp, s_hi);
-      const uint32_t mo = par ^ sm[NH], ml = sm[NH];
+      const uint32_t so = (par ^ sm[NH]) >> 31, sl = sm[NH] >> 31;
       if (FM) {
         // first lanes: the plain decision on the LLR, and the phi of the
         // clamped magnitude written back for the steady state
         const float o = __uint_as_float(__float_as_uint(d1_out(s_hi, clamp)) | (par ^ sm[NH]));
         const uint32_t fb = (l + o < 0.0f) ? 1u : 0u;
-        dbit = first ? fb : d1_bit_phi(ml, mo, s_hi, phd, phc);
+        dbit = first ? fb : d1_bit_phi(sl, so, s_hi, phd, phc);
         const float stored = __uint_as_float(__float_as_uint(fabsf(l) > clamp ? phc : phf) | sm[NH]);
-        st_pred(lq + kb * LW, stored, on && first);
+        st_pred(llrg + static_cast<size_t>(i0 + kb) * LW, stored, on && first);
       } else {
-        dbit = d1_bit_phi(ml, mo, s_hi, phd, phc);
+        dbit = d1_bit_phi(sl, so, s_hi, phd, phc);
       }
       dbit = on ? dbit : 0u;
     } else {
@@ -826,28 +806,27 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const float o = __uint_as_float(__float_as_uint(out[j]) | (par ^ sm[j]));
-      if (!kConstC) stcs_pred(cq + (kb * NH + j) * LW, o, on);
+      if (!kConstC) stcs_pred(cq + static_cast<size_t>((i0 + kb) * NH + j) * LW, o, on);
     }
     if (ND && !kPhiD) {
       const float o = __uint_as_float(__float_as_uint(out[NH]) | (par ^ sm[NH]));
       const float pd = l + o;  // posterior of the degree-1 variable
       dbit = (on && pd < 0.0f) ? 1u : 0u;
-      if (WANT_POST) st_pred(dq + kb * LW, pd, on);
+      if (WANT_POST) st_pred(dq + static_cast<size_t>(i0 + kb) * LW, pd, on);
     }
     if constexpr (LW == 32) {
       // the syndrome word is the target word xor the degree-1 word (a
-      // ballot is linear over xor): one ballot per check, not two.  Lane 0
-      // parks the degree-1 word in the check's target-word slot (every lane
-      // read that slot before the ballot: its bit feeds dbit); the chunk
-      // loop's epilogue hands lane i check i's words (no per-check selects)
+      // ballot is linear over xor): one ballot per check, not two
+      uint32_t dw = 0u;
       if (ND) {
-        const uint32_t dw = __ballot_sync(0xffffffffu, dbit);
-        if (lane == 0) ssyn[ci] = dw;
+        dw = __ballot_sync(0xffffffffu, dbit);
+        if (lane == ci) *d1w = dw;
       }
+      if (lane == ci) *synw = ssyn[ci] ^ dw;
     } else {
       constexpr uint32_t kMask = (1u << LW) - 1u;
       const uint32_t bd = ND ? __ballot_sync(0xffffffffu, dbit) : 0u;
-      const uint32_t bs = __ballot_sync(0xffffffffu, qok && (((spar >> 31) ^ dbit) & 1u));
+      const uint32_t bs = __ballot_sync(0xffffffffu, qok && ((sbit ^ dbit) & 1u));
 #pragma unroll
       for (int qq = 0; qq < FE; ++qq) {
         if (lane == i0 + kb + qq) {
@@ -861,9 +840,8 @@ __device__ __forceinline__ void check_batch_compute(const float* stage, float* c
 
 template <int NH, int ND, bool WANT_POST, bool FM, int RING, int LW = 32, bool PHID = false>
 __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, int db, const int32_t* hh,
-                                                 uint32_t* ssyn, float* ring, int lane, bool act, bool first,
-                                                 uint32_t amask, uint32_t fmask, uint32_t sy_own, uint32_t* synw,
-                                                 uint32_t* d1w) {
+                                                 const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
+                                                 uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   constexpr bool kNoC = NH == 1 && ND == 1 && !FM;  // steady-state (1,1): no c2v rows staged
   using SH = CheckShape<NH, ND, RING, kNoC, LW>;
   constexpr int K = SH::K;
@@ -914,17 +892,6 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
     if (++slot_c == NS) slot_c = 0;
     __syncwarp();  // stage is refilled in the next round
   }
-  if constexpr (LW == 32) {
-    // lane i: check i's degree-1 word (parked in ssyn by lane 0) and its
-    // syndrome word = target word xor degree-1 word (sy_own: this lane's
-    // target word, loaded with the chunk's setup)
-    if (ND) {
-      *d1w = ssyn[lane];
-      *synw = sy_own ^ *d1w;
-    } else {
-      *synw = sy_own;
-    }
-  }
 }
 
 // SPLIT_FM: a separate steady-state copy (no first-iteration lanes) of the
@@ -934,20 +901,19 @@ __device__ __forceinline__ void check_chunk_loop(const Args& a, int g, int hb, i
 // is drained before a group is narrowed).
 template <int NH, int ND, bool WANT_POST, bool SPLIT_FM, int RING, int LW>
 __device__ __forceinline__ void check_chunk_typed(const Args& a, int g, int hb, int db, const int32_t* hh,
-                                                  uint32_t* ssyn, float* ring, int lane, bool act, bool first,
-                                                  uint32_t amask, uint32_t fmask, uint32_t sy_own, uint32_t* synw,
-                                                  uint32_t* d1w) {
+                                                  const uint32_t* ssyn, float* ring, int lane, bool act, bool first,
+                                                  uint32_t amask, uint32_t fmask, uint32_t* synw, uint32_t* d1w) {
   // the phi-domain degree-1 edge needs the steady-state copy (the general
   // copy would evaluate both forms: measured slower)
   if constexpr (LW < 32)
     check_chunk_loop<NH, ND, WANT_POST, false, RING, LW, SPLIT_FM>(a, g, hb, db, hh, ssyn, ring, lane, act, first,
-                                                                   amask, 0u, sy_own, synw, d1w);
+                                                                   amask, 0u, synw, d1w);
   else if (!SPLIT_FM || fmask)
     check_chunk_loop<NH, ND, WANT_POST, true, RING, 32, SPLIT_FM>(a, g, hb, db, hh, ssyn, ring, lane, act, first,
-                                                                  amask, fmask, sy_own, synw, d1w);
+                                                                  amask, fmask, synw, d1w);
   else
     check_chunk_loop<NH, ND, WANT_POST, false, RING, 32, SPLIT_FM>(a, g, hb, db, hh, ssyn, ring, lane, act, first,
-                                                                   amask, fmask, sy_own, synw, d1w);
+                                                                   amask, fmask, synw, d1w);
 }
 
 template <int MAXD>
@@ -976,49 +942,33 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
   const int wi = threadIdx.x >> 5;
   const bool moved = __ldcg(&a.counters[12]) != 0;
   const int chunks = (a.M + 31) / 32;
-  // dynamic chunk schedule (counters[7], generic chunks first): one chunk
-  // per atomic (two consecutive chunks on one warp measured 9 % slower than
-  // side by side on two warps; a static warp-strided assignment 23 % slower:
-  // chunk costs differ by type), two grabs in flight while the current chunk
-  // is processed (a steady-state (1,1) chunk is shorter than the atomic's
-  // round trip under load).  Grab k = chunk csdesc[k % chunks] of the
-  // (k / chunks)-th live group: the descriptor comes with one load.
-  int kp0 = sched_issue_n(a, 7, lane, 1);
-  int kp1 = sched_issue_n(a, 7, lane, 1);
-  int kp2 = sched_issue_n(a, 7, lane, 1);
-  int rot = 0;
-  int g = -1;
-  int4 cdk = make_int4(0, 0, 0, 0);
+  const long long total = static_cast<long long>(a.G) * chunks;
+  // dynamic chunk schedule (counters[7], generic chunks first): a grab is
+  // kCheckGrab consecutive chunks per atomic (1: two consecutive chunks on
+  // one warp measured 9 % slower than side by side on two warps; a static
+  // warp-strided assignment 23 % slower: chunk costs differ by type), the
+  // next grab in flight while the current one is processed
+  int kbase = __shfl_sync(0xffffffffu, sched_issue_n(a, 7, lane, kCheckGrab), 0);
+  int kpend = sched_issue_n(a, 7, lane, kCheckGrab);
+  int sub = 0;
   auto next_chunk = [&]() {
-    int k;
-    if (rot == 0) {
-      k = __shfl_sync(0xffffffffu, kp0, 0);
-      kp0 = sched_issue_n(a, 7, lane, 1);
-      rot = 1;
-    } else if (rot == 1) {
-      k = __shfl_sync(0xffffffffu, kp1, 0);
-      kp1 = sched_issue_n(a, 7, lane, 1);
-      rot = 2;
-    } else {
-      k = __shfl_sync(0xffffffffu, kp2, 0);
-      kp2 = sched_issue_n(a, 7, lane, 1);
-      rot = 0;
+    if (++sub == kCheckGrab) {
+      sub = 0;
+      kbase = __shfl_sync(0xffffffffu, kpend, 0);
+      kpend = sched_issue_n(a, 7, lane, kCheckGrab);
     }
-    const int gi = k / chunks;
-    g = -1;
-    if (gi < a.G) {
-      cdk = __ldg(&a.csdesc[k - gi * chunks]);
-      g = sched_group(a, gi, lane);
-    }
+    return sched_map(a, kbase + sub, lane, chunks, a.csched);
   };
-  next_chunk();
-  while (g >= 0) {
-    const int ch = cdk.x >> 8;
+  long long w = sched_map(a, kbase, lane, chunks, a.csched);
+  while (w < total) {
+    const int g = static_cast<int>(w / chunks);
+    const int ch = static_cast<int>(w - static_cast<long long>(g) * chunks);
     const int c0 = ch * 32;
     const int nc = min(32, a.M - c0);
     // the chunk's independent setup loads first (one round trip instead of
     // a chain: the slot iteration is loaded for every lane and masked, the
     // target syndrome word before the skip test)
+    const int4 cdk = __ldg(&a.ctype[ch]);
     const uint32_t amask = a.group_active[g];
     const int it_raw = a.slot_iter[g * kLanes + lane];
     const uint32_t sy = lane < nc ? a.syn_target[static_cast<size_t>(g) * a.M + c0 + lane] : 0u;
@@ -1026,12 +976,11 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
     const int it = act ? it_raw : 0;
     const bool first = (it == 1);
     const uint32_t fmask = __ballot_sync(0xffffffffu, act && first);
-    const int tx = cdk.x & 0xff;
-    const int type = kStage && tx != 0xff ? tx : -1;
+    const int type = kStage ? cdk.x : -1;
     // degree-1 checks only change in a frame's first iteration (and their
     // bit words must follow frames that k_compact moved)
     if ((type == 1 || type == 8) && fmask == 0u && !moved) {
-      next_chunk();
+      w = next_chunk();
       continue;
     }
     __syncwarp();
@@ -1055,7 +1004,7 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
   case NH_ * 8 + ND_:                                                                               \
     if (NH_ + ND_ <= MAXD)                                                                          \
       check_chunk_typed<NH_, ND_, WANT_POST, (MAXD <= kSplitMaxD), kRing, LW>(a, g, hb0, db0, s_hh[wi], s_syn[wi], s_ring[wi], \
-                                             lane, act, first, amask, fmask, sy, &synw, &d1w);      \
+                                             lane, act, first, amask, fmask, &synw, &d1w);          \
     else                                                                                            \
       typed = false;                                                                                \
     break;
@@ -1101,7 +1050,7 @@ __device__ __forceinline__ void check_body(const Args& a, CheckSmem<MAXD>& sm) {
       }
     }
     if (lane < nc) a.synp[static_cast<size_t>(g) * a.M + c0 + lane] = synw;
-    next_chunk();
+    w = next_chunk();
   }
 }
 
@@ -2865,12 +2814,6 @@ void GpuDecoder::init(const Code& code, int max_slots) {
       const int cls = x < 0 ? 0 : ((x == 1 || x == 8) ? 2 : 1);
       if (cls == pass) csched.push_back(static_cast<int32_t>(k));
     }
-  std::vector<int4> csdesc(csched.size());
-  for (size_t k = 0; k < csched.size(); ++k) {
-    int4 t = ctype[csched[k]];
-    t.x = (csched[k] << 8) | (t.x & 0xff);
-    csdesc[k] = t;
-  }
   const int64_t EH = static_cast<int64_t>(chk_hi_h.size());
   std::vector<int32_t> vptr(NV + 1, 0), vedge;
   vedge.reserve(EH);
@@ -2944,7 +2887,6 @@ void GpuDecoder::init(const Code& code, int max_slots) {
   a.cdev = up(cdev, static_cast<int32_t*>(nullptr));
   a.ctype = up(ctype, static_cast<int4*>(nullptr));
   a.csched = up(csched, static_cast<int32_t*>(nullptr));
-  a.csdesc = up(csdesc, static_cast<int4*>(nullptr));
   a.vtile = up(vtile, static_cast<int2*>(nullptr));
   a.vsched = up(vsched, static_cast<int32_t*>(nullptr));
   a.vedge_t = up(vedge_t, static_cast<int32_t*>(nullptr));

@@ -95,3 +95,70 @@ def test_fit_errors_reproduce(a_split):
     V = np.vstack([ws ** (k + 1) for k in range(4)]).T
     c, *_ = np.linalg.lstsq(V, h, rcond=None)
     assert np.max(np.abs(V @ c - h)) < 2e-8
+
+
+# ---- t domain (the shipped form; csrc/phi.cuh second half) -----------------
+def _f(x):
+    return np.asarray(x, dtype=np.float32)
+
+
+def t_emulated_outputs(m, clamp=np.float32(30.0)):
+    """float32 restatement of t_outputs<3, 3> (tdom, tf_pair, tmag) for
+    degree-3 checks: m[..., 3] magnitudes -> out[..., 3], exact exp2 / log2
+    standing in for MUFU.EX2 / MUFU.LG2."""
+    f = np.float32
+    with np.errstate(all="ignore"):
+        t = np.exp2(_f(m) * f(-1.4426950408889634)).astype(np.float32)
+        out = []
+        for a, b in ((1, 2), (0, 2), (0, 1)):
+            n = (t[..., a] + t[..., b]).astype(np.float32)
+            d = (t[..., a].astype(np.float64) * t[..., b].astype(np.float64) + 1.0).astype(np.float32)  # fma
+            mag = np.abs(((np.log2(d).astype(np.float32) - np.log2(n).astype(np.float32)).astype(np.float32)
+                          * f(0.6931471805599453)).astype(np.float32))
+            out.append(np.minimum(mag, clamp))
+    return np.stack(out, axis=-1)
+
+
+def exact_outputs(m, clamp=30.0):
+    m = np.asarray(m, dtype=np.float64)
+    th = np.tanh(m / 2)
+    out = []
+    for a, b in ((1, 2), (0, 2), (0, 1)):
+        # 2 atanh(x y) through log1p of the complementary product (exact near saturation)
+        ta, tb = np.exp(-m[..., a]), np.exp(-m[..., b])
+        T = (ta + tb) / (1 + ta * tb)
+        with np.errstate(divide="ignore"):
+            out.append(np.minimum(-np.log(T), clamp))
+    del th
+    return np.stack(out, axis=-1)
+
+
+def test_t_domain_accuracy_grid():
+    """The t-domain check update stays within 2e-6 (abs + rel) of the exact
+    value over magnitudes 0..30, including the saturation corner where the
+    float tanh form collapses."""
+    rng = np.random.default_rng(7)
+    m = np.concatenate([
+        rng.uniform(0, 30, size=(200000, 3)),
+        rng.uniform(0, 1e-3, size=(20000, 3)),
+        rng.uniform(25, 30, size=(20000, 3)),
+        np.array([[30, 30, 30], [0, 5, 7], [0, 0, 0], [30, 1e-6, 12], [20, 20, 20]], dtype=np.float64),
+    ]).astype(np.float32)
+    got = t_emulated_outputs(m).astype(np.float64)
+    want = exact_outputs(m.astype(np.float64))
+    err = np.abs(got - want) / (1.0 + np.abs(want))
+    assert err.max() < 2e-6, err.max()
+    # a zero input makes the other outputs exactly zero (tanh 0 = 0 in the reference)
+    z = t_emulated_outputs(_f([[0.0, 5.0, 7.0]]))
+    assert z[0, 1] == 0.0 and z[0, 2] == 0.0 and abs(z[0, 0] - exact_outputs([[0.0, 5.0, 7.0]])[0, 0]) < 1e-5
+
+
+def test_t_domain_beats_double_tanh_at_saturation():
+    """At (30, 30) the reference's double tanh/atanh form is 5.7e-6 off the
+    exact value; the float t domain is within 1e-6."""
+    m = _f([[30.0, 30.0, 30.0]])
+    got = float(t_emulated_outputs(m, clamp=np.float32(100.0))[0, 0])
+    exact = float(exact_outputs(m.astype(np.float64), clamp=100.0)[0, 0])
+    ref = float(2 * np.arctanh(np.tanh(15.0) * np.tanh(15.0)))
+    assert abs(got - exact) < 1e-6
+    assert abs(ref - exact) > 3e-6
