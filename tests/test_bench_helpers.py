@@ -52,3 +52,20 @@ def test_workload_beta_defaults():
     assert bench.workload_beta(ns("cfg5")) == (None, (0.92, 1.0))
     assert bench.workload_beta(ns("met")) == (0.87, None)       # inside the waterfall
     assert bench.workload_beta(ns("cfg2", 0.9)) == (0.9, None)
+
+
+def test_sweep_tables_render_committed_profiles():
+    """scripts/sweep_tables.py renders DESIGN.md's ET tables from the
+    committed sweep JSONs (one row per beta, FER / D-bar columns present)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prof = os.path.join(root, "profiles", "r2")
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "sweep_tables.py"),
+                          os.path.join(prof, "et_sweep_cfg2.json"), os.path.join(prof, "et_sweep_cfg5.json")],
+                         capture_output=True, text=True, check=True).stdout
+    rows = [l for l in out.splitlines() if l.startswith("| 0.") or l.startswith("| cfg5")]
+    assert len(rows) == 14 and "| 0.96 |" in out
+    met = subprocess.run([sys.executable, os.path.join(root, "scripts", "sweep_tables.py"), "--met",
+                          os.path.join(prof, "et_sweep_met.json")], capture_output=True, text=True, check=True).stdout
+    assert met.count("\n| 0.") == 8 and "beta_opt" in met
