@@ -41,7 +41,10 @@ def met_table(path):
         fer = " / ".join(f"{pol[k]['fer']:.3f}" if k in pol else "–" for k in ks)
         dec = f"{e(r['pce']['decoded_info_bits_per_s'])} / {e(r['vnr']['decoded_info_bits_per_s'])}"
         kr = {"250": r.get("k_vnr_over_k_pce250"), "500": r.get("k_vnr_over_k_pce"), "1000": r.get("k_vnr_over_k_pce1000")}
+        ci = r.get("k_vnr_over_k_pce_ci95")
         kk = " / ".join(("–" if kr.get(k) is None else f"{kr[k]:.2f}") for k in ("250", "500", "1000"))
+        if ci:
+            kk += f" (500: {ci[0]:.2f}–{ci[1]:.2f})"
         sd = " / ".join(f"{pol[k]['skr_dec_eq3']:.1f}" if k in pol else "–" for k in ("500", "1000", "vnr"))
         print(f"| {r['beta']:.3f} | {db} | {fer} | {dec} | {kk} | {sd} |")
     print("beta_opt:", json.dumps(d.get("beta_opt")))

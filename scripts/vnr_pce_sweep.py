@@ -20,6 +20,7 @@ import os
 import sys
 import time
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -50,6 +51,8 @@ class Acc:
         self.frames = self.errors = self.success = self.undetected = self.iters = 0
         self.seconds = 0.0
         self.stops = [0, 0, 0]
+        self.per_frame_it = []   # per-frame iterations / success, for the paired bootstrap of Eq. (2) ratios
+        self.per_frame_ok = []
 
     def add(self, cfg, out, x, dt):
         it = out["iterations"].cpu().numpy()
@@ -63,6 +66,8 @@ class Acc:
         self.errors += int(len(it) - success.sum())
         self.undetected += int(((rs == 0) & ~ok_bits).sum())
         self.iters += int(it.sum())
+        self.per_frame_it.append(it.astype(np.int64))
+        self.per_frame_ok.append(success.astype(np.int64))
         self.seconds += dt
         for k in range(3):
             self.stops[k] += int((rs == k).sum())
@@ -77,6 +82,26 @@ class Acc:
                 "edge_updates_per_s": self.iters * E / self.seconds,
                 "decoded_info_bits_per_s": self.success * (N - M) / self.seconds,
                 "processed_info_bits_per_s": self.frames * (N - M) / self.seconds}
+
+
+def k_ratio_ci(a_vnr, a_pce, n_boot=2000, seed=1):
+    """95 % interval of K_VNR / K_PCE (Eq. 2: K ~ (1 - FER) / D_bar) by a
+    paired bootstrap over frames: both policies decoded the same frames
+    (common random numbers), so frames are resampled jointly."""
+    iv, ov = np.concatenate(a_vnr.per_frame_it), np.concatenate(a_vnr.per_frame_ok)
+    ip, op = np.concatenate(a_pce.per_frame_it), np.concatenate(a_pce.per_frame_ok)
+    n = len(iv)
+    rng = np.random.default_rng(seed)
+    vals = []
+    for _ in range(n_boot):
+        idx = rng.integers(0, n, n)
+        sv, sp = ov[idx].sum(), op[idx].sum()
+        if sp == 0 or sv == 0:
+            continue
+        vals.append((ip[idx].sum() / iv[idx].sum()) * (sv / sp))
+    if len(vals) < n_boot // 2:
+        return None
+    return [float(np.percentile(vals, 2.5)), float(np.percentile(vals, 97.5))]
 
 
 def timed_decode(dec, cfg, llr, syn, out):
@@ -142,6 +167,7 @@ def main():
             if name.startswith("pce") and row[name]["fer"] < 1.0:
                 row[f"k_vnr_over_k_{name}"] = (row[name]["d_bar"] / row["vnr"]["d_bar"]) * \
                     (1.0 - row["vnr"]["fer"]) / (1.0 - row[name]["fer"])
+                row[f"k_vnr_over_k_{name}_ci95"] = k_ratio_ci(acc["vnr"], acc[name])
         # Eq. (1)-(3) at the paper's operating point (V_A such that I_AB =
         # R / beta; 80 km, eta 0.4, nu_el 0.01, xi 0.001, heterodyne,
         # N_privacy 1e8): SKR per pulse, K and SKR_dec per iteration latency,
