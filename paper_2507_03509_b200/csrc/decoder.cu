@@ -191,6 +191,7 @@ struct Args {
   uint8_t* ferr;              // [ring_cap] frame had a non-finite input LLR
 };
 
+constexpr int kAvailPieces = 8;        // a submitted batch's LLR upload is cut into at most this many pieces
 constexpr int kMaxStreamBatches = 32;  // batches in flight in stream mode (poll ring reports them)
 constexpr int kPollWords = 4 + kMaxStreamBatches;
 
@@ -3453,7 +3454,7 @@ struct GpuDecoder::Stream {
   double* r_q = nullptr;
   // pinned host staging
   int32_t* h_fbatch = nullptr;  // [cap]
-  int32_t* h_avail = nullptr;   // [kMaxStreamBatches]
+  int32_t* h_avail = nullptr;   // [kMaxStreamBatches][kAvailPieces]
   uint8_t* h_ferr = nullptr;    // [cap]
   Args a{};
   struct Batch {
@@ -3522,7 +3523,7 @@ void GpuDecoder::stream_open(const DecodeParams& p, bool packed, bool want_bits,
     CUDA_OK(cudaMemset(z.r_bdone, 0, kMaxStreamBatches * sizeof(int32_t)));
     CUDA_OK(cudaMemset(z.r_ferr, 0, C));
     CUDA_OK(cudaHostAlloc(&z.h_fbatch, C * sizeof(int32_t), cudaHostAllocDefault));
-    CUDA_OK(cudaHostAlloc(&z.h_avail, kMaxStreamBatches * sizeof(int32_t), cudaHostAllocDefault));
+    CUDA_OK(cudaHostAlloc(&z.h_avail, kMaxStreamBatches * kAvailPieces * sizeof(int32_t), cudaHostAllocDefault));
     CUDA_OK(cudaHostAlloc(&z.h_ferr, C, cudaHostAllocDefault));
     for (auto& bt : z.batches) CUDA_OK(cudaEventCreateWithFlags(&bt.ev, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreate(&z.t_first));
@@ -3619,10 +3620,8 @@ int64_t GpuDecoder::stream_submit(int32_t n, const float* llr, const uint32_t* s
   if (n2) CUDA_OK(cudaMemcpyAsync(z.r_fbatch, z.h_fbatch, n2 * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
   fill(z.r_ferr, 1, 0);
   if (z.want_q) fill(z.r_q, z.p.d_max * sizeof(double), 0xff);  // NaN past the stop
-  rows(z.r_llr, llr, base.N);
   if (syn) rows(z.r_syn, syn, base.MW);
   else fill(z.r_syn, base.MW * sizeof(uint32_t), 0);
-  z.h_avail[slot] = static_cast<int32_t>(g0 + n);
   {
     std::lock_guard<std::mutex> lk(z.mu);
     Stream::Batch& bt = z.batches[slot];
@@ -3640,8 +3639,27 @@ int64_t GpuDecoder::stream_submit(int32_t n, const float* llr, const uint32_t* s
     z.next_g = g0 + n;
     ++z.decoding;
   }
-  // the frames become available once their rows have landed
-  CUDA_OK(cudaMemcpyAsync(base.counters + 9, z.h_avail + slot, sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+  // the LLR rows in up to kAvailPieces pieces (whole 32-frame groups), each
+  // followed by the advance of the frames-available counter: the first
+  // group of a batch starts decoding while the rest is still uploading
+  // (the start-up of a stream: one 276 MB cfg2 batch is ~5 ms of PCIe time)
+  const size_t wN = static_cast<size_t>(base.N);
+  const int piece = std::max(32, ((n + kAvailPieces - 1) / kAvailPieces + 31) / 32 * 32);
+  int pi = 0;
+  for (int i0 = 0; i0 < n; i0 += piece, ++pi) {
+    const size_t cnt = static_cast<size_t>(std::min(piece, n - i0));
+    const size_t q0 = (p0 + static_cast<size_t>(i0)) % C;
+    const size_t m1 = std::min(cnt, C - q0);
+    CUDA_OK(cudaMemcpyAsync(z.r_llr + q0 * wN, llr + static_cast<size_t>(i0) * wN, m1 * wN * sizeof(float),
+                            cudaMemcpyDefault, cs));
+    if (cnt > m1)
+      CUDA_OK(cudaMemcpyAsync(z.r_llr, llr + (static_cast<size_t>(i0) + m1) * wN, (cnt - m1) * wN * sizeof(float),
+                              cudaMemcpyDefault, cs));
+    int32_t* ha = z.h_avail + slot * kAvailPieces + pi;
+    *ha = static_cast<int32_t>(g0 + i0 + static_cast<int64_t>(cnt));
+    // the frames become available once their rows have landed
+    CUDA_OK(cudaMemcpyAsync(base.counters + 9, ha, sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+  }
   z.cv_work.notify_one();
   return t;
 }
