@@ -4,6 +4,8 @@
 random LLR mixtures (punctured zeros, values beyond the clamp), random
 D_max / ET mode / message clamp / slot count / batch — the CUDA decoder
 against the compiled reference with the tie rule of tests/_parity.py."""
+import os
+
 import numpy as np
 import pytest
 
@@ -43,7 +45,8 @@ def _random_llr(rng, frames, n, clamp):
     return llr.astype(np.float32)
 
 
-@pytest.mark.parametrize("seed", range(24))
+# BPDEC_FUZZ_SEEDS=<n> widens the sweep (profiles/r2/fuzz_extended.md: 300 seeds)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("BPDEC_FUZZ_SEEDS", "24"))))
 def test_random_codes_vs_reference(P, ref, seed):
     rng = np.random.default_rng(1000 + seed)
     code = _random_code(P, rng)
