@@ -3646,6 +3646,7 @@ int64_t GpuDecoder::stream_submit(int32_t n, const float* llr, const uint32_t* s
   const size_t wN = static_cast<size_t>(base.N);
   const int piece = std::max(32, ((n + kAvailPieces - 1) / kAvailPieces + 31) / 32 * 32);
   int pi = 0;
+  try {
   for (int i0 = 0; i0 < n; i0 += piece, ++pi) {
     const size_t cnt = static_cast<size_t>(std::min(piece, n - i0));
     const size_t q0 = (p0 + static_cast<size_t>(i0)) % C;
@@ -3659,6 +3660,15 @@ int64_t GpuDecoder::stream_submit(int32_t n, const float* llr, const uint32_t* s
     *ha = static_cast<int32_t>(g0 + i0 + static_cast<int64_t>(cnt));
     // the frames become available once their rows have landed
     CUDA_OK(cudaMemcpyAsync(base.counters + 9, ha, sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+  }
+  } catch (const std::exception& e) {
+    // the batch is registered but its frames can no longer all arrive: the
+    // stream is unusable (waits and later submits fail instead of hanging)
+    std::lock_guard<std::mutex> lk(z.mu);
+    z.fatal = std::string("stream submit: ") + e.what();
+    z.cv_done.notify_all();
+    z.cv_work.notify_all();
+    throw;
   }
   z.cv_work.notify_one();
   return t;
